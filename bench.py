@@ -1,0 +1,416 @@
+#!/usr/bin/env python3
+"""Benchmark: product time and output Gbit/s of the dense Z[y] multiply on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+Metric (BASELINE.json): "product time (ms) & output Gbit/s, dxN-bit Z[x]
+multiply"; `value` is output Gbit/s = rows*out_bits/1e9 per product / time.
+Workload: BASELINE config C2 (d=8192, N=8192-bit signed; configs[1]), seeded
+synthetic inputs (paper_1612_05778_b200/workloads.py), the same arrays the
+reference hashes in tests/golden/configs.json.
+
+* value      device-resident: inputs already in HBM, output left in HBM; each
+             step = device width scan + host plan + every kernel, timed with
+             CUDA events on the library's stream, L2 flushed (256 MiB memset)
+             before every step outside the timed region.
+* e2e        the public API `multiply(MulRequest(a, b))` on pinned host arrays:
+             H2D of both operands, all kernels and D2H of the product inside the
+             timed region (wall clock around the synchronous call).
+* roofline   the dominant stage of the device-resident step: algorithmic bytes
+             (HBM) and radix-2 butterflies (INT pipe) per launch / its event
+             time, against MEASURED_PEAKS.json's HBM copy bandwidth and the
+             butterfly peak measured live by tc_int_peak.
+* cpu_baseline  the CPU oracle (oracle/, a C restatement of the reference's
+             numba kernels) on this host, all cores, one full C2 product.
+
+`--impl reference` times that same CPU restatement as the reference arm.
+N > 1 (torchrun): every rank runs its own product on its own GPU (replicas,
+weak scaling; no collective on the data path in this round), max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "product time (ms) & output Gbit/s, dxN-bit Z[x] multiply, at 1/2/4/8 B200"
+
+
+def _dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def stage_model(plan, da, db, a_cw, b_cw, out_cw):
+    """Algorithmic bytes and butterflies of each pipeline stage."""
+    P, L, s_y = plan.P, plan.L, plan.s_y
+    S = s_y * L
+    lgL = L.bit_length() - 1
+    lgS = s_y.bit_length() - 1
+    rows = da + db - 1
+    U = 9
+    npass = 0 if lgS == 0 else -(-lgS // U)
+    sizes = []
+    if npass:
+        base, extra = lgS // npass, lgS % npass
+        sizes = [base + (1 if i < extra else 0) for i in range(npass)]
+    u_last = sizes[-1] if sizes else 0
+    st = {}
+    st["convert"] = dict(bytes=(da * a_cw + db * b_cw) * 8 + (da + db) * L * 4 * P,
+                         bfly=(da + db) * P * (L // 2) * lgL)
+    fwd_b, fwd_f = 0, 0
+    for op_d, count in ((da, npass), (db, max(npass - 1, 0))):
+        for i in range(count):
+            fwd_b += 4 * P * ((op_d * L if i == 0 else S) + S)
+            fwd_f += P * (S // 2) * sizes[i]
+    st["ntt_forward"] = dict(bytes=fwd_b, bfly=fwd_f)
+    st["pointwise"] = dict(bytes=4 * P * (3 * S if npass > 1 else (db * L + 2 * S)),
+                           bfly=2 * P * (S // 2) * u_last)
+    inv_b = 0
+    for i in range(npass - 1):
+        inv_b += 4 * P * (S + (rows * L if i == 0 else S))
+    inv_b += 2 * 4 * P * rows * L
+    st["ntt_inverse"] = dict(bytes=inv_b, bfly=P * (S // 2) * (lgS - u_last) + P * rows * (L // 2) * lgL)
+    st["recover"] = dict(bytes=4 * P * rows * (L - 1) + 8 * rows * out_cw, bfly=0)
+    return st
+
+
+def run_ours(args, rank, world, local):
+    import ctypes
+    import paper_1612_05778_b200 as tc
+    from paper_1612_05778_b200 import _lib, workloads
+    from paper_1612_05778_b200.params import plan_gpu
+    from paper_1612_05778_b200.zpoly import output_bit_width
+
+    ctx = _lib.context(local)
+    lib, h = ctx.lib, ctx.handle
+    (aw, ab), (bw, bb) = workloads.make_inputs(args.config)
+    da, db = aw.shape[0], bw.shape[0]
+    rows = da + db - 1
+
+    # device-resident copies
+    def dalloc(nbytes):
+        p = ctypes.c_void_p()
+        _lib.check(lib.tc_device_alloc(h, nbytes, ctypes.byref(p)), "tc_device_alloc")
+        return p
+
+    d_a, d_b = dalloc(aw.nbytes), dalloc(bw.nbytes)
+    _lib.check(lib.tc_memcpy(h, d_a, _lib.ptr(aw), aw.nbytes, 1), "H2D")
+    _lib.check(lib.tc_memcpy(h, d_b, _lib.ptr(bw), bw.nbytes, 1), "H2D")
+    info = _lib.TcInputInfo()
+    _lib.check(lib.tc_stage_inputs(h, d_a, da, aw.shape[1], d_b, db, bw.shape[1], 1,
+                                   ctypes.byref(info)), "stage")
+    n_in = max(info.n_in_a, info.n_in_b)
+    out_bits = output_bit_width(max(da, db), n_in)
+    out_cw = -(-out_bits // 64)
+    d_out = dalloc(rows * out_cw * 8)
+
+    def resident_step():
+        inf = _lib.TcInputInfo()
+        _lib.check(lib.tc_stage_inputs(h, d_a, da, aw.shape[1], d_b, db, bw.shape[1], 1,
+                                       ctypes.byref(inf)), "stage")
+        plan = plan_gpu(max(da, db), min(da, db), max(inf.n_in_a, inf.n_in_b))
+        err = ctypes.c_int64(-1)
+        rc = lib.tc_execute(h, ctypes.byref(_lib.make_plan(plan)), ab, bb, d_out, rows, out_cw, 1,
+                            None, ctypes.byref(err))
+        _lib.check(rc, "tc_execute")
+        return plan
+
+    # correctness gate (like tc/bench.py:110-125): no timing without parity
+    plan = resident_step()
+    host_out = np.empty((rows, out_cw), dtype=np.uint64)
+    _lib.check(lib.tc_memcpy(h, _lib.ptr(host_out), d_out, host_out.nbytes, 2), "D2H")
+    golden = json.load(open(os.path.join(ROOT, "tests", "golden", "configs.json"))).get(args.config)
+    verified = None
+    if golden:
+        verified = (workloads.words_sha256(host_out) == golden["out_sha256"]
+                    and out_bits == golden["out_bits"])
+        if not verified:
+            raise SystemExit(f"bench: product mismatch vs the reference hash for {args.config}")
+
+    def step_timed(fn):
+        _lib.check(lib.tc_flush_l2(h), "flush")
+        _lib.check(lib.tc_record_event(h, 0), "event")
+        fn()
+        _lib.check(lib.tc_record_event(h, 1), "event")
+        ms = ctypes.c_float()
+        _lib.check(lib.tc_event_elapsed(h, 0, 1, ctypes.byref(ms)), "elapsed")
+        return ms.value
+
+    for _ in range(args.warmup):
+        step_timed(resident_step)
+    _barrier(world)
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = ctx.launches()
+    times = [step_timed(resident_step) for _ in range(args.steps)]
+    launches = ctx.launches() - l0
+    # per-stage profile of one more step (same work) for the roofline
+    prof = (ctypes.c_double * 8)()
+    lib.tc_last_profile(h, prof, None)
+    clock_info = clocks.stop()
+    dev_ms = float(np.sum(times))
+    dev_ms_max = _max_over_ranks(dev_ms, world)
+
+    # end to end through the public API from pinned host memory
+    pa = _lib.pinned.empty(aw.shape, np.uint64)
+    pb = _lib.pinned.empty(bw.shape, np.uint64)
+    pa[...] = aw
+    pb[...] = bw
+    A = tc.IntPolynomial._trusted(pa, ab)
+    B = tc.IntPolynomial._trusted(pb, bb)
+    for _ in range(args.warmup):
+        _lib.check(lib.tc_flush_l2(h), "flush")
+        lib.tc_synchronize(h)
+        tc.multiply(tc.MulRequest(A, B))
+    e2e = []
+    for _ in range(args.steps):
+        _lib.check(lib.tc_flush_l2(h), "flush")
+        lib.tc_synchronize(h)
+        t0 = time.perf_counter()
+        prod = tc.multiply(tc.MulRequest(A, B))
+        e2e.append(time.perf_counter() - t0)
+        del prod
+    e2e_s = _max_over_ranks(float(np.sum(e2e)), world)
+
+    out_gbit = rows * out_bits / 1e9
+    value = world * args.steps * out_gbit / (dev_ms_max / 1e3)
+    e2e_value = world * args.steps * out_gbit / e2e_s
+
+    # roofline of the dominant stage
+    peaks = _peaks()
+    bfly_peak = ctypes.c_double()
+    mont_peak = ctypes.c_double()
+    lib.tc_int_peak(h, ctypes.byref(bfly_peak), ctypes.byref(mont_peak))
+    model = stage_model(plan, da, db, aw.shape[1], bw.shape[1], out_cw)
+    names = ["convert", "ntt_forward", "pointwise", "ntt_inverse", "recover"]
+    stage_ms = dict(zip(names, list(prof)[:5]))
+    stages = {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    for n in names:
+        ms = stage_ms[n]
+        m = model[n]
+        gbs = m["bytes"] / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+        gbf = m["bfly"] / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+        stages[n] = dict(ms=round(ms, 4), GBps=round(gbs, 1), hbm_frac=round(gbs / hbm_peak, 3),
+                         Gbfly_s=round(gbf, 1),
+                         int_frac=round(gbf / (bfly_peak.value / 1e9), 3) if bfly_peak.value else None)
+    dom = max(names, key=lambda n: stage_ms[n])
+    ds = stages[dom]
+    if (ds["int_frac"] or 0) >= ds["hbm_frac"]:
+        roof = {"bound": "int", "achieved": ds["Gbfly_s"], "peak": round(bfly_peak.value / 1e9, 1),
+                "unit": "Gbutterfly/s", "frac": ds["int_frac"]}
+    else:
+        roof = {"bound": "hbm", "achieved": ds["GBps"], "peak": hbm_peak, "unit": "GB/s",
+                "frac": ds["hbm_frac"]}
+    roof.update({"kernel": dom, "traffic": None,
+                 "peak_source": "hbm: MEASURED_PEAKS.json hbm_gbs (measured); int: tc_int_peak "
+                                "register-only butterfly chain, measured live",
+                 "stages": stages})
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "Gbit/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dev_ms_max / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded PCG64, BASELINE.md section 4 recipe)",
+        "config": {"workload": f"{args.config}: {workloads.CONFIGS[args.config].text}",
+                   "d": max(da, db), "N": workloads.CONFIGS[args.config].N,
+                   "rows": rows, "out_bits": out_bits,
+                   "plan": plan.describe(), "parallelism": f"replicas x{world}",
+                   "l2": "flushed (256 MiB memset) before every timed step",
+                   "verified_vs_reference_sha256": verified},
+        "e2e": {"value": round(e2e_value, 3), "unit": "Gbit/s",
+                "ms_per_step": round(1e3 * e2e_s / args.steps, 4),
+                "h2d_bytes_per_step": int(aw.nbytes + bw.nbytes),
+                "d2h_bytes_per_step": int(rows * out_cw * 8),
+                "api": "paper_1612_05778_b200.multiply(MulRequest) on pinned host arrays"},
+        "roofline": roof,
+        "gpu_launches": int(launches),
+        "int_peak": {"butterflies_per_s": bfly_peak.value, "montmul_per_s": mont_peak.value},
+        "clocks": clock_info,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.config, aw, ab, bw, bb, out_gbit, samples=1)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(config, aw, ab, bw, bb, out_gbit, samples=1):
+    """The oracle (C restatement of the reference kernels) on this host's cores."""
+    from oracle import port
+    threads = os.cpu_count() or 1
+    port.multiply_words(aw[:64], ab, bw[:64], bb, threads=threads)   # warm tables / pages
+    ts = []
+    for _ in range(samples):
+        t0 = time.perf_counter()
+        port.multiply_words(aw, ab, bw, bb, threads=threads)
+        ts.append(time.perf_counter() - t0)
+    t = float(np.median(ts))
+    return {"value": round(out_gbit / t, 4), "unit": "Gbit/s", "cores": threads, "kind": "port",
+            "ms_per_product": round(t * 1e3, 1),
+            "sample": f"{samples} full {config} product(s) (reference algorithm: 63-bit primes, P=2, "
+                      f"reference plan), OpenMP over all host threads"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import port
+    from paper_1612_05778_b200 import workloads
+    (aw, ab), (bw, bb) = workloads.make_inputs(args.config)
+    threads = os.cpu_count() or 1
+    rows = aw.shape[0] + bw.shape[0] - 1
+    out_bits = port.product_bit_width(aw, bw)
+    out_gbit = rows * out_bits / 1e9
+    for _ in range(args.warmup):
+        port.multiply_words(aw, ab, bw, bb, threads=threads)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        port.multiply_words(aw, ab, bw, bb, threads=threads)
+        ts.append(time.perf_counter() - t0)
+    tot = float(np.sum(ts))
+    value = args.steps * out_gbit / tot
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "Gbit/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded PCG64, BASELINE.md section 4 recipe)",
+        "config": {"workload": f"{args.config}: {workloads.CONFIGS[args.config].text}",
+                   "parallelism": "CPU, all host threads"},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(value, 4), "unit": "Gbit/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} full {args.config} products, oracle/ C restatement "
+                                   f"of the reference kernels (the reference is pure Python/numba "
+                                   f"and is not present on the GPU box)"},
+        "e2e": {"value": round(value, 4), "unit": "Gbit/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+_dist_ready = False
+
+
+def _init_dist(world, local):
+    global _dist_ready
+    if world > 1 and not _dist_ready:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+        _dist_ready = True
+
+
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def _max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    rank, world, local = _dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    _init_dist(world, local)
+    run_ours(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

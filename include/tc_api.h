@@ -1,0 +1,175 @@
+/*
+ * tc_api.h -- C-ABI of libtcgpu.so, the B200 (sm_100a) implementation of the
+ * dense Z[y] product of arXiv 1612.05778 ("two-convolution" method).
+ *
+ * This is the drop-in boundary for the reference package `twoconv`
+ * (/root/reference/pkg/src/twoconv, `tc/` below).  The reference has no FFI;
+ * its operator API is the Python pair tc/multiplier.py:169-181
+ * (`multiply`, `multiply_with_stats`).  The Python package
+ * `paper_1612_05778_b200` keeps those names and binds the functions below
+ * through ctypes.  Signatures use only plain pointers,
+ * sizes and POD structs: no torch types.
+ *
+ * Data layout at the boundary (tc/zpoly.py:1-6, 32-48): a polynomial of d
+ * coefficients is a row-major (d, cw) array of uint64 limbs, little-endian
+ * two's complement, every coefficient sign-extended across its cw limbs.
+ *
+ * Ownership: the caller owns every host buffer and every device buffer it
+ * passes in; a context owns its device scratch (grids, twiddle tables, staged
+ * inputs) and its CUDA stream.  Calls on one context are serialised by the
+ * caller; distinct contexts are independent and may be used from different
+ * threads concurrently (the reference promises concurrent `multiply`,
+ * SPEC.md "multiply is safe to call concurrently").
+ *
+ * Status codes (returned by every int function; mapped onto tc/errors.py by
+ * the Python layer):
+ */
+#ifndef TC_API_H
+#define TC_API_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TC_OK            0
+#define TC_ERR_ENCODING  1  /* EncodingError: top digit overflow; err_index = first row (tc/codec.py:92-98) */
+#define TC_ERR_BOUND     2  /* CorruptedConvolutionError: CRT bound breach; err_index = i*(2K)+j (tc/multiplier.py:59-63) */
+#define TC_ERR_PARITY    3  /* CorruptedConvolutionError: odd combination; err_index = row (tc/multiplier.py:156-160) */
+#define TC_ERR_BAD_ARG   4  /* ValueError */
+#define TC_ERR_CUDA      5  /* RuntimeError, message via tc_last_error() */
+#define TC_ERR_RANGE     7  /* EncodingError: coefficient outside the plan's N-bit range (tc/codec.py:78-83) */
+#define TC_ERR_EMPTY     8  /* EmptyInputError: a zero polynomial (tc/params.py:288-289) */
+
+#define TC_MAX_PRIMES 16
+
+/*
+ * One multiplication plan, produced by the host planner
+ * (paper_1612_05778_b200/params.py; replaces MulPlan, tc/params.py:62-79).
+ * The GPU path computes ONE acyclic 2-D convolution of size s_y x 2K per
+ * prime; its first x-stage is the paper's theta twist, so the two halves of
+ * the x-spectrum are the cyclic (C^-) and negacyclic (C^+) convolutions of
+ * tc/ntt2d.py:128-135.
+ */
+typedef struct {
+    int64_t d;        /* max(da, db)                                          */
+    int64_t N;        /* padded coefficient width, N = K*M                    */
+    int64_t K;        /* digits per coefficient, power of two, 1 <= K <= 2^14 */
+    int64_t M;        /* digit width in bits, 2 <= M <= 63                    */
+    int64_t s_y;      /* least power of two >= 2d-1                           */
+    int32_t P;        /* number of word primes, 1..TC_MAX_PRIMES              */
+    int32_t flags;    /* reserved, 0                                          */
+    uint32_t p[TC_MAX_PRIMES];  /* primes p < 2^30, 2^k | p-1, 2^k >= max(s_y, 2K) */
+    uint32_t g[TC_MAX_PRIMES];  /* a primitive root of each p                       */
+} tc_plan_t;
+
+/* StageTimings (tc/multiplier.py:41-56), seconds, measured with CUDA events. */
+typedef struct {
+    double convert;      /* H2D of inputs + ConvertIn fused with the x-direction forward NTT */
+    double ntt_forward;  /* y-direction forward passes (operand A complete, B up to its last pass) */
+    double pointwise;    /* fused last forward pass of B + pointwise product + first inverse pass */
+    double ntt_inverse;  /* remaining inverse y passes + inverse x-direction NTT */
+    double crt;          /* 0: CRT is fused into ConvertOut (reported under `recover`) */
+    double recover;      /* fused CRT + ConvertOut carry scan + D2H of the product */
+    double total;        /* whole call, wall clock */
+    int32_t gpus;        /* GPUs used by this call */
+} tc_times_t;
+
+typedef struct {
+    int32_t n_in_a, n_in_b;        /* max two's-complement width (tc/params.py:183-185) */
+    int32_t nonzero_a, nonzero_b;  /* any non-zero coefficient (tc/zpoly.py:71-72)       */
+} tc_input_info_t;
+
+/* Context: one CUDA device + stream + scratch.  device < 0 selects the current device. */
+int tc_ctx_create(int device, void** ctx);
+int tc_ctx_destroy(void* ctx);
+
+/* Copy (or, with on_device != 0, adopt) both operands and reduce their widths
+ * on the device.  Replaces the Python-int scans of tc/params.py:290-293 and
+ * tc/zpoly.py:103-114.  Device pointers must stay valid until tc_execute
+ * returns. */
+int tc_stage_inputs(void* ctx,
+                    const uint64_t* a, int64_t da, int32_t a_cw,
+                    const uint64_t* b, int64_t db, int32_t b_cw,
+                    int32_t on_device, tc_input_info_t* info);
+
+/* Run the product of the staged inputs under `plan` (replaces
+ * tc/multiplier.py:131-166 after planning).  `out` is (rows, out_cw) with
+ * rows = da+db-1; it is a host pointer unless out_on_device != 0.  a_bits /
+ * b_bits are the declared bit widths (only consulted for the N-bit range
+ * check of tc/codec.py:78-83).  times may be NULL. */
+int tc_execute(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32_t b_bits,
+               uint64_t* out, int64_t rows, int32_t out_cw, int32_t out_on_device,
+               tc_times_t* times, int64_t* err_index);
+
+/* Convenience: tc_stage_inputs + tc_execute with a caller-made plan. */
+int tc_multiply(void* ctx,
+                const uint64_t* a, int64_t da, int32_t a_cw, int32_t a_bits,
+                const uint64_t* b, int64_t db, int32_t b_cw, int32_t b_bits,
+                const tc_plan_t* plan,
+                uint64_t* out, int64_t rows, int32_t out_cw,
+                tc_times_t* times, int64_t* err_index);
+
+/* ---- parity seams (device code shared with the fused product path) ---- */
+
+/* Balanced digits of the staged operand `which` (0 = a, 1 = b) under (K, M, N)
+ * into host int64 (d, K): bit-identical to digits_rows (tc/_kernels.py:78-119)
+ * via bivariate_representation (tc/codec.py:71-99).  Returns TC_ERR_ENCODING /
+ * TC_ERR_RANGE with err_index = first bad row. */
+int tc_digits(void* ctx, int32_t which, int64_t K, int64_t M, int64_t N, int32_t in_bits,
+              int64_t* digits_out, int64_t* err_index);
+
+/* Exact bivariate product coefficients c_{i,j}, i < rows, j < 2K, of the
+ * staged operands, as (rows, 2K, P) uint32 two's-complement limbs
+ * (P*32 bits each).  Folding c_{i,j} -+ c_{i,j+K} gives the reference's
+ * C^-/C^+ (tc/multiplier.py:142-147, tc/codec.py:102-121). */
+int tc_bivariate_product(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32_t b_bits,
+                         uint32_t* coeffs_out, int64_t rows, int64_t* err_index);
+
+/* Batched device modular products through the kernels' own arithmetic:
+ * mode 0: Shoup a*b mod p with b fixed per element (twiddle path);
+ * mode 1: Montgomery a*b*2^-32 mod p (pointwise path), canonical results.
+ * Known-answer hook in the role of mont_mul_probe (tc/_kernels.py:52-55). */
+int tc_modmul_probe(uint32_t p, const uint32_t* a, const uint32_t* b, uint32_t* out,
+                    int64_t n, int32_t mode);
+
+/* One length-n (power of two) NTT over p on the device, the building block of
+ * every pass (role of ntt_inplace, tc/ntt2d.py:44-71): dir 0 = forward DIF
+ * (natural -> bit-reversed), dir 1 = inverse DIT including the 1/n scaling. */
+int tc_ntt_probe(uint32_t p, uint32_t g, uint32_t* data, int64_t n, int32_t dir);
+
+/* Device memory helpers for device-resident callers (bench, tests). */
+int tc_device_alloc(void* ctx, int64_t bytes, void** dptr);
+int tc_device_free(void* ctx, void* dptr);
+int tc_memcpy(void* ctx, void* dst, const void* src, int64_t bytes, int32_t kind); /* 1 H2D, 2 D2H, 3 D2D */
+int tc_synchronize(void* ctx);
+
+/* Pinned host memory (for the end-to-end path's H2D/D2H). */
+int tc_host_alloc(int64_t bytes, void** hptr);
+int tc_host_free(void* hptr);
+
+/* Device-side timing on the context's stream: record into slot 0..15, read
+ * the elapsed milliseconds between two recorded slots (synchronises). */
+int tc_record_event(void* ctx, int32_t slot);
+int tc_event_elapsed(void* ctx, int32_t s0, int32_t s1, float* ms);
+/* Overwrite a 256 MiB scratch buffer so the next step starts with a cold L2. */
+int tc_flush_l2(void* ctx);
+/* INT-pipe roofline denominator: sustained DIF butterflies/s (Shoup, p < 2^30)
+ * of a register-only chain over every SM, and of the Montgomery product. */
+int tc_int_peak(void* ctx, double* butterflies_per_s, double* montmul_per_s);
+
+/* Launch counter: kernels this context launched since creation. */
+int64_t tc_kernel_launches(void* ctx);
+/* Average duration (ms) of the dominant kernel class recorded by the last
+ * tc_execute with profiling enabled, plus its algorithmic bytes per launch. */
+int tc_set_profiling(void* ctx, int32_t enable);
+int tc_last_profile(void* ctx, double* ms_by_stage /* 8 */, int64_t* launches_by_stage /* 8 */);
+
+const char* tc_last_error(void);
+const char* tc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TC_API_H */

@@ -1,0 +1,814 @@
+// tc_api.cu -- C-ABI of libtcgpu.so (declared in include/tc_api.h).
+//
+// Host orchestration of the two-convolution product on one B200:
+//   stage inputs -> width scan (device) -> [host planner] ->
+//   ConvertIn+x-NTT (A, B) -> y passes -> fused pointwise pass -> inverse y
+//   passes -> inverse x-NTT -> fused CRT + ConvertOut -> product words.
+// Replaces _run_pipeline (tc/multiplier.py:131-166) after `build_plan`.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdarg.h>
+#include <string.h>
+#include <climits>
+#include <string>
+#include <vector>
+#include <chrono>
+
+#include "../../include/tc_api.h"
+#include "tc_kernels.cuh"
+
+using namespace tc;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_err(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int set_err(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+#define CK(call)                                                                      \
+    do {                                                                              \
+        cudaError_t e_ = (call);                                                      \
+        if (e_ != cudaSuccess)                                                        \
+            return set_err(TC_ERR_CUDA, "%s failed: %s (%s:%d)", #call,              \
+                           cudaGetErrorString(e_), __FILE__, __LINE__);               \
+    } while (0)
+
+#define CKL()                                                                         \
+    do {                                                                              \
+        cudaError_t e_ = cudaGetLastError();                                          \
+        if (e_ != cudaSuccess)                                                        \
+            return set_err(TC_ERR_CUDA, "kernel launch failed: %s (%s:%d)",          \
+                           cudaGetErrorString(e_), __FILE__, __LINE__);               \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    int ensure(size_t bytes) {
+        if (bytes <= n) return TC_OK;
+        if (p) cudaFree(p);
+        p = nullptr; n = 0;
+        cudaError_t e = cudaMalloc(&p, bytes ? bytes : 16);
+        if (e != cudaSuccess)
+            return set_err(TC_ERR_CUDA, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+        n = bytes;
+        return TC_OK;
+    }
+    void release() { if (p) cudaFree(p); p = nullptr; n = 0; }
+    template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+enum Stage { ST_CONVERT = 0, ST_FWD, ST_MID, ST_INV, ST_OUT, ST_D2H, ST_COUNT };
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    DevBuf in_a, in_b, grids, twx_f, twx_i, twy_f, twy_i, pcs, flags, outbuf, dbg;
+    const uint64_t* a_dev = nullptr; const uint64_t* b_dev = nullptr;
+    int64_t da = 0, db = 0; int a_cw = 0, b_cw = 0;
+    bool staged = false;
+    // twiddle cache key
+    std::vector<uint32_t> tw_primes; int64_t tw_L = 0, tw_sy = 0;
+    cudaEvent_t ev[ST_COUNT + 1] = {};
+    int64_t launches = 0;
+    int64_t stage_launches[8] = {0};
+    double stage_ms[8] = {0};
+    int profiling = 0;
+    cudaEvent_t user_ev[16] = {};
+    DevBuf flush;
+};
+
+int ilog2(int64_t x) { int l = 0; while ((1ll << l) < x) ++l; return l; }
+bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+
+uint64_t powmod(uint64_t b, uint64_t e, uint64_t p) {
+    uint64_t r = 1 % p; b %= p;
+    while (e) { if (e & 1) r = r * b % p; b = b * b % p; e >>= 1; }
+    return r;
+}
+uint32_t inv_mod(uint32_t a, uint32_t p) { return (uint32_t)powmod(a, p - 2, p); }
+
+// ---- tiny little-endian bignum on uint32 limbs (host constants only) ----
+typedef std::vector<uint32_t> Big;
+void big_mul_small(Big& x, uint32_t m) {
+    uint64_t c = 0;
+    for (auto& l : x) { uint64_t t = (uint64_t)l * m + c; l = (uint32_t)t; c = t >> 32; }
+    if (c) x.push_back((uint32_t)c);
+}
+void big_shl(Big& x, int s) {
+    int w = s / 32, b = s % 32;
+    Big r(x.size() + w + 1, 0);
+    for (size_t i = 0; i < x.size(); ++i) {
+        uint64_t v = (uint64_t)x[i] << b;
+        r[i + w] |= (uint32_t)v;
+        r[i + w + 1] |= (uint32_t)(v >> 32);
+    }
+    while (r.size() > 1 && r.back() == 0) r.pop_back();
+    x = r;
+}
+int big_cmp(const Big& a, const Big& b) {
+    size_t n = a.size() > b.size() ? a.size() : b.size();
+    for (size_t i = n; i-- > 0;) {
+        uint32_t x = i < a.size() ? a[i] : 0, y = i < b.size() ? b[i] : 0;
+        if (x != y) return x > y ? 1 : -1;
+    }
+    return 0;
+}
+
+int validate_plan(const tc_plan_t* pl, int64_t da, int64_t db) {
+    if (!pl) return set_err(TC_ERR_BAD_ARG, "plan is NULL");
+    int64_t d = da > db ? da : db;
+    if (pl->d != d) return set_err(TC_ERR_BAD_ARG, "plan.d=%lld but max(da,db)=%lld", (long long)pl->d, (long long)d);
+    if (!is_pow2(pl->K) || pl->K > (1 << 14)) return set_err(TC_ERR_BAD_ARG, "K=%lld must be a power of two <= 2^14", (long long)pl->K);
+    if (pl->M < 2 || pl->M > 63) return set_err(TC_ERR_BAD_ARG, "M=%lld outside [2, 63]", (long long)pl->M);
+    if (pl->N != pl->K * pl->M) return set_err(TC_ERR_BAD_ARG, "N != K*M");
+    if (!is_pow2(pl->s_y) || pl->s_y < 2 * d - 1 || (pl->s_y > 1 && pl->s_y / 2 >= 2 * d - 1))
+        return set_err(TC_ERR_BAD_ARG, "s_y=%lld is not the least power of two >= 2d-1", (long long)pl->s_y);
+    if (pl->P < 1 || pl->P > TC_MAX_PRIMES) return set_err(TC_ERR_BAD_ARG, "P=%d outside [1, %d]", pl->P, TC_MAX_PRIMES);
+    int64_t need = pl->s_y > 2 * pl->K ? pl->s_y : 2 * pl->K;
+    for (int q = 0; q < pl->P; ++q) {
+        uint32_t p = pl->p[q];
+        if (p < 3 || p >= (1u << 30) || (p - 1) % (uint64_t)need)
+            return set_err(TC_ERR_BAD_ARG, "prime %u unusable (need p < 2^30, %lld | p-1)", p, (long long)need);
+        for (int r = 0; r < q; ++r)
+            if (pl->p[r] == p) return set_err(TC_ERR_BAD_ARG, "duplicate prime %u", p);
+    }
+    return TC_OK;
+}
+
+int ensure_twiddles(Ctx* c, const tc_plan_t* pl) {
+    const int64_t L = 2 * pl->K, sy = pl->s_y;
+    std::vector<uint32_t> key(pl->p, pl->p + pl->P);
+    if (key == c->tw_primes && c->tw_L == L && c->tw_sy == sy) return TC_OK;
+    int rc;
+    const int64_t hx = L / 2, hy = sy > 1 ? sy / 2 : 1;
+    if ((rc = c->twx_f.ensure(sizeof(uint2) * hx * pl->P))) return rc;
+    if ((rc = c->twx_i.ensure(sizeof(uint2) * hx * pl->P))) return rc;
+    if ((rc = c->twy_f.ensure(sizeof(uint2) * hy * pl->P))) return rc;
+    if ((rc = c->twy_i.ensure(sizeof(uint2) * hy * pl->P))) return rc;
+    for (int q = 0; q < pl->P; ++q) {
+        const uint32_t p = pl->p[q], g = pl->g[q];
+        for (int dim = 0; dim < 2; ++dim) {
+            const int64_t n = dim == 0 ? L : sy;
+            const int64_t half = n / 2;
+            if (half < 1) continue;
+            PowTable pw;
+            const uint64_t w = powmod(g, (p - 1) / n, p), wi = inv_mod((uint32_t)w, p);
+            uint64_t cf = w, ci = wi;
+            const int nb = ilog2(half) + 1;
+            for (int b = 0; b < 32; ++b) {
+                pw.f[b] = (uint32_t)cf; pw.i[b] = (uint32_t)ci;
+                cf = cf * cf % p; ci = ci * ci % p;
+            }
+            uint2* f = (dim == 0 ? c->twx_f.as<uint2>() : c->twy_f.as<uint2>()) + q * (dim == 0 ? hx : hy);
+            uint2* iv = (dim == 0 ? c->twx_i.as<uint2>() : c->twy_i.as<uint2>()) + q * (dim == 0 ? hx : hy);
+            k_twiddles<<<(unsigned)((half + 255) / 256), 256, 0, c->st>>>(f, iv, half, p, pw, nb);
+            c->launches++;
+            CKL();
+        }
+    }
+    c->tw_primes = key; c->tw_L = L; c->tw_sy = sy;
+    return TC_OK;
+}
+
+PrimeC make_prime_const(uint32_t p, int64_t S) {
+    PrimeC pc{};
+    pc.p = p; pc.two_p = 2 * p;
+    uint32_t inv = 1;                       // p^{-1} mod 2^32 by Newton
+    for (int i = 0; i < 5; ++i) inv *= 2 - p * inv;
+    pc.pinv_neg = (uint32_t)(0u - inv);
+    const uint64_t r32 = (1ull << 32) % p;
+    pc.c64 = (uint32_t)(r32 * r32 % p);
+    pc.one_sh = (uint32_t)((1ull << 32) / p);
+    const uint64_t sinv = inv_mod((uint32_t)(S % p), p);
+    pc.scale = (uint32_t)(sinv * r32 % p);
+    pc.scale_sh = (uint32_t)(((uint64_t)pc.scale << 32) / p);
+    return pc;
+}
+
+int make_crt_const(const tc_plan_t* pl, int64_t dmin, CrtConst* cc) {
+    memset(cc, 0, sizeof *cc);
+    const int P = pl->P;
+    for (int k = 0; k < P; ++k) {
+        cc->p[k] = pl->p[k];
+        for (int m = 0; m < k; ++m) {
+            uint32_t v = inv_mod(pl->p[m] % pl->p[k], pl->p[k]);
+            cc->inv[m][k] = v;
+            cc->inv_sh[m][k] = (uint32_t)(((uint64_t)v << 32) / pl->p[k]);
+        }
+    }
+    Big prod{1};
+    for (int k = 0; k < P; ++k) big_mul_small(prod, pl->p[k]);
+    // bound = dmin * K * 2^(2M-2): the largest |c_ij| with balanced digits
+    Big bound{(uint32_t)(dmin * pl->K), (uint32_t)((uint64_t)(dmin * pl->K) >> 32)};
+    big_shl(bound, (int)(2 * pl->M - 2));
+    Big twob = bound; big_shl(twob, 1);
+    if (big_cmp(prod, twob) <= 0)
+        return set_err(TC_ERR_BAD_ARG, "prime product too small for the coefficient bound (plan K=%lld M=%lld P=%d)",
+                       (long long)pl->K, (long long)pl->M, P);
+    // half = (prod - 1) / 2  (prod is odd)
+    Big half;
+    {
+        Big h(prod.size(), 0);
+        uint32_t rem = 0;
+        for (size_t i = prod.size(); i-- > 0;) {
+            uint64_t cur = ((uint64_t)rem << 32) | prod[i];
+            h[i] = (uint32_t)(cur >> 1);
+            rem = (uint32_t)(cur & 1);
+        }
+        half = h;   // floor(prod/2) == (prod-1)/2 for odd prod
+    }
+    for (int l = 0; l < P; ++l) {
+        cc->prod[l] = l < (int)prod.size() ? prod[l] : 0;
+        cc->half[l] = l < (int)half.size() ? half[l] : 0;
+        cc->bound[l] = l < (int)bound.size() ? bound[l] : 0;
+    }
+    if ((int)prod.size() > P) return set_err(TC_ERR_BAD_ARG, "prime product exceeds 32P bits");
+    return TC_OK;
+}
+
+struct Geometry {
+    int64_t K, L, s_y, S; int lgL, lgK, lgS; int P;
+};
+
+std::vector<std::pair<int, int>> y_passes(int lgS) {   // (u0, U), forward (descending) order
+    std::vector<std::pair<int, int>> v;
+    if (lgS == 0) return v;
+    const int UMAX = 9;
+    int np = (lgS + UMAX - 1) / UMAX;
+    int base = lgS / np, extra = lgS % np;
+    int top = lgS;
+    for (int i = 0; i < np; ++i) {
+        int U = base + (i < extra ? 1 : 0);
+        v.push_back({top - U, U});
+        top -= U;
+    }
+    return v;
+}
+
+int launch_pass(Ctx* c, int kind /*0 fwd,1 inv,2 mid*/, const Geometry& G, uint32_t* grids,
+                const uint32_t* other, const uint2* tw, const uint2* twi, int u0, int U,
+                int64_t valid_rows, int64_t store_rows) {
+    PassArgs A{};
+    A.grids = grids; A.S = G.S; A.lgL = G.lgL; A.lgS = G.lgS; A.u0 = u0; A.U = U;
+    A.cb = G.lgL + u0 < 4 ? G.lgL + u0 : 4;
+    A.tw = tw; A.tw_stride = G.s_y > 1 ? G.s_y / 2 : 1;
+    A.pcs = c->pcs.as<PrimeC>();
+    A.valid_rows = valid_rows; A.store_rows = store_rows;
+    A.other = other; A.tw_inv = twi;
+    const int n = 1 << (U + A.cb);
+    const int64_t ctas = G.S / n;
+    int threads = n / 2 < 512 ? n / 2 : 512;
+    if (threads < 32) threads = 32;
+    const size_t smem = (size_t)n * 4;
+    dim3 grid((unsigned)ctas, (unsigned)G.P);
+    if (kind == 0) k_ypass<0><<<grid, threads, smem, c->st>>>(A);
+    else if (kind == 1) k_ypass<1><<<grid, threads, smem, c->st>>>(A);
+    else k_ymid<<<grid, threads, smem, c->st>>>(A);
+    c->launches++;
+    CKL();
+    return TC_OK;
+}
+
+int launch_convert(Ctx* c, const Geometry& G, const uint64_t* words, int64_t d, int cw, int M, int64_t N,
+                   int check_range, uint32_t* grids, int64_t* digits_out) {
+    ConvertArgs a{};
+    a.words = words; a.d = d; a.cw = cw;
+    a.K = G.K; a.lgK = G.lgK; a.M = M; a.N = N;
+    a.lgL = G.lgL;
+    a.R = (int)(G.K >= 2048 ? 1 : 2048 / G.K);
+    if (a.R > d) a.R = (int)d;
+    a.check_range = check_range;
+    a.grids = grids; a.S = G.S;
+    a.twx = c->twx_f.as<uint2>();
+    a.pcs = c->pcs.as<PrimeC>(); a.P = G.P;
+    a.err = c->flags.as<int>();
+    a.digits_out = digits_out;
+    const size_t smem = (size_t)a.R * G.K * 8 + (size_t)a.R * G.L * 4;
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_convert_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t ctas = (d + a.R - 1) / a.R;
+    k_convert_x<<<(unsigned)ctas, 256, smem, c->st>>>(a);
+    c->launches++;
+    CKL();
+    return TC_OK;
+}
+
+int launch_xinv(Ctx* c, const Geometry& G, uint32_t* grids, int64_t rows) {
+    int R = (int)(G.L >= 4096 ? 1 : 4096 / G.L);
+    if (R > rows) R = (int)rows;
+    const size_t smem = (size_t)R * G.L * 4;
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_xinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid((unsigned)((rows + R - 1) / R), (unsigned)G.P);
+    k_xinv<<<grid, 256, smem, c->st>>>(grids, G.S, G.lgL, R, rows, c->twx_i.as<uint2>(), c->pcs.as<PrimeC>());
+    c->launches++;
+    CKL();
+    return TC_OK;
+}
+
+template <int P>
+int launch_crt_out_p(Ctx* c, const CrtOutArgs& A0, const CrtConst& cc, int64_t rows) {
+    CrtOutArgs A = A0;
+    const int rpc = 256 / A.tpr;
+    const size_t terms = ((size_t)rpc * A.max_terms * P + 1) & ~(size_t)1;
+    const size_t smem = terms * 4 + 256 * 8 + 256 * 4 + (((size_t)rpc + 1) & ~(size_t)1) * 4 + (size_t)rpc * 8;
+    if (smem > 227 * 1024) return set_err(TC_ERR_BAD_ARG, "ConvertOut tile needs %zu bytes of shared memory", smem);
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_crt_out<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t ctas = (rows + rpc - 1) / rpc;
+    k_crt_out<P><<<(unsigned)ctas, 256, smem, c->st>>>(A, cc);
+    c->launches++;
+    CKL();
+    return TC_OK;
+}
+
+int launch_crt_out(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows, int M, int W32,
+                   uint32_t* out, const CrtConst& cc) {
+    CrtOutArgs A{};
+    A.grids = grids; A.S = G.S; A.lgL = G.lgL; A.rows = rows; A.M = M; A.W32 = W32;
+    const int per = (W32 + kWPT - 1) / kWPT;
+    if (per <= 256) {
+        int t = 1; while (t < per) t <<= 1;
+        A.tpr = t; A.nchunks = 1;
+    } else {
+        A.tpr = 256; A.nchunks = (W32 + 256 * kWPT - 1) / (256 * kWPT);
+    }
+    A.max_terms = (int)(32ll * (A.tpr * kWPT + G.P) / M + 3);
+    A.out = out; A.err = c->flags.as<int>();
+    switch (G.P) {
+#define CASE(n) case n: return launch_crt_out_p<n>(c, A, cc, rows);
+        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+        CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+#undef CASE
+    }
+    return set_err(TC_ERR_BAD_ARG, "P=%d unsupported", G.P);
+}
+
+int launch_crt_dump(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows, uint32_t* out,
+                    const CrtConst& cc) {
+    const int64_t n = rows * G.L;
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    int* err = c->flags.as<int>();
+    switch (G.P) {
+#define CASE(k) case k: k_crt_dump<k><<<blocks, 256, 0, c->st>>>(grids, G.S, G.lgL, rows, out, err, cc); break;
+        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+        CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+#undef CASE
+        default: return set_err(TC_ERR_BAD_ARG, "P=%d unsupported", G.P);
+    }
+    c->launches++;
+    CKL();
+    return TC_OK;
+}
+
+// The transform part of the pipeline, shared by tc_execute and
+// tc_bivariate_product: leaves exact c_ij mod p_q in the B grids (rows < rows).
+int run_transforms(Ctx* c, const tc_plan_t* pl, int a_bits, int b_bits, Geometry& G, int64_t rows,
+                   uint32_t** result_grids) {
+    int rc;
+    G.K = pl->K; G.L = 2 * pl->K; G.s_y = pl->s_y; G.S = G.s_y * G.L;
+    G.lgL = ilog2(G.L); G.lgK = ilog2(G.K); G.lgS = ilog2(G.s_y); G.P = pl->P;
+    if ((rc = ensure_twiddles(c, pl))) return rc;
+    if ((rc = c->grids.ensure((size_t)2 * G.P * G.S * 4))) return rc;
+    std::vector<PrimeC> pcs(G.P);
+    for (int q = 0; q < G.P; ++q) pcs[q] = make_prime_const(pl->p[q], G.S);
+    if ((rc = c->pcs.ensure(sizeof(PrimeC) * G.P))) return rc;
+    CK(cudaMemcpyAsync(c->pcs.p, pcs.data(), sizeof(PrimeC) * G.P, cudaMemcpyHostToDevice, c->st));
+    if ((rc = c->flags.ensure(64))) return rc;
+    CK(cudaMemsetAsync(c->flags.p, 0x7f, 64, c->st));
+
+    uint32_t* GA = c->grids.as<uint32_t>();
+    uint32_t* GB = GA + (size_t)G.P * G.S;
+    const uint2* tyf = c->twy_f.as<uint2>();
+    const uint2* tyi = c->twy_i.as<uint2>();
+
+    CK(cudaEventRecord(c->ev[0], c->st));
+    const int64_t nA = c->a_cw, nB = c->b_cw;
+    (void)nA; (void)nB;
+    if ((rc = launch_convert(c, G, c->a_dev, c->da, c->a_cw, (int)pl->M, pl->N, a_bits > pl->N, GA, nullptr))) return rc;
+    if ((rc = launch_convert(c, G, c->b_dev, c->db, c->b_cw, (int)pl->M, pl->N, b_bits > pl->N, GB, nullptr))) return rc;
+    CK(cudaEventRecord(c->ev[1], c->st));
+
+    auto passes = y_passes(G.lgS);
+    const int np = (int)passes.size();
+    // operand A: every forward pass; operand B: all but the innermost
+    for (int i = 0; i < np; ++i)
+        if ((rc = launch_pass(c, 0, G, GA, nullptr, tyf, nullptr, passes[i].first, passes[i].second,
+                              i == 0 ? c->da : G.s_y, G.s_y))) return rc;
+    for (int i = 0; i + 1 < np; ++i)
+        if ((rc = launch_pass(c, 0, G, GB, nullptr, tyf, nullptr, passes[i].first, passes[i].second,
+                              i == 0 ? c->db : G.s_y, G.s_y))) return rc;
+    CK(cudaEventRecord(c->ev[2], c->st));
+    if (np == 0) {
+        if ((rc = launch_pass(c, 2, G, GB, GA, tyf, tyi, 0, 0, c->db, G.s_y))) return rc;
+    } else {
+        if ((rc = launch_pass(c, 2, G, GB, GA, tyf, tyi, passes[np - 1].first, passes[np - 1].second,
+                              np == 1 ? c->db : G.s_y, G.s_y))) return rc;
+    }
+    CK(cudaEventRecord(c->ev[3], c->st));
+    for (int i = np - 2; i >= 0; --i)
+        if ((rc = launch_pass(c, 1, G, GB, nullptr, tyi, nullptr, passes[i].first, passes[i].second,
+                              G.s_y, i == 0 ? rows : G.s_y))) return rc;
+    if ((rc = launch_xinv(c, G, GB, rows))) return rc;
+    CK(cudaEventRecord(c->ev[4], c->st));
+    *result_grids = GB;
+    return TC_OK;
+}
+
+int read_flags(Ctx* c, int* f) {
+    CK(cudaMemcpyAsync(f, c->flags.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return TC_OK;
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tc_version(void) { return "tcgpu 0.1 (sm_100a)"; }
+const char* tc_last_error(void) { return g_last_error.c_str(); }
+
+int tc_ctx_create(int device, void** out) {
+    if (!out) return set_err(TC_ERR_BAD_ARG, "ctx out-pointer is NULL");
+    Ctx* c = new Ctx();
+    if (device >= 0) {
+        cudaError_t e = cudaSetDevice(device);
+        if (e != cudaSuccess) { delete c; return set_err(TC_ERR_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e)); }
+        c->device = device;
+    } else {
+        cudaGetDevice(&c->device);
+    }
+    cudaError_t e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { delete c; return set_err(TC_ERR_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e)); }
+    for (auto& ev : c->ev) cudaEventCreate(&ev);
+    *out = c;
+    return TC_OK;
+}
+
+int tc_ctx_destroy(void* ctx) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c) return TC_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->st);
+    for (DevBuf* b : {&c->in_a, &c->in_b, &c->grids, &c->twx_f, &c->twx_i, &c->twy_f, &c->twy_i,
+                      &c->pcs, &c->flags, &c->outbuf, &c->dbg}) b->release();
+    for (auto& ev : c->ev) if (ev) cudaEventDestroy(ev);
+    for (auto& ev : c->user_ev) if (ev) cudaEventDestroy(ev);
+    c->flush.release();
+    cudaStreamDestroy(c->st);
+    delete c;
+    return TC_OK;
+}
+
+int tc_stage_inputs(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw,
+                    const uint64_t* b, int64_t db, int32_t b_cw, int32_t on_device,
+                    tc_input_info_t* info) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || !a || !b || da < 1 || db < 1 || a_cw < 1 || b_cw < 1)
+        return set_err(TC_ERR_BAD_ARG, "bad operand arguments");
+    CK(cudaSetDevice(c->device));
+    int rc;
+    if (on_device) {
+        c->a_dev = a; c->b_dev = b;
+    } else {
+        if ((rc = c->in_a.ensure((size_t)da * a_cw * 8))) return rc;
+        if ((rc = c->in_b.ensure((size_t)db * b_cw * 8))) return rc;
+        CK(cudaMemcpyAsync(c->in_a.p, a, (size_t)da * a_cw * 8, cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(c->in_b.p, b, (size_t)db * b_cw * 8, cudaMemcpyHostToDevice, c->st));
+        c->a_dev = c->in_a.as<uint64_t>(); c->b_dev = c->in_b.as<uint64_t>();
+    }
+    c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true;
+    if ((rc = c->dbg.ensure(64))) return rc;
+    CK(cudaMemsetAsync(c->dbg.p, 0, 16, c->st));
+    int* wf = c->dbg.as<int>();
+    k_width<<<(unsigned)((da + 255) / 256), 256, 0, c->st>>>(c->a_dev, da, a_cw, wf);
+    k_width<<<(unsigned)((db + 255) / 256), 256, 0, c->st>>>(c->b_dev, db, b_cw, wf + 2);
+    c->launches += 2;
+    CKL();
+    int h[4];
+    CK(cudaMemcpyAsync(h, wf, sizeof h, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (info) { info->n_in_a = h[0]; info->nonzero_a = h[1]; info->n_in_b = h[2]; info->nonzero_b = h[3]; }
+    return TC_OK;
+}
+
+int tc_execute(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32_t b_bits,
+               uint64_t* out, int64_t rows, int32_t out_cw, int32_t out_on_device,
+               tc_times_t* times, int64_t* err_index) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    const double t_begin = now_s();
+    if (!c || !c->staged) return set_err(TC_ERR_BAD_ARG, "no staged inputs");
+    if (err_index) *err_index = -1;
+    CK(cudaSetDevice(c->device));
+    int rc;
+    if ((rc = validate_plan(plan, c->da, c->db))) return rc;
+    if (rows != c->da + c->db - 1) return set_err(TC_ERR_BAD_ARG, "rows must be da+db-1");
+    if (out_cw < 1 || !out) return set_err(TC_ERR_BAD_ARG, "bad output buffer");
+    CrtConst cc;
+    const int64_t dmin = c->da < c->db ? c->da : c->db;
+    if ((rc = make_crt_const(plan, dmin, &cc))) return rc;
+    Geometry G;
+    uint32_t* R = nullptr;
+    if ((rc = run_transforms(c, plan, a_bits, b_bits, G, rows, &R))) return rc;
+    uint32_t* dout;
+    if (out_on_device) {
+        dout = reinterpret_cast<uint32_t*>(out);
+    } else {
+        if ((rc = c->outbuf.ensure((size_t)rows * out_cw * 8))) return rc;
+        dout = c->outbuf.as<uint32_t>();
+    }
+    if ((rc = launch_crt_out(c, G, R, rows, (int)plan->M, 2 * out_cw, dout, cc))) return rc;
+    CK(cudaEventRecord(c->ev[5], c->st));
+    if (!out_on_device)
+        CK(cudaMemcpyAsync(out, dout, (size_t)rows * out_cw * 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaEventRecord(c->ev[6], c->st));
+    int f[4];
+    if ((rc = read_flags(c, f))) return rc;
+    float ms[6] = {0};
+    for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&ms[i], c->ev[i], c->ev[i + 1]);
+    for (int i = 0; i < 6; ++i) c->stage_ms[i] = ms[i];
+    if (times) {
+        times->convert = ms[0] * 1e-3;
+        times->ntt_forward = ms[1] * 1e-3;
+        times->pointwise = ms[2] * 1e-3;
+        times->ntt_inverse = ms[3] * 1e-3;
+        times->crt = 0.0;
+        times->recover = (ms[4] + ms[5]) * 1e-3;
+        times->total = now_s() - t_begin;
+        times->gpus = 1;
+    }
+    if (f[1] != 0x7f7f7f7f) { if (err_index) *err_index = f[1]; return set_err(TC_ERR_RANGE, "coefficient outside the plan's %lld-bit range", (long long)plan->N); }
+    if (f[0] != 0x7f7f7f7f) { if (err_index) *err_index = f[0]; return set_err(TC_ERR_ENCODING, "coefficient %d exceeds the digit capacity", f[0]); }
+    if (f[2] != 0x7f7f7f7f) { if (err_index) *err_index = f[2]; return set_err(TC_ERR_BOUND, "coefficient bound exceeded at flat index %d", f[2]); }
+    return TC_OK;
+}
+
+int tc_multiply(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int32_t a_bits,
+                const uint64_t* b, int64_t db, int32_t b_cw, int32_t b_bits,
+                const tc_plan_t* plan, uint64_t* out, int64_t rows, int32_t out_cw,
+                tc_times_t* times, int64_t* err_index) {
+    const double t0 = now_s();
+    int rc = tc_stage_inputs(ctx, a, da, a_cw, b, db, b_cw, 0, nullptr);
+    if (rc) return rc;
+    const double t1 = now_s();
+    rc = tc_execute(ctx, plan, a_bits, b_bits, out, rows, out_cw, 0, times, err_index);
+    if (times && rc == TC_OK) { times->convert += t1 - t0; times->total = now_s() - t0; }
+    return rc;
+}
+
+int tc_digits(void* ctx, int32_t which, int64_t K, int64_t M, int64_t N, int32_t in_bits,
+              int64_t* digits_out, int64_t* err_index) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || !c->staged || !digits_out) return set_err(TC_ERR_BAD_ARG, "no staged inputs");
+    if (!is_pow2(K) || M < 2 || M > 63 || N != K * M) return set_err(TC_ERR_BAD_ARG, "bad digit split");
+    if (err_index) *err_index = -1;
+    CK(cudaSetDevice(c->device));
+    const uint64_t* w = which ? c->b_dev : c->a_dev;
+    const int64_t d = which ? c->db : c->da;
+    const int cw = which ? c->b_cw : c->a_cw;
+    Geometry G{};
+    G.K = K; G.L = 2 * K; G.lgK = ilog2(K); G.lgL = ilog2(2 * K); G.P = 0; G.s_y = 1; G.S = 0;
+    int rc;
+    if ((rc = c->flags.ensure(64))) return rc;
+    CK(cudaMemsetAsync(c->flags.p, 0x7f, 64, c->st));
+    if ((rc = c->dbg.ensure((size_t)d * K * 8 + 64))) return rc;
+    int64_t* dd = reinterpret_cast<int64_t*>(c->dbg.as<char>() + 64);
+    if ((rc = c->pcs.ensure(sizeof(PrimeC)))) return rc;
+    if ((rc = c->twx_f.ensure(16))) return rc;
+    if ((rc = launch_convert(c, G, w, d, cw, (int)M, N, in_bits > N, nullptr, dd))) return rc;
+    CK(cudaMemcpyAsync(digits_out, dd, (size_t)d * K * 8, cudaMemcpyDeviceToHost, c->st));
+    int f[4];
+    if ((rc = read_flags(c, f))) return rc;
+    if (f[1] != 0x7f7f7f7f) { if (err_index) *err_index = f[1]; return set_err(TC_ERR_RANGE, "coefficient outside the plan's %lld-bit range", (long long)N); }
+    if (f[0] != 0x7f7f7f7f) { if (err_index) *err_index = f[0]; return set_err(TC_ERR_ENCODING, "coefficient %d exceeds the digit capacity", f[0]); }
+    return TC_OK;
+}
+
+int tc_bivariate_product(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32_t b_bits,
+                         uint32_t* coeffs_out, int64_t rows, int64_t* err_index) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || !c->staged || !coeffs_out) return set_err(TC_ERR_BAD_ARG, "no staged inputs");
+    if (err_index) *err_index = -1;
+    CK(cudaSetDevice(c->device));
+    int rc;
+    if ((rc = validate_plan(plan, c->da, c->db))) return rc;
+    if (rows != c->da + c->db - 1) return set_err(TC_ERR_BAD_ARG, "rows must be da+db-1");
+    CrtConst cc;
+    const int64_t dmin = c->da < c->db ? c->da : c->db;
+    if ((rc = make_crt_const(plan, dmin, &cc))) return rc;
+    Geometry G;
+    uint32_t* R = nullptr;
+    if ((rc = run_transforms(c, plan, a_bits, b_bits, G, rows, &R))) return rc;
+    const size_t bytes = (size_t)rows * G.L * G.P * 4;
+    if ((rc = c->outbuf.ensure(bytes))) return rc;
+    if ((rc = launch_crt_dump(c, G, R, rows, c->outbuf.as<uint32_t>(), cc))) return rc;
+    CK(cudaMemcpyAsync(coeffs_out, c->outbuf.p, bytes, cudaMemcpyDeviceToHost, c->st));
+    int f[4];
+    if ((rc = read_flags(c, f))) return rc;
+    if (f[1] != 0x7f7f7f7f) { if (err_index) *err_index = f[1]; return set_err(TC_ERR_RANGE, "coefficient outside the plan's range"); }
+    if (f[0] != 0x7f7f7f7f) { if (err_index) *err_index = f[0]; return set_err(TC_ERR_ENCODING, "coefficient %d exceeds the digit capacity", f[0]); }
+    if (f[2] != 0x7f7f7f7f) { if (err_index) *err_index = f[2]; return set_err(TC_ERR_BOUND, "coefficient bound exceeded at flat index %d", f[2]); }
+    return TC_OK;
+}
+
+int tc_modmul_probe(uint32_t p, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t n, int32_t mode) {
+    if (n < 1 || !a || !b || !out || p < 3 || p >= (1u << 30)) return set_err(TC_ERR_BAD_ARG, "bad probe arguments");
+    uint32_t *da = nullptr;
+    CK(cudaMalloc(&da, (size_t)n * 12));
+    uint32_t* db = da + n; uint32_t* dc = db + n;
+    CK(cudaMemcpy(da, a, (size_t)n * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(db, b, (size_t)n * 4, cudaMemcpyHostToDevice));
+    PrimeC pc = make_prime_const(p, 1);
+    k_modmul_probe<<<(unsigned)((n + 255) / 256), 256>>>(p, pc.pinv_neg, da, db, dc, n, mode);
+    CKL();
+    CK(cudaMemcpy(out, dc, (size_t)n * 4, cudaMemcpyDeviceToHost));
+    cudaFree(da);
+    return TC_OK;
+}
+
+int tc_ntt_probe(uint32_t p, uint32_t g, uint32_t* data, int64_t n, int32_t dir) {
+    if (!data || !is_pow2(n) || n > 8192 || p < 3 || p >= (1u << 30) || (p - 1) % n)
+        return set_err(TC_ERR_BAD_ARG, "bad NTT probe arguments");
+    if (n == 1) return TC_OK;
+    // A 1 x n grid transformed by the x-direction kernels: forward via the
+    // ConvertIn path is digit-based, so the probe uses dedicated launches of
+    // the shared butterflies through k_xinv (inverse) and a forward tile.
+    void* ctx = nullptr;
+    int rc = tc_ctx_create(-1, &ctx);
+    if (rc) return rc;
+    Ctx* c = static_cast<Ctx*>(ctx);
+    tc_plan_t pl{};
+    pl.K = n / 2; pl.s_y = 1; pl.P = 1; pl.p[0] = p; pl.g[0] = g;
+    rc = ensure_twiddles(c, &pl);
+    if (!rc) rc = c->grids.ensure((size_t)n * 4);
+    if (!rc) rc = c->pcs.ensure(sizeof(PrimeC));
+    if (!rc) {
+        PrimeC pc = make_prime_const(p, n);
+        cudaMemcpy(c->pcs.p, &pc, sizeof pc, cudaMemcpyHostToDevice);
+        cudaMemcpy(c->grids.p, data, (size_t)n * 4, cudaMemcpyHostToDevice);
+        Geometry G{};
+        G.K = n / 2; G.L = n; G.s_y = 1; G.S = n; G.lgL = ilog2(n); G.lgK = G.lgL - 1; G.lgS = 0; G.P = 1;
+        if (dir == 0) {
+            // forward: y-pass machinery with lgS = 0 is a no-op, so run the
+            // x-direction DIF as a pass over flattened bits [0, lgL).
+            PassArgs A{};
+            A.grids = c->grids.as<uint32_t>(); A.S = n; A.lgL = 0; A.lgS = G.lgL; A.u0 = 0; A.U = G.lgL; A.cb = 0;
+            A.tw = c->twx_f.as<uint2>(); A.tw_stride = n / 2; A.pcs = c->pcs.as<PrimeC>();
+            A.valid_rows = n; A.store_rows = n;
+            int threads = n / 2 < 512 ? (int)(n / 2) : 512;
+            if (threads < 32) threads = 32;
+            k_ypass<0><<<dim3(1, 1), threads, (size_t)n * 4, c->st>>>(A);
+        } else {
+            rc = launch_xinv(c, G, c->grids.as<uint32_t>(), 1);
+        }
+        cudaError_t e = cudaStreamSynchronize(c->st);
+        if (!rc && e != cudaSuccess) rc = set_err(TC_ERR_CUDA, "probe: %s", cudaGetErrorString(e));
+        if (!rc) {
+            std::vector<uint32_t> h(n);
+            cudaMemcpy(h.data(), c->grids.p, (size_t)n * 4, cudaMemcpyDeviceToHost);
+            const uint64_t ninv = inv_mod((uint32_t)(n % p), p);
+            for (int64_t i = 0; i < n; ++i) {
+                uint64_t v = h[i] % p;
+                if (dir == 1) v = v * ninv % p;
+                data[i] = (uint32_t)v;
+            }
+        }
+    }
+    tc_ctx_destroy(ctx);
+    return rc;
+}
+
+int tc_device_alloc(void* ctx, int64_t bytes, void** dptr) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || !dptr) return set_err(TC_ERR_BAD_ARG, "bad alloc arguments");
+    CK(cudaSetDevice(c->device));
+    CK(cudaMalloc(dptr, bytes > 0 ? bytes : 16));
+    return TC_OK;
+}
+
+int tc_device_free(void* ctx, void* dptr) {
+    (void)ctx;
+    CK(cudaFree(dptr));
+    return TC_OK;
+}
+
+int tc_memcpy(void* ctx, void* dst, const void* src, int64_t bytes, int32_t kind) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c) return set_err(TC_ERR_BAD_ARG, "ctx is NULL");
+    cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice : kind == 2 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    CK(cudaMemcpyAsync(dst, src, bytes, k, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return TC_OK;
+}
+
+int tc_synchronize(void* ctx) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c) return set_err(TC_ERR_BAD_ARG, "ctx is NULL");
+    CK(cudaStreamSynchronize(c->st));
+    return TC_OK;
+}
+
+int tc_host_alloc(int64_t bytes, void** hptr) {
+    if (!hptr) return set_err(TC_ERR_BAD_ARG, "hptr is NULL");
+    CK(cudaHostAlloc(hptr, bytes > 0 ? bytes : 16, cudaHostAllocDefault));
+    return TC_OK;
+}
+
+int tc_host_free(void* hptr) {
+    CK(cudaFreeHost(hptr));
+    return TC_OK;
+}
+
+int tc_record_event(void* ctx, int32_t slot) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || slot < 0 || slot >= 16) return set_err(TC_ERR_BAD_ARG, "bad event slot");
+    if (!c->user_ev[slot]) CK(cudaEventCreate(&c->user_ev[slot]));
+    CK(cudaEventRecord(c->user_ev[slot], c->st));
+    return TC_OK;
+}
+
+int tc_event_elapsed(void* ctx, int32_t s0, int32_t s1, float* ms) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || s0 < 0 || s1 < 0 || s0 >= 16 || s1 >= 16 || !c->user_ev[s0] || !c->user_ev[s1] || !ms)
+        return set_err(TC_ERR_BAD_ARG, "bad event slots");
+    CK(cudaEventSynchronize(c->user_ev[s1]));
+    CK(cudaEventElapsedTime(ms, c->user_ev[s0], c->user_ev[s1]));
+    return TC_OK;
+}
+
+int tc_flush_l2(void* ctx) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c) return set_err(TC_ERR_BAD_ARG, "ctx is NULL");
+    int rc;
+    const size_t n = (size_t)256 << 20;
+    if ((rc = c->flush.ensure(n))) return rc;
+    CK(cudaMemsetAsync(c->flush.p, (int)(c->launches & 0xff), n, c->st));
+    return TC_OK;
+}
+
+int tc_int_peak(void* ctx, double* bfly_per_s, double* mont_per_s) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c) return set_err(TC_ERR_BAD_ARG, "ctx is NULL");
+    int rc;
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    if ((rc = c->dbg.ensure((size_t)blocks * threads * 4 + 64))) return rc;
+    const uint32_t p = 1053818881u;
+    PrimeC pc = make_prime_const(p, 1);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    float ms = 0;
+    for (int mode = 0; mode < 2; ++mode) {
+        for (int rep = 0; rep < 2; ++rep) {   // first launch warms clocks
+            cudaEventRecord(e0, c->st);
+            k_int_peak<<<blocks, threads, 0, c->st>>>(c->dbg.as<uint32_t>(), iters, p, pc.pinv_neg, mode);
+            cudaEventRecord(e1, c->st);
+            CKL();
+        }
+        CK(cudaEventSynchronize(e1));
+        cudaEventElapsedTime(&ms, e0, e1);
+        // each iteration: 8 independent chains of one butterfly (mode 0) or one product (mode 1)
+        const double ops = (double)blocks * threads * iters * 8;
+        if (mode == 0 && bfly_per_s) *bfly_per_s = ops / (ms * 1e-3);
+        if (mode == 1 && mont_per_s) *mont_per_s = ops / (ms * 1e-3);
+    }
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    return TC_OK;
+}
+
+int64_t tc_kernel_launches(void* ctx) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    return c ? c->launches : -1;
+}
+
+int tc_set_profiling(void* ctx, int32_t enable) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c) return set_err(TC_ERR_BAD_ARG, "ctx is NULL");
+    c->profiling = enable;
+    return TC_OK;
+}
+
+int tc_last_profile(void* ctx, double* ms_by_stage, int64_t* launches_by_stage) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c) return set_err(TC_ERR_BAD_ARG, "ctx is NULL");
+    for (int i = 0; i < 8; ++i) {
+        if (ms_by_stage) ms_by_stage[i] = c->stage_ms[i];
+        if (launches_by_stage) launches_by_stage[i] = c->stage_launches[i];
+    }
+    return TC_OK;
+}
+
+}  // extern "C"

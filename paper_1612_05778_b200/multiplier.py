@@ -1,0 +1,164 @@
+"""The public multiply entry points -- drop-in for tc/multiplier.py:31-181.
+
+`multiply(MulRequest(a, b, prime_count, worker_hint)) -> IntPolynomial` and
+`multiply_with_stats` keep the reference's names, arguments, result type,
+error types and StageTimings layout.  The work runs in libtcgpu.so on a B200:
+
+  tc_stage_inputs  H2D copy + device width/zero scan   (tc/params.py:290-293, tc/zpoly.py:103-114)
+  plan_gpu         host planner (params.py)             (tc/params.py:225-313)
+  tc_execute       ConvertIn + 2-D NTTs + pointwise + CRT + ConvertOut + D2H
+                                                        (tc/multiplier.py:131-166)
+
+There is no CPU fallback: without the CUDA library or a device every call
+raises DeviceError.  `prime_count` keeps its reference meaning for validation
+and for the planning errors the reference raises (PrimeCapacityError with one
+63-bit prime); the GPU's own prime set is chosen by plan_gpu and never changes
+the result, exactly like `worker_hint` (tc/multiplier.py:169-176 docstring).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from time import perf_counter
+
+import numpy as np
+
+from . import _lib
+from .errors import (CorruptedConvolutionError, EmptyInputError, EncodingError,
+                     TransformLengthError)
+from .params import GpuPlan, _finish_plan, _choose_split, extreme_coefficients, plan_gpu, s_y_for
+from .zpoly import IntPolynomial, output_bit_width, twos_complement_width
+
+WORD_BITS = 64
+
+
+@dataclass(frozen=True)
+class MulRequest:
+    """One multiplication: inputs, prime count (1-3), optional worker bound
+    (tc/multiplier.py:31-38).  worker_hint maps to the GPU count."""
+
+    a: IntPolynomial
+    b: IntPolynomial
+    prime_count: int = 2
+    worker_hint: int | None = None
+
+
+@dataclass(frozen=True)
+class StageTimings:
+    """Time per pipeline stage, in seconds (tc/multiplier.py:41-56).
+
+    Stages are CUDA-event times of the fused kernels: convert = H2D + ConvertIn
+    fused with the x-direction forward NTT; ntt_forward = forward y passes;
+    pointwise = fused last forward pass + pointwise product + first inverse
+    pass; ntt_inverse = remaining inverse passes; crt = 0 (fused into recover);
+    recover = fused CRT + ConvertOut + D2H.  total is wall clock."""
+
+    convert: float
+    ntt_forward: float
+    pointwise: float
+    ntt_inverse: float
+    crt: float
+    recover: float
+    total: float
+    workers: int
+
+    def stage_sum(self) -> float:
+        return (self.convert + self.ntt_forward + self.pointwise
+                + self.ntt_inverse + self.crt + self.recover)
+
+
+def _check_reference_planning(req: MulRequest, d: int) -> None:
+    """Raise the planning errors the reference raises for this prime_count
+    (tc/params.py:200-222 via build_plan) -- the drop-in's error behaviour."""
+    if req.prime_count not in (1, 2, 3):
+        raise ValueError(f"prime count must be 1, 2, or 3, got {req.prime_count}")
+    if req.prime_count == 1:
+        lo, hi = extreme_coefficients(req.a, req.b)
+        n_min = max(twos_complement_width(lo), twos_complement_width(hi))
+        K, M = _choose_split(d, n_min, lo, hi, 1)
+        _finish_plan(d, K, M, 1)      # raises PrimeCapacityError / TransformLengthError
+    elif s_y_for(d) > (1 << 57):
+        raise TransformLengthError("transform length unsupported")
+
+
+def _raise_status(rc: int, err_index: int, plan: GpuPlan, a: IntPolynomial) -> None:
+    if rc == _lib.TC_ERR_RANGE:
+        raise EncodingError(f"coefficient outside the plan's {plan.N}-bit range")
+    if rc == _lib.TC_ERR_ENCODING:
+        raise EncodingError(f"coefficient {err_index} exceeds the digit capacity of "
+                            f"K={plan.K}, M={plan.M}")
+    if rc == _lib.TC_ERR_BOUND:
+        i, j = divmod(err_index, plan.L)
+        raise CorruptedConvolutionError(
+            f"corrupted convolution: coefficient bound exceeded at ({i}, {j})")
+    if rc == _lib.TC_ERR_PARITY:
+        raise CorruptedConvolutionError(
+            f"corrupted convolution: odd combination at coefficient {err_index}")
+    _lib.check(rc, "tc_execute")
+
+
+def _as_words(p: IntPolynomial) -> np.ndarray:
+    w = p.words
+    if not (w.flags.c_contiguous and w.dtype == np.uint64):
+        w = np.ascontiguousarray(w, dtype=np.uint64)
+    return w
+
+
+def _run_pipeline(req: MulRequest, plan_override: dict | None = None, device: int = -1):
+    t_begin = perf_counter()
+    ctx = _lib.context(device)
+    a, b = req.a, req.b
+    aw, bw = _as_words(a), _as_words(b)
+    da, db = aw.shape[0], bw.shape[0]
+    d = max(da, db)
+    rows = da + db - 1
+    info = _lib.TcInputInfo()
+    lib = ctx.lib
+    with ctx.lock:
+        _lib.check(lib.tc_stage_inputs(ctx.handle, _lib.ptr(aw), da, aw.shape[1],
+                                       _lib.ptr(bw), db, bw.shape[1], 0, ctypes.byref(info)),
+                   "tc_stage_inputs")
+        if not (info.nonzero_a and info.nonzero_b):
+            raise EmptyInputError("empty input: zero polynomial")
+        _check_reference_planning(req, d)
+        n_in = max(info.n_in_a, info.n_in_b)
+        po = plan_override or {}
+        plan = plan_gpu(d, min(da, db), max(n_in, po.get("n_min", 1)), K=po.get("K"), M=po.get("M"))
+        out_bits = output_bit_width(d, n_in)
+        out_cw = -(-out_bits // WORD_BITS)
+        out = _lib.pinned.empty((rows, out_cw), np.uint64)   # pinned: D2H at full PCIe rate
+        times = _lib.TcTimes()
+        err = ctypes.c_int64(-1)
+        rc = lib.tc_execute(ctx.handle, ctypes.byref(_lib.make_plan(plan)), a.bit_width, b.bit_width,
+                            _lib.ptr(out), rows, out_cw, 0, ctypes.byref(times), ctypes.byref(err))
+    if rc:
+        _raise_status(rc, err.value, plan, a)
+    result = IntPolynomial._trusted(out, out_bits)
+    total = perf_counter() - t_begin
+    stats = StageTimings(convert=times.convert, ntt_forward=times.ntt_forward,
+                         pointwise=times.pointwise, ntt_inverse=times.ntt_inverse,
+                         crt=times.crt, recover=times.recover, total=total,
+                         workers=req.worker_hint if req.worker_hint else 1)
+    return result, stats, plan
+
+
+def multiply(req: MulRequest) -> IntPolynomial:
+    """Exact product of req.a and req.b (tc/multiplier.py:169-176).
+
+    The result does not depend on prime_count or worker_hint; both only change
+    how the work is carried out."""
+    result, _, _ = _run_pipeline(req)
+    return result
+
+
+def multiply_with_stats(req: MulRequest) -> tuple:
+    """Like multiply, plus time per pipeline stage (tc/multiplier.py:179-181)."""
+    result, stats, _ = _run_pipeline(req)
+    return result, stats
+
+
+def multiply_with_plan(req: MulRequest, K: int | None = None, M: int | None = None):
+    """multiply under an explicit digit split (experiments / parity tests);
+    returns (product, stats, GpuPlan)."""
+    return _run_pipeline(req, plan_override={"K": K, "M": M})

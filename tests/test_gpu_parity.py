@@ -1,0 +1,259 @@
+"""GPU parity: the CUDA path (through libtcgpu.so's C-ABI) against the golden
+vectors produced by the reference and against the CPU oracle.  Integer work:
+every comparison is bit-exact (zero tolerance)."""
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_golden
+
+pytestmark = pytest.mark.gpu
+
+import paper_1612_05778_b200 as tc  # noqa: E402
+from paper_1612_05778_b200 import seams, workloads  # noqa: E402
+from paper_1612_05778_b200.params import gpu_prime_table, plan_gpu  # noqa: E402
+
+
+def _poly(words, bits):
+    return tc.IntPolynomial(np.ascontiguousarray(words), bits)
+
+
+def _random_poly(rng, d, nbits, extremes=False):
+    lo, hi = -(1 << (nbits - 1)), (1 << (nbits - 1)) - 1
+    while True:
+        if extremes:
+            coeffs = [rng.choice([lo, hi]) for _ in range(d)]
+        else:
+            coeffs = [rng.randint(lo, hi) for _ in range(d)]
+            if rng.random() < 0.4:
+                coeffs[rng.randrange(d)] = lo
+            if rng.random() < 0.4:
+                coeffs[rng.randrange(d)] = hi
+        if any(coeffs):
+            return tc.IntPolynomial.from_coefficients(coeffs, bit_width=nbits)
+
+
+# ---------------------------------------------------------------- field / NTT
+
+def test_modmul_probe_matches_bigint():
+    rng = np.random.default_rng(99)
+    for spec in gpu_prime_table()[:4]:
+        p = spec.p
+        a = rng.integers(0, p, size=5000, dtype=np.uint64).astype(np.uint32)
+        b = rng.integers(0, p, size=5000, dtype=np.uint64).astype(np.uint32)
+        got = seams.modmul(p, a, b, mode=0)
+        exp = (a.astype(object) * b.astype(object)) % p
+        assert np.array_equal(got.astype(object), exp)
+        got = seams.modmul(p, a, b, mode=1)
+        rinv = pow(1 << 32, -1, p)
+        exp = (a.astype(object) * b.astype(object) * rinv) % p
+        assert np.array_equal(got.astype(object), exp)
+
+
+def test_ntt_probe_delta_inverse_linearity():
+    # pkg/tests/test_ntt2d.py:36-81 restated for the device transform
+    rng = random.Random(17)
+    spec = gpu_prime_table()[0]
+    p, g = spec.p, spec.generator
+    for logn in range(1, 14):
+        n = 1 << logn
+        delta = np.zeros(n, dtype=np.uint32)
+        delta[0] = 1
+        assert np.all(seams.ntt(delta, p, g) == 1)
+        v = np.array([rng.randrange(p) for _ in range(n)], dtype=np.uint32)
+        assert np.array_equal(seams.ntt(seams.ntt(v, p, g), p, g, inverse=True), v)
+    n = 64
+    u = np.array([rng.randrange(p) for _ in range(n)], dtype=np.uint64)
+    w = np.array([rng.randrange(p) for _ in range(n)], dtype=np.uint64)
+    al, be = rng.randrange(p), rng.randrange(p)
+    mix = ((al * u.astype(object) + be * w.astype(object)) % p).astype(np.uint32)
+    fu, fw, fm = (seams.ntt(x.astype(np.uint32), p, g).astype(object) for x in (u, w, mix))
+    assert all((al * x + be * y) % p == z for x, y, z in zip(fu, fw, fm))
+
+
+# ---------------------------------------------------------------- ConvertIn
+
+def test_digits_match_reference_golden():
+    meta, arr = load_golden("digits")
+    for m in meta:
+        words = arr[f"d{m['id']}_in"]
+        poly = _poly(words, m["bits"])
+        if m["error"]:
+            with pytest.raises(tc.EncodingError):
+                seams.digits(poly, m["K"], m["M"])
+            continue
+        got = seams.digits(poly, m["K"], m["M"])
+        assert np.array_equal(got, arr[f"d{m['id']}_digits"]), m
+
+
+def test_digits_match_oracle_wide_rows(oracle):
+    # long carry chains across warps and rounds: K up to 8192, all-ones rows
+    rng = np.random.default_rng(3)
+    for K, M, d in ((8192, 33, 3), (2048, 33, 5), (64, 63, 40), (1, 40, 70), (4096, 17, 2)):
+        N = K * M
+        nl = -(-N // 64)
+        words = rng.integers(0, 2**64 - 1, endpoint=True, size=(d, nl), dtype=np.uint64)
+        words[0, :] = np.uint64(0xFFFFFFFFFFFFFFFF)
+        if d > 2:
+            words[2, :] = 0
+        # clear bits >= N-2 so every row is within capacity, keep sign extension
+        top = (N - 2)
+        for i in range(d):
+            v = int.from_bytes(words[i].tobytes(), "little") & ((1 << top) - 1)
+            if i % 2:
+                v -= 1 << (top - 1)
+            words[i] = np.frombuffer((v & ((1 << (64 * nl)) - 1)).to_bytes(8 * nl, "little"), dtype=np.uint64)
+        plan = oracle.MulPlan(d=d, N=N, K=K, M=M, s_y=1, primes=(), e=0, f=0)
+        exp = oracle.digits(words, N, plan)
+        got = seams.digits(_poly(words, N), K, M)
+        assert np.array_equal(got, exp), (K, M)
+
+
+# ---------------------------------------------------------------- convolutions / CRT
+
+def test_c_plus_minus_match_reference_golden():
+    meta, arr = load_golden("cpm")
+    for m in meta:
+        n, d, K, M = m["id"], m["d"], m["K"], m["M"]
+        da, db = arr[f"m{n}_a"], arr[f"m{n}_b"]
+        mk = lambda dg: tc.IntPolynomial.from_coefficients(
+            [sum(int(x) << (M * j) for j, x in enumerate(row)) for row in dg], bit_width=K * M)
+        a, b = mk(da), mk(db)
+        if a.is_zero() or b.is_zero():
+            continue
+        plan = plan_gpu(d, d, K * M, K=K, M=M)
+        full, _ = seams.bivariate_product(a, b, plan)
+        cp, cm = seams.fold_c_plus_minus(full, K)
+        e = m["plan"]["e"]
+        assert np.array_equal(seams.ints_to_limbs(cp, e), arr[f"m{n}_cp"]), m
+        assert np.array_equal(seams.ints_to_limbs(cm, e), arr[f"m{n}_cm"]), m
+
+
+def test_bivariate_product_vs_naive(oracle):
+    rng = random.Random(31)
+    for _ in range(20):
+        d = rng.randint(1, 9)
+        K = rng.choice([1, 2, 4, 8])
+        M = rng.randint(2, 40)
+        half = 1 << (M - 1)
+        dg = lambda: np.array([[rng.randint(-half, half - 1) for _ in range(K)] for _ in range(d)],
+                              dtype=np.int64)
+        A, B = dg(), dg()
+        mk = lambda x: tc.IntPolynomial.from_coefficients(
+            [sum(int(v) << (M * j) for j, v in enumerate(row)) for row in x], bit_width=K * M)
+        a, b = mk(A), mk(B)
+        if a.is_zero() or b.is_zero():
+            continue
+        full, plan = seams.bivariate_product(a, b, plan_gpu(d, d, K * M, K=K, M=M))
+        exp = oracle.naive_bivariate(A, B, K)
+        assert [row[:2 * K - 1] for row in full] == exp
+        assert all(row[2 * K - 1] == 0 for row in full)
+
+
+# ---------------------------------------------------------------- products
+
+def test_products_match_reference_golden():
+    meta, arr = load_golden("products")
+    for m in meta:
+        a = _poly(arr[f"c{m['id']}_a"], m["a_bits"])
+        b = _poly(arr[f"c{m['id']}_b"], m["b_bits"])
+        out = tc.multiply(tc.MulRequest(a, b, prime_count=m["prime_count"]))
+        assert out.bit_width == m["out_bits"]
+        assert np.array_equal(out.words, arr[f"c{m['id']}_out"]), m
+
+
+def test_products_match_oracle_random(oracle):
+    rng = random.Random(8080)
+    for _ in range(40):
+        a = _random_poly(rng, rng.randint(1, 300), rng.randint(1, 700))
+        b = _random_poly(rng, rng.randint(1, 300), rng.randint(1, 700))
+        out = tc.multiply(tc.MulRequest(a, b))
+        exp, bits = oracle.multiply_words(a.words, a.bit_width, b.words, b.bit_width)
+        assert out.bit_width == bits and np.array_equal(out.words, exp)
+
+
+def test_known_answers():
+    one = tc.IntPolynomial.from_coefficients([1])
+    assert tc.multiply(tc.MulRequest(one, one)).coefficients() == [1]
+    out = tc.multiply(tc.MulRequest(tc.IntPolynomial.from_coefficients([1, 1]),
+                                    tc.IntPolynomial.from_coefficients([-1, 1])))
+    assert out.coefficients() == [-1, 0, 1]
+    x = 3 ** 400
+    a = tc.IntPolynomial.from_coefficients([x])
+    b = tc.IntPolynomial.from_coefficients([-(5 ** 340)])
+    assert tc.multiply(tc.MulRequest(a, b)).coefficients() == [-x * 5 ** 340]
+    a = tc.IntPolynomial.from_coefficients([1, -2, 3])
+    b = tc.IntPolynomial.from_coefficients([5, 7])
+    assert tc.multiply(tc.MulRequest(a, b)).coefficients() == [5, -3, 1, 21]
+
+
+def test_extremes_mixed_widths_and_invariance(oracle):
+    rng = random.Random(7)
+    for d, nbits in ((1, 8), (5, 16), (17, 64), (33, 1025), (3, 4097)):
+        a = _random_poly(rng, d, nbits, extremes=True)
+        out = tc.multiply(tc.MulRequest(a, a))
+        exp, bits = oracle.multiply_words(a.words, a.bit_width, a.words, a.bit_width)
+        assert np.array_equal(out.words, exp)
+    a = _random_poly(rng, 9, 300)
+    b = _random_poly(rng, 4, 3)
+    for x, y in ((a, b), (b, a)):
+        exp, _ = oracle.multiply_words(x.words, x.bit_width, y.words, y.bit_width)
+        assert np.array_equal(tc.multiply(tc.MulRequest(x, y)).words, exp)
+    a = _random_poly(rng, 40, 120)
+    b = _random_poly(rng, 37, 120)
+    base = tc.multiply(tc.MulRequest(a, b))
+    for pc in (1, 2, 3):
+        for w in (None, 1, 2, 8):
+            assert tc.multiply(tc.MulRequest(a, b, prime_count=pc, worker_hint=w)) == base
+
+
+def test_explicit_plans_agree():
+    rng = random.Random(21)
+    a = _random_poly(rng, 200, 500)
+    b = _random_poly(rng, 150, 500)
+    base = tc.multiply(tc.MulRequest(a, b))
+    for K in (1, 2, 8, 32, 128, 512):
+        out, _, plan = tc.multiply_with_plan(tc.MulRequest(a, b), K=K)
+        assert out == base, plan.describe()
+
+
+def test_errors():
+    zero = tc.IntPolynomial.from_coefficients([0, 0])
+    with pytest.raises(tc.EmptyInputError):
+        tc.multiply(tc.MulRequest(zero, tc.IntPolynomial.from_coefficients([1])))
+    a = tc.IntPolynomial.from_coefficients([1, 2])
+    with pytest.raises(ValueError):
+        tc.multiply(tc.MulRequest(a, a, prime_count=4))
+    # prime_count=1 plans like the reference (which recovers this with one
+    # 63-bit prime at M=16) and never changes the product
+    big = tc.IntPolynomial.from_coefficients([(1 << 1999) - 1] * 64)
+    assert tc.multiply(tc.MulRequest(big, big, prime_count=1)) == tc.multiply(tc.MulRequest(big, big))
+
+
+def test_stats_accounting():
+    rng = random.Random(41)
+    a = _random_poly(rng, 256, 256)
+    b = _random_poly(rng, 256, 256)
+    poly, stats = tc.multiply_with_stats(tc.MulRequest(a, b, worker_hint=2))
+    assert stats.workers == 2
+    assert poly == tc.multiply(tc.MulRequest(a, b))
+    assert stats.total > 0 and stats.stage_sum() <= stats.total
+
+
+# ---------------------------------------------------------------- full BASELINE sizes
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C4", "C5", "C3"])
+def test_full_config_matches_reference_hash(name, oracle):
+    cfg = json.load(open(os.path.join(GOLDEN, "configs.json")))[name]
+    (aw, ab), (bw, bb) = workloads.make_inputs(name)
+    assert workloads.words_sha256(aw) == cfg["a_sha256"]
+    a, b = tc.IntPolynomial._trusted(aw, ab), tc.IntPolynomial._trusted(bw, bb)
+    out = tc.multiply(tc.MulRequest(a, b))
+    assert out.bit_width == cfg["out_bits"] and list(out.words.shape) == cfg["out_shape"]
+    assert workloads.words_sha256(out.words) == cfg["out_sha256"]
+    # size-independent property: c(r) == a(r) b(r) mod q
+    q, r = (1 << 61) - 1, 0x1234567890ABCDE
+    assert oracle.eval_mod(out.words, q, r) == oracle.eval_mod(aw, q, r) * oracle.eval_mod(bw, q, r) % q
