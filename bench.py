@@ -114,36 +114,35 @@ def _peaks():
 
 
 def stage_model(plan, da, db, a_cw, b_cw, out_cw):
-    """Algorithmic bytes and butterflies of each pipeline stage."""
+    """Algorithmic HBM bytes and radix-2 butterflies of each pipeline stage,
+    for the pass layout the library runs (params.pass_layout == make_geometry
+    in csrc/tc_api.cu).  Butterflies are the canonical count (zero padding
+    not pruned); bytes are one read of each input and one write of each output
+    of every kernel in the stage."""
+    from paper_1612_05778_b200.params import pass_layout
     P, L, s_y = plan.P, plan.L, plan.s_y
     S = s_y * L
     lgL = L.bit_length() - 1
     lgS = s_y.bit_length() - 1
     rows = da + db - 1
-    U = 9
-    npass = 0 if lgS == 0 else -(-lgS // U)
-    sizes = []
-    if npass:
-        base, extra = lgS // npass, lgS % npass
-        sizes = [base + (1 if i < extra else 0) for i in range(npass)]
-    u_last = sizes[-1] if sizes else 0
+    yl, high = pass_layout(lgL, lgS, P)
+    low_bits = lgL + yl
+    g = 4 * P * S                      # one sweep over one operand's P grids
     st = {}
-    st["convert"] = dict(bytes=(da * a_cw + db * b_cw) * 8 + (da + db) * L * 4 * P,
-                         bfly=(da + db) * P * (L // 2) * lgL)
-    fwd_b, fwd_f = 0, 0
-    for op_d, count in ((da, npass), (db, max(npass - 1, 0))):
-        for i in range(count):
-            fwd_b += 4 * P * ((op_d * L if i == 0 else S) + S)
-            fwd_f += P * (S // 2) * sizes[i]
-    st["ntt_forward"] = dict(bytes=fwd_b, bfly=fwd_f)
-    st["pointwise"] = dict(bytes=4 * P * (3 * S if npass > 1 else (db * L + 2 * S)),
-                           bfly=2 * P * (S // 2) * u_last)
-    inv_b = 0
-    for i in range(npass - 1):
-        inv_b += 4 * P * (S + (rows * L if i == 0 else S))
-    inv_b += 2 * 4 * P * rows * L
-    st["ntt_inverse"] = dict(bytes=inv_b, bfly=P * (S // 2) * (lgS - u_last) + P * rows * (L // 2) * lgL)
-    st["recover"] = dict(bytes=4 * P * rows * (L - 1) + 8 * rows * out_cw, bfly=0)
+    st["convert"] = dict(bytes=(da * a_cw + db * b_cw) * 8 + 2 * g, bfly=2 * P * (S // 2) * low_bits)
+    fb = ff = 0
+    for i, (u0, U) in enumerate(high):
+        for op in ("A", "B"):
+            if op == "B" and i == len(high) - 1:
+                continue
+            fb += 2 * g
+            ff += P * (S // 2) * U
+    st["ntt_forward"] = dict(bytes=fb, bfly=ff)
+    u_last = high[-1][1] if high else 0
+    st["pointwise"] = dict(bytes=3 * g, bfly=2 * P * (S // 2) * u_last)
+    st["ntt_inverse"] = dict(bytes=2 * g * max(len(high) - 1, 0),
+                             bfly=sum(P * (S // 2) * U for (_, U) in high[:-1]))
+    st["recover"] = dict(bytes=g + 8 * rows * out_cw, bfly=P * (S // 2) * low_bits)
     return st
 
 

@@ -238,144 +238,134 @@ int make_crt_const(const tc_plan_t* pl, int64_t dmin, CrtConst* cc) {
 }
 
 struct Geometry {
-    int64_t K, L, s_y, S; int lgL, lgK, lgS; int P;
+    int64_t K, L, s_y, S;
+    int lgL, lgK, lgS, P;
+    int yl;                                    // y levels inside k_low / k_final tiles
+    std::vector<std::pair<int, int>> high;     // (u0, U) of the k_high passes, ascending
 };
 
-std::vector<std::pair<int, int>> y_passes(int lgS) {   // (u0, U), forward (descending) order
-    std::vector<std::pair<int, int>> v;
-    if (lgS == 0) return v;
-    const int UMAX = 9;
-    int np = (lgS + UMAX - 1) / UMAX;
-    int base = lgS / np, extra = lgS % np;
-    int top = lgS;
-    for (int i = 0; i < np; ++i) {
-        int U = base + (i < extra ? 1 : 0);
-        v.push_back({top - U, U});
-        top -= U;
+// Pass layout: k_final keeps P tiles of 2^(lgL+yl) words in shared memory
+// (<= 96 KiB when possible), k_low tiles are the same size, and the remaining
+// y levels go to balanced k_high passes of <= 2^14-word tiles.
+int make_geometry(const tc_plan_t* pl, Geometry& G) {
+    G.K = pl->K; G.L = 2 * pl->K; G.s_y = pl->s_y; G.S = G.s_y * G.L;
+    G.lgL = ilog2(G.L); G.lgK = ilog2(G.K); G.lgS = ilog2(G.s_y); G.P = pl->P;
+    if (G.lgL + G.lgS > 31) return set_err(TC_ERR_BAD_ARG, "grid of 2^%d slots exceeds 2^31", G.lgL + G.lgS);
+    const int64_t budget = 96 * 1024;
+    int tb = 0;
+    while ((int64_t)4 * G.P * (2ll << tb) <= budget) ++tb;   // largest tile_bits within budget
+    if (tb > 13) tb = 13;
+    int yl = tb - G.lgL;
+    if (yl < 0) yl = 0;
+    if (yl > G.lgS) yl = G.lgS;
+    G.yl = yl;
+    const int64_t fin = (int64_t)4 * G.P * padded_words((uint32_t)(1u << (G.lgL + yl)));
+    if (fin > 220 * 1024)
+        return set_err(TC_ERR_BAD_ARG, "P*L = %d*%lld words exceed the final tile's shared memory",
+                       G.P, (long long)G.L);
+    G.high.clear();
+    const int nlev = G.lgS - yl;
+    if (nlev > 0) {
+        const int cb = G.lgL + yl < 4 ? G.lgL + yl : 4;
+        const int UH = 14 - cb;
+        const int np = (nlev + UH - 1) / UH;
+        const int base = nlev / np, extra = nlev % np;
+        int u = yl;
+        for (int i = 0; i < np; ++i) {
+            const int U = base + (i < extra ? 1 : 0);
+            G.high.push_back({u, U});
+            u += U;
+        }
     }
-    return v;
-}
-
-int launch_pass(Ctx* c, int kind /*0 fwd,1 inv,2 mid*/, const Geometry& G, uint32_t* grids,
-                const uint32_t* other, const uint2* tw, const uint2* twi, int u0, int U,
-                int64_t valid_rows, int64_t store_rows) {
-    PassArgs A{};
-    A.grids = grids; A.S = G.S; A.lgL = G.lgL; A.lgS = G.lgS; A.u0 = u0; A.U = U;
-    A.cb = G.lgL + u0 < 4 ? G.lgL + u0 : 4;
-    A.tw = tw; A.tw_stride = G.s_y > 1 ? G.s_y / 2 : 1;
-    A.pcs = c->pcs.as<PrimeC>();
-    A.valid_rows = valid_rows; A.store_rows = store_rows;
-    A.other = other; A.tw_inv = twi;
-    const int n = 1 << (U + A.cb);
-    const int64_t ctas = G.S / n;
-    int threads = n / 2 < 512 ? n / 2 : 512;
-    if (threads < 32) threads = 32;
-    const size_t smem = (size_t)n * 4;
-    dim3 grid((unsigned)ctas, (unsigned)G.P);
-    if (kind == 0) k_ypass<0><<<grid, threads, smem, c->st>>>(A);
-    else if (kind == 1) k_ypass<1><<<grid, threads, smem, c->st>>>(A);
-    else k_ymid<<<grid, threads, smem, c->st>>>(A);
-    c->launches++;
-    CKL();
     return TC_OK;
 }
 
-int launch_convert(Ctx* c, const Geometry& G, const uint64_t* words, int64_t d, int cw, int M, int64_t N,
-                   int check_range, uint32_t* grids, int64_t* digits_out) {
-    ConvertArgs a{};
-    a.words = words; a.d = d; a.cw = cw;
-    a.K = G.K; a.lgK = G.lgK; a.M = M; a.N = N;
-    a.lgL = G.lgL;
-    a.R = (int)(G.K >= 2048 ? 1 : 2048 / G.K);
-    if (a.R > d) a.R = (int)d;
-    a.check_range = check_range;
-    a.grids = grids; a.S = G.S;
-    a.twx = c->twx_f.as<uint2>();
+int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* words, int64_t d, int cw,
+               int check_range, uint32_t* grids) {
+    LowArgs a{};
+    a.src.words = words; a.src.d = d; a.src.cw = cw;
+    a.src.K = G.K; a.src.lgK = G.lgK; a.src.M = (int)pl->M; a.src.N = pl->N;
+    a.src.check_range = check_range; a.src.err = c->flags.as<int>();
+    a.lgL = G.lgL; a.lgS = G.lgS; a.yl = G.yl;
+    a.g = grids; a.S = G.S;
+    a.twx = c->twx_f.as<uint2>(); a.twy = c->twy_f.as<uint2>();
+    a.twy_stride = G.s_y > 1 ? G.s_y / 2 : 1;
     a.pcs = c->pcs.as<PrimeC>(); a.P = G.P;
-    a.err = c->flags.as<int>();
-    a.digits_out = digits_out;
-    const size_t smem = (size_t)a.R * G.K * 8 + (size_t)a.R * G.L * 4;
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_convert_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t ctas = (d + a.R - 1) / a.R;
-    k_convert_x<<<(unsigned)ctas, 256, smem, c->st>>>(a);
+    const int R = 1 << G.yl;
+    const uint32_t n = 1u << (G.lgL + G.yl);
+    const size_t smem = (size_t)R * G.K * 8 + (size_t)R * 8 + (size_t)padded_words(n) * 4;
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_low, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t ctas = G.S / n;
+    k_low<<<(unsigned)ctas, 512, smem, c->st>>>(a);
     c->launches++;
     CKL();
     return TC_OK;
 }
 
-int launch_xinv(Ctx* c, const Geometry& G, uint32_t* grids, int64_t rows) {
-    int R = (int)(G.L >= 4096 ? 1 : 4096 / G.L);
-    if (R > rows) R = (int)rows;
-    const size_t smem = (size_t)R * G.L * 4;
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_xinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dim3 grid((unsigned)((rows + R - 1) / R), (unsigned)G.P);
-    k_xinv<<<grid, 256, smem, c->st>>>(grids, G.S, G.lgL, R, rows, c->twx_i.as<uint2>(), c->pcs.as<PrimeC>());
-    c->launches++;
-    CKL();
-    return TC_OK;
-}
-
-template <int P>
-int launch_crt_out_p(Ctx* c, const CrtOutArgs& A0, const CrtConst& cc, int64_t rows) {
-    CrtOutArgs A = A0;
-    const int rpc = 256 / A.tpr;
-    const size_t terms = ((size_t)rpc * A.max_terms * P + 1) & ~(size_t)1;
-    const size_t smem = terms * 4 + 256 * 8 + 256 * 4 + (((size_t)rpc + 1) & ~(size_t)1) * 4 + (size_t)rpc * 8;
-    if (smem > 227 * 1024) return set_err(TC_ERR_BAD_ARG, "ConvertOut tile needs %zu bytes of shared memory", smem);
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_crt_out<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t ctas = (rows + rpc - 1) / rpc;
-    k_crt_out<P><<<(unsigned)ctas, 256, smem, c->st>>>(A, cc);
-    c->launches++;
-    CKL();
-    return TC_OK;
-}
-
-int launch_crt_out(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows, int M, int W32,
-                   uint32_t* out, const CrtConst& cc) {
-    CrtOutArgs A{};
-    A.grids = grids; A.S = G.S; A.lgL = G.lgL; A.rows = rows; A.M = M; A.W32 = W32;
-    const int per = (W32 + kWPT - 1) / kWPT;
-    if (per <= 256) {
-        int t = 1; while (t < per) t <<= 1;
-        A.tpr = t; A.nchunks = 1;
+int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint32_t* other, int u0, int U) {
+    HighArgs A{};
+    A.g = grids; A.other = other; A.S = G.S;
+    A.lgL = G.lgL; A.lgS = G.lgS; A.u0 = u0; A.U = U;
+    A.cb = G.lgL + u0 < 4 ? G.lgL + u0 : 4;
+    A.twf = c->twy_f.as<uint2>(); A.twi = c->twy_i.as<uint2>();
+    A.tw_stride = G.s_y > 1 ? G.s_y / 2 : 1;
+    A.pcs = c->pcs.as<PrimeC>();
+    const uint32_t n = 1u << (U + A.cb);
+    const size_t smem = (size_t)padded_words(n) * 4;
+    int threads = (int)(n / 16 > 512 ? 512 : n / 16);
+    if (threads < 32) threads = 32;
+    dim3 grid((unsigned)(G.S / n), (unsigned)G.P);
+    if (mode == MODE_FWD) {
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_high<MODE_FWD><<<grid, threads, smem, c->st>>>(A);
+    } else if (mode == MODE_INV) {
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_high<MODE_INV><<<grid, threads, smem, c->st>>>(A);
     } else {
-        A.tpr = 256; A.nchunks = (W32 + 256 * kWPT - 1) / (256 * kWPT);
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_MID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_high<MODE_MID><<<grid, threads, smem, c->st>>>(A);
     }
-    A.max_terms = (int)(32ll * (A.tpr * kWPT + G.P) / M + 3);
+    c->launches++;
+    CKL();
+    return TC_OK;
+}
+
+template <int P, bool DUMP>
+int launch_final_p(Ctx* c, const Geometry& G, const FinalArgs& A, const CrtConst& cc) {
+    const uint32_t n = 1u << (G.lgL + G.yl);
+    const size_t smem = (size_t)P * padded_words(n) * 4;
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_final<P, DUMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_final<P, DUMP><<<(unsigned)(G.S / n), 512, smem, c->st>>>(A, cc);
+    c->launches++;
+    CKL();
+    return TC_OK;
+}
+
+int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows, int M, int W32,
+                 uint32_t* out, const CrtConst& cc, bool dump) {
+    FinalArgs A{};
+    A.g = grids; A.S = G.S; A.lgL = G.lgL; A.lgS = G.lgS; A.yl = G.yl;
+    A.twx = c->twx_i.as<uint2>(); A.twy = c->twy_i.as<uint2>();
+    A.twy_stride = G.s_y > 1 ? G.s_y / 2 : 1;
+    A.pcs = c->pcs.as<PrimeC>();
+    A.rows_out = rows; A.M = M; A.minv = (uint32_t)(0xffffffffu / (uint32_t)M); A.W32 = W32;
     A.out = out; A.err = c->flags.as<int>();
+#define CASE(k) case k: return dump ? launch_final_p<k, true>(c, G, A, cc) : launch_final_p<k, false>(c, G, A, cc);
     switch (G.P) {
-#define CASE(n) case n: return launch_crt_out_p<n>(c, A, cc, rows);
         CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
         CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
-#undef CASE
     }
+#undef CASE
     return set_err(TC_ERR_BAD_ARG, "P=%d unsupported", G.P);
 }
 
-int launch_crt_dump(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows, uint32_t* out,
-                    const CrtConst& cc) {
-    const int64_t n = rows * G.L;
-    const unsigned blocks = (unsigned)((n + 255) / 256);
-    int* err = c->flags.as<int>();
-    switch (G.P) {
-#define CASE(k) case k: k_crt_dump<k><<<blocks, 256, 0, c->st>>>(grids, G.S, G.lgL, rows, out, err, cc); break;
-        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
-        CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
-#undef CASE
-        default: return set_err(TC_ERR_BAD_ARG, "P=%d unsupported", G.P);
-    }
-    c->launches++;
-    CKL();
-    return TC_OK;
-}
-
-// The transform part of the pipeline, shared by tc_execute and
-// tc_bivariate_product: leaves exact c_ij mod p_q in the B grids (rows < rows).
-int run_transforms(Ctx* c, const tc_plan_t* pl, int a_bits, int b_bits, Geometry& G, int64_t rows,
-                   uint32_t** result_grids) {
+// The whole product on the device: leaves the product words (or, with
+// dump, the exact c_ij limbs) in `out`.  Events 0..5 bracket the stages.
+int run_pipeline(Ctx* c, const tc_plan_t* pl, int a_bits, int b_bits, int64_t rows, int W32,
+                 uint32_t* out, bool dump, const CrtConst& cc) {
     int rc;
-    G.K = pl->K; G.L = 2 * pl->K; G.s_y = pl->s_y; G.S = G.s_y * G.L;
-    G.lgL = ilog2(G.L); G.lgK = ilog2(G.K); G.lgS = ilog2(G.s_y); G.P = pl->P;
+    Geometry G;
+    if ((rc = make_geometry(pl, G))) return rc;
     if ((rc = ensure_twiddles(c, pl))) return rc;
     if ((rc = c->grids.ensure((size_t)2 * G.P * G.S * 4))) return rc;
     std::vector<PrimeC> pcs(G.P);
@@ -387,39 +377,32 @@ int run_transforms(Ctx* c, const tc_plan_t* pl, int a_bits, int b_bits, Geometry
 
     uint32_t* GA = c->grids.as<uint32_t>();
     uint32_t* GB = GA + (size_t)G.P * G.S;
-    const uint2* tyf = c->twy_f.as<uint2>();
-    const uint2* tyi = c->twy_i.as<uint2>();
+    const int nh = (int)G.high.size();
+    int64_t l0 = c->launches;
 
     CK(cudaEventRecord(c->ev[0], c->st));
-    const int64_t nA = c->a_cw, nB = c->b_cw;
-    (void)nA; (void)nB;
-    if ((rc = launch_convert(c, G, c->a_dev, c->da, c->a_cw, (int)pl->M, pl->N, a_bits > pl->N, GA, nullptr))) return rc;
-    if ((rc = launch_convert(c, G, c->b_dev, c->db, c->b_cw, (int)pl->M, pl->N, b_bits > pl->N, GB, nullptr))) return rc;
+    if ((rc = launch_low(c, G, pl, c->a_dev, c->da, c->a_cw, a_bits > pl->N, GA))) return rc;
+    if ((rc = launch_low(c, G, pl, c->b_dev, c->db, c->b_cw, b_bits > pl->N, GB))) return rc;
+    c->stage_launches[0] = c->launches - l0; l0 = c->launches;
     CK(cudaEventRecord(c->ev[1], c->st));
-
-    auto passes = y_passes(G.lgS);
-    const int np = (int)passes.size();
-    // operand A: every forward pass; operand B: all but the innermost
-    for (int i = 0; i < np; ++i)
-        if ((rc = launch_pass(c, 0, G, GA, nullptr, tyf, nullptr, passes[i].first, passes[i].second,
-                              i == 0 ? c->da : G.s_y, G.s_y))) return rc;
-    for (int i = 0; i + 1 < np; ++i)
-        if ((rc = launch_pass(c, 0, G, GB, nullptr, tyf, nullptr, passes[i].first, passes[i].second,
-                              i == 0 ? c->db : G.s_y, G.s_y))) return rc;
+    for (int i = 0; i < nh; ++i)
+        if ((rc = launch_high(c, MODE_FWD, G, GA, nullptr, G.high[i].first, G.high[i].second))) return rc;
+    for (int i = 0; i + 1 < nh; ++i)
+        if ((rc = launch_high(c, MODE_FWD, G, GB, nullptr, G.high[i].first, G.high[i].second))) return rc;
+    c->stage_launches[1] = c->launches - l0; l0 = c->launches;
     CK(cudaEventRecord(c->ev[2], c->st));
-    if (np == 0) {
-        if ((rc = launch_pass(c, 2, G, GB, GA, tyf, tyi, 0, 0, c->db, G.s_y))) return rc;
-    } else {
-        if ((rc = launch_pass(c, 2, G, GB, GA, tyf, tyi, passes[np - 1].first, passes[np - 1].second,
-                              np == 1 ? c->db : G.s_y, G.s_y))) return rc;
-    }
+    if (nh > 0) rc = launch_high(c, MODE_MID, G, GB, GA, G.high[nh - 1].first, G.high[nh - 1].second);
+    else rc = launch_high(c, MODE_MID, G, GB, GA, G.lgS, 0);
+    if (rc) return rc;
+    c->stage_launches[2] = c->launches - l0; l0 = c->launches;
     CK(cudaEventRecord(c->ev[3], c->st));
-    for (int i = np - 2; i >= 0; --i)
-        if ((rc = launch_pass(c, 1, G, GB, nullptr, tyi, nullptr, passes[i].first, passes[i].second,
-                              G.s_y, i == 0 ? rows : G.s_y))) return rc;
-    if ((rc = launch_xinv(c, G, GB, rows))) return rc;
+    for (int i = nh - 2; i >= 0; --i)
+        if ((rc = launch_high(c, MODE_INV, G, GB, nullptr, G.high[i].first, G.high[i].second))) return rc;
+    c->stage_launches[3] = c->launches - l0; l0 = c->launches;
     CK(cudaEventRecord(c->ev[4], c->st));
-    *result_grids = GB;
+    if ((rc = launch_final(c, G, GB, rows, (int)pl->M, W32, out, cc, dump))) return rc;
+    c->stage_launches[4] = c->launches - l0;
+    CK(cudaEventRecord(c->ev[5], c->st));
     return TC_OK;
 }
 
@@ -519,9 +502,6 @@ int tc_execute(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32_t b_bits,
     CrtConst cc;
     const int64_t dmin = c->da < c->db ? c->da : c->db;
     if ((rc = make_crt_const(plan, dmin, &cc))) return rc;
-    Geometry G;
-    uint32_t* R = nullptr;
-    if ((rc = run_transforms(c, plan, a_bits, b_bits, G, rows, &R))) return rc;
     uint32_t* dout;
     if (out_on_device) {
         dout = reinterpret_cast<uint32_t*>(out);
@@ -529,8 +509,7 @@ int tc_execute(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32_t b_bits,
         if ((rc = c->outbuf.ensure((size_t)rows * out_cw * 8))) return rc;
         dout = c->outbuf.as<uint32_t>();
     }
-    if ((rc = launch_crt_out(c, G, R, rows, (int)plan->M, 2 * out_cw, dout, cc))) return rc;
-    CK(cudaEventRecord(c->ev[5], c->st));
+    if ((rc = run_pipeline(c, plan, a_bits, b_bits, rows, 2 * out_cw, dout, false, cc))) return rc;
     if (!out_on_device)
         CK(cudaMemcpyAsync(out, dout, (size_t)rows * out_cw * 8, cudaMemcpyDeviceToHost, c->st));
     CK(cudaEventRecord(c->ev[6], c->st));
@@ -578,16 +557,21 @@ int tc_digits(void* ctx, int32_t which, int64_t K, int64_t M, int64_t N, int32_t
     const uint64_t* w = which ? c->b_dev : c->a_dev;
     const int64_t d = which ? c->db : c->da;
     const int cw = which ? c->b_cw : c->a_cw;
-    Geometry G{};
-    G.K = K; G.L = 2 * K; G.lgK = ilog2(K); G.lgL = ilog2(2 * K); G.P = 0; G.s_y = 1; G.S = 0;
     int rc;
     if ((rc = c->flags.ensure(64))) return rc;
     CK(cudaMemsetAsync(c->flags.p, 0x7f, 64, c->st));
     if ((rc = c->dbg.ensure((size_t)d * K * 8 + 64))) return rc;
     int64_t* dd = reinterpret_cast<int64_t*>(c->dbg.as<char>() + 64);
-    if ((rc = c->pcs.ensure(sizeof(PrimeC)))) return rc;
-    if ((rc = c->twx_f.ensure(16))) return rc;
-    if ((rc = launch_convert(c, G, w, d, cw, (int)M, N, in_bits > N, nullptr, dd))) return rc;
+    DigitSrc src{};
+    src.words = w; src.d = d; src.cw = cw; src.K = K; src.lgK = ilog2(K); src.M = (int)M; src.N = N;
+    src.check_range = in_bits > N; src.err = c->flags.as<int>();
+    int R = (int)(K >= 2048 ? 1 : 2048 / K);
+    if (R > d) R = (int)d;
+    const size_t smem = (size_t)R * K * 8 + (size_t)R * 8;
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_digits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_digits<<<(unsigned)((d + R - 1) / R), 256, smem, c->st>>>(src, R, dd);
+    c->launches++;
+    CKL();
     CK(cudaMemcpyAsync(digits_out, dd, (size_t)d * K * 8, cudaMemcpyDeviceToHost, c->st));
     int f[4];
     if ((rc = read_flags(c, f))) return rc;
@@ -608,12 +592,9 @@ int tc_bivariate_product(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32
     CrtConst cc;
     const int64_t dmin = c->da < c->db ? c->da : c->db;
     if ((rc = make_crt_const(plan, dmin, &cc))) return rc;
-    Geometry G;
-    uint32_t* R = nullptr;
-    if ((rc = run_transforms(c, plan, a_bits, b_bits, G, rows, &R))) return rc;
-    const size_t bytes = (size_t)rows * G.L * G.P * 4;
+    const size_t bytes = (size_t)rows * 2 * plan->K * plan->P * 4;
     if ((rc = c->outbuf.ensure(bytes))) return rc;
-    if ((rc = launch_crt_dump(c, G, R, rows, c->outbuf.as<uint32_t>(), cc))) return rc;
+    if ((rc = run_pipeline(c, plan, a_bits, b_bits, rows, 0, c->outbuf.as<uint32_t>(), true, cc))) return rc;
     CK(cudaMemcpyAsync(coeffs_out, c->outbuf.p, bytes, cudaMemcpyDeviceToHost, c->st));
     int f[4];
     if ((rc = read_flags(c, f))) return rc;
@@ -642,9 +623,6 @@ int tc_ntt_probe(uint32_t p, uint32_t g, uint32_t* data, int64_t n, int32_t dir)
     if (!data || !is_pow2(n) || n > 8192 || p < 3 || p >= (1u << 30) || (p - 1) % n)
         return set_err(TC_ERR_BAD_ARG, "bad NTT probe arguments");
     if (n == 1) return TC_OK;
-    // A 1 x n grid transformed by the x-direction kernels: forward via the
-    // ConvertIn path is digit-based, so the probe uses dedicated launches of
-    // the shared butterflies through k_xinv (inverse) and a forward tile.
     void* ctx = nullptr;
     int rc = tc_ctx_create(-1, &ctx);
     if (rc) return rc;
@@ -653,37 +631,19 @@ int tc_ntt_probe(uint32_t p, uint32_t g, uint32_t* data, int64_t n, int32_t dir)
     pl.K = n / 2; pl.s_y = 1; pl.P = 1; pl.p[0] = p; pl.g[0] = g;
     rc = ensure_twiddles(c, &pl);
     if (!rc) rc = c->grids.ensure((size_t)n * 4);
-    if (!rc) rc = c->pcs.ensure(sizeof(PrimeC));
     if (!rc) {
         PrimeC pc = make_prime_const(p, n);
-        cudaMemcpy(c->pcs.p, &pc, sizeof pc, cudaMemcpyHostToDevice);
         cudaMemcpy(c->grids.p, data, (size_t)n * 4, cudaMemcpyHostToDevice);
-        Geometry G{};
-        G.K = n / 2; G.L = n; G.s_y = 1; G.S = n; G.lgL = ilog2(n); G.lgK = G.lgL - 1; G.lgS = 0; G.P = 1;
-        if (dir == 0) {
-            // forward: y-pass machinery with lgS = 0 is a no-op, so run the
-            // x-direction DIF as a pass over flattened bits [0, lgL).
-            PassArgs A{};
-            A.grids = c->grids.as<uint32_t>(); A.S = n; A.lgL = 0; A.lgS = G.lgL; A.u0 = 0; A.U = G.lgL; A.cb = 0;
-            A.tw = c->twx_f.as<uint2>(); A.tw_stride = n / 2; A.pcs = c->pcs.as<PrimeC>();
-            A.valid_rows = n; A.store_rows = n;
-            int threads = n / 2 < 512 ? (int)(n / 2) : 512;
-            if (threads < 32) threads = 32;
-            k_ypass<0><<<dim3(1, 1), threads, (size_t)n * 4, c->st>>>(A);
-        } else {
-            rc = launch_xinv(c, G, c->grids.as<uint32_t>(), 1);
-        }
+        const int lg = ilog2(n);
+        k_ntt_probe<<<1, 256, (size_t)padded_words((uint32_t)n) * 4, c->st>>>(
+            c->grids.as<uint32_t>(), lg, c->twx_f.as<uint2>(), c->twx_i.as<uint2>(), pc, dir);
         cudaError_t e = cudaStreamSynchronize(c->st);
-        if (!rc && e != cudaSuccess) rc = set_err(TC_ERR_CUDA, "probe: %s", cudaGetErrorString(e));
+        if (e != cudaSuccess) rc = set_err(TC_ERR_CUDA, "probe: %s", cudaGetErrorString(e));
         if (!rc) {
             std::vector<uint32_t> h(n);
             cudaMemcpy(h.data(), c->grids.p, (size_t)n * 4, cudaMemcpyDeviceToHost);
             const uint64_t ninv = inv_mod((uint32_t)(n % p), p);
-            for (int64_t i = 0; i < n; ++i) {
-                uint64_t v = h[i] % p;
-                if (dir == 1) v = v * ninv % p;
-                data[i] = (uint32_t)v;
-            }
+            for (int64_t i = 0; i < n; ++i) data[i] = (uint32_t)(dir == 1 ? h[i] * ninv % p : h[i]);
         }
     }
     tc_ctx_destroy(ctx);

@@ -1,21 +1,31 @@
 // tc_kernels.cuh -- the sm_100a kernels of the two-convolution product.
 //
-// Layout in HBM: per prime q, one operand grid is a row-major (s_y, L) array
-// of uint32 residues, L = 2K (row i = y-degree, column j = x-degree); the P
-// grids of an operand are contiguous ([P][s_y][L]).  Every 2-D transform is
-// an in-place sequence of radix-2 stages over the flattened index
-// f = i*L + j: x-stages touch bits [0, lgL), y-stages bits [lgL, lgL+lgS).
-// A "pass" loads a tile of 2^U stage-bit positions x 2^cb contiguous batch
-// elements into shared memory, runs U stages there and writes back.
+// Layout in HBM.  Per prime q, an operand grid is a row-major (s_y, L) array
+// of uint32 residues, L = 2K; the P grids of an operand are contiguous
+// ([P][s_y][L]).  Flattened index f = pos*L + j: x-stages act on bits
+// [0, lgL), y-stages on bits [lgL, lgL+lgS).  Rows are stored in BIT-REVERSED
+// order: coefficient i of an operand (and row i of the product) lives at row
+// position bitrev_lgS(i).  That lets the forward y-transform run as DIT
+// (bit-reversed in -> natural out, low bits first) and the inverse as DIF
+// (natural in -> bit-reversed out, high bits first), so
+//   * the FIRST forward pass holds whole rows: ConvertIn + every x-stage + the
+//     low y-stages in one kernel (k_low), and
+//   * the LAST inverse pass holds whole rows again: the low y-stages + every
+//     x-stage + CRT + ConvertOut in one kernel (k_final).
+// The high y-bits in between are covered by k_high passes; operand B's last
+// forward pass is fused with the pointwise product and the first inverse pass
+// (k_high<MODE_MID>).
+//
+// Inside a pass the tile lives in shared memory; each thread runs "rounds" of
+// up to 4 radix-2 stages on 16 elements held in registers (radix-16), so one
+// shared-memory round trip serves four stages.  All indexing is 32-bit
+// (S <= 2^31 per prime).
 //
 // Reference counterparts (tc/ = /root/reference/pkg/src/twoconv):
-//   k_convert_x    digits_rows + embed_rows(_scaled) + ntt_x_fwd   (tc/_kernels.py:78-164)
-//   k_ypass<0>     ntt_y_fwd                                        (tc/_kernels.py:186-205)
-//   k_ymid         last ntt_y_fwd pass + pointwise_rows + first ntt_y_inv pass (+ scale_rows' 1/S)
-//   k_ypass<1>     ntt_y_inv                                        (tc/_kernels.py:208-225)
-//   k_xinv         ntt_x_inv                                        (tc/_kernels.py:167-183)
-//   k_crt_out<P>   lift1/crt2/_combine_three + recover_rows         (tc/_kernels.py:258-423,
-//                                                                     tc/multiplier.py:66-128)
+//   k_low      digits_rows + embed_rows(_scaled) + ntt_x_fwd + first ntt_y_fwd stages
+//   k_high     ntt_y_fwd / ntt_y_inv passes; MID adds pointwise_rows + scale_rows' 1/S
+//   k_final    last ntt_y_inv stages + ntt_x_inv + lift1/crt2/_combine_three + recover_rows
+//              (tc/_kernels.py:78-423, tc/multiplier.py:66-160)
 #pragma once
 #include <stdint.h>
 #include "tc_field.cuh"
@@ -27,7 +37,6 @@ constexpr int kMaxPrimes = 16;
 // ---------------------------------------------------------------------------
 // Width scan: max two's-complement width and non-zero flag of a polynomial
 // (replaces the Python-int scans tc/params.py:290-293, tc/zpoly.py:103-114).
-// out[0] = max width (atomicMax), out[1] |= nonzero.
 // ---------------------------------------------------------------------------
 __global__ void k_width(const uint64_t* __restrict__ words, int64_t d, int cw, int* out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -52,10 +61,8 @@ __global__ void k_width(const uint64_t* __restrict__ words, int64_t d, int cw, i
     }
 }
 
-// ---------------------------------------------------------------------------
 // Twiddle tables: entry m < n/2 is {w^m, floor(w^m 2^32 / p)} for the order-n
 // root w (forward) and w^-1 (inverse) -- the roles of tc/modfield.py:78-99.
-// ---------------------------------------------------------------------------
 struct PowTable { uint32_t f[32]; uint32_t i[32]; };
 
 __global__ void k_twiddles(uint2* fwd, uint2* inv, int64_t half, uint32_t p, PowTable pw, int nb) {
@@ -68,74 +75,63 @@ __global__ void k_twiddles(uint2* fwd, uint2* inv, int64_t half, uint32_t p, Pow
     inv[m] = make_uint2((uint32_t)wi, (uint32_t)((wi << 32) / p));
 }
 
+__device__ __forceinline__ uint32_t bitrev(uint32_t x, int bits) {
+    return bits ? __brev(x) >> (32 - bits) : 0u;
+}
+
+// Padded shared-memory index: one spare word per 32 keeps the stride-16
+// accesses of radix-16 rounds on low bits conflict-free.
+__device__ __forceinline__ uint32_t padi(uint32_t e) { return e + (e >> 5); }
+__host__ __device__ constexpr uint32_t padded_words(uint32_t n) { return n + (n >> 5) + 1; }
+
 // ---------------------------------------------------------------------------
-// ConvertIn fused with the x-direction forward NTT.
-//
-// Balanced digits (tc/_kernels.py:78-119): chunk j of coefficient i is bits
-// [jM, jM+M) of its N-bit sign-extended value; cu = chunk + carry_j;
-// digit = cu >= 2^(M-1) ? cu - 2^M : cu with carry_{j+1} = [cu >= 2^(M-1)];
-// the top digit absorbs the sign.  The carry chain is a generate/propagate
-// scan: g_j = chunk >= half, p_j = chunk == half-1 (carry-out = g | p&cin).
-// Within a warp the carries come from one 64-bit add of the ballot masks
-// (A = g|p, B = g: carries = (A + B + cin) ^ A ^ B); across warps and rounds a
-// serial scan of per-warp transfer bits.  The top digit of every row has
-// g = p = 0, so the flat chain over the CTA's rows never crosses a row.
-//
-// Then per prime: digit mod p (the embed of tc/_kernels.py:122-141), row
-// zero-padded to L = 2K, radix-2 DIF over the row.  The first stage of the
-// length-2K DIF on a zero-padded row is (x_j, x_j * theta^j): the theta twist
-// of the negacyclic convolution (tc/modfield.py:119-152) is this stage.
-//
-// err[0]: first row whose top digit overflows (EncodingError, row index);
-// err[1]: first row outside the plan's N-bit range (tc/codec.py:78-83).
-// digits_out != nullptr: write the (d, K) int64 digits and stop (parity seam).
+// Balanced digits (tc/_kernels.py:78-119) for up to R rows of one CTA.
+// chunk j of coefficient i = bits [jM, jM+M) of its N-bit sign-extended
+// value; cu = chunk + carry_j; digit = cu >= 2^(M-1) ? cu - 2^M : cu with
+// carry_{j+1} = [cu >= 2^(M-1)]; the top digit absorbs the sign.  The carry
+// chain is a generate/propagate scan: g = chunk >= half, p = chunk == half-1.
+// Within a warp the carries of 32 digits come from one 64-bit add of the
+// ballot masks (A = g|p, B = g: carries = (A + B + cin) ^ A ^ B); across warps
+// and rounds a serial scan of per-warp transfer bits.  The top digit of every
+// row has g = p = 0, so the flat chain over the CTA's rows never crosses rows.
+// err[0]: first coefficient whose top digit overflows; err[1]: first
+// coefficient outside the plan's N-bit range (tc/codec.py:78-83).
 // ---------------------------------------------------------------------------
-struct ConvertArgs {
-    const uint64_t* words; int64_t d; int cw;      // input (d, cw)
-    int64_t K; int lgK; int M; int64_t N;          // digit split
-    int lgL; int R;                                // rows per CTA
+struct DigitSrc {
+    const uint64_t* words; int64_t d; int cw;
+    int64_t K; int lgK; int M; int64_t N;
     int check_range;
-    uint32_t* grids; int64_t S;                    // [P][s_y][L]
-    const uint2* twx;                              // [P][L/2]
-    const PrimeC* pcs; int P;
     int* err;
-    int64_t* digits_out;
 };
 
 __device__ __forceinline__ uint64_t limb_at(const uint64_t* row, int cw, int64_t k, uint64_t signw) {
     return k < cw ? row[k] : signw;
 }
 
-__global__ void __launch_bounds__(256) k_convert_x(ConvertArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    int64_t* dig = reinterpret_cast<int64_t*>(smem_raw);
-    uint32_t* tile = reinterpret_cast<uint32_t*>(dig + (int64_t)a.R * a.K);
-    __shared__ uint32_t warp_tf[32];
-    __shared__ uint32_t warp_cin[32];
-    __shared__ uint32_t round_carry;
+struct DigitScratch { uint32_t warp_tf[32]; uint32_t warp_cin[32]; uint32_t round_carry; };
 
+// coeff[r] (r < R) is the coefficient index held by tile row r, or -1.
+__device__ void compute_digits(const DigitSrc& a, int R, const int64_t* coeff, int64_t* dig,
+                               DigitScratch& ds) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    const int64_t r0 = (int64_t)blockIdx.x * a.R;
-    const int nrows = (int)min((int64_t)a.R, a.d - r0);
     const int M = a.M;
     const uint64_t half = 1ull << (M - 1);
     const uint64_t beta = 1ull << M;
     const uint64_t mask = beta - 1;
     const int64_t sq = (a.N - 1) >> 6;
     const int sr = (int)((a.N - 1) & 63);
-    const int64_t ndig = (int64_t)a.R * a.K;
+    const int64_t ndig = (int64_t)R * a.K;
 
-    if (tid == 0) round_carry = 0;
-    // N-bit range check (only when the declared width exceeds N).
-    for (int rr = tid; a.check_range && rr < nrows; rr += blockDim.x) {
-        const int64_t i = r0 + rr;
+    if (tid == 0) ds.round_carry = 0;
+    for (int rr = tid; a.check_range && rr < R; rr += blockDim.x) {
+        const int64_t i = coeff[rr];
+        if (i < 0) continue;
         const uint64_t* row = a.words + i * a.cw;
-        uint64_t signw = (row[a.cw - 1] >> 63) ? ~0ull : 0ull;
-        uint64_t s = (limb_at(row, a.cw, sq, signw) >> sr) & 1 ? ~0ull : 0ull;
+        const uint64_t signw = (row[a.cw - 1] >> 63) ? ~0ull : 0ull;
+        const uint64_t s = ((limb_at(row, a.cw, sq, signw) >> sr) & 1) ? ~0ull : 0ull;
         bool bad = false;
         for (int64_t k = sq; k < a.cw; ++k) {
-            uint64_t lim = row[k];
-            uint64_t expect = s;
+            uint64_t lim = row[k], expect = s;
             if (k == sq) { lim >>= sr; expect >>= sr; }
             if (lim != expect) { bad = true; break; }
         }
@@ -147,11 +143,12 @@ __global__ void __launch_bounds__(256) k_convert_x(ConvertArgs a) {
         const int64_t idx = base + tid;
         const int r = (int)(idx >> a.lgK);
         const int64_t j = idx & (a.K - 1);
-        const bool active = idx < ndig && r < nrows;
+        const int64_t ci = (idx < ndig) ? coeff[r] : -1;
+        const bool active = ci >= 0;
         uint64_t chunk = 0;
         bool neg = false;
         if (active) {
-            const uint64_t* row = a.words + (r0 + r) * a.cw;
+            const uint64_t* row = a.words + ci * a.cw;
             const uint64_t signw = (row[a.cw - 1] >> 63) ? ~0ull : 0ull;
             const int64_t off = j * M;
             const int64_t wq = off >> 6;
@@ -166,15 +163,15 @@ __global__ void __launch_bounds__(256) k_convert_x(ConvertArgs a) {
         const unsigned Pm = __ballot_sync(0xffffffffu, active && !top && chunk == half - 1);
         const uint64_t A = (uint64_t)(G | Pm), B = (uint64_t)G;
         if (lane == 0)
-            warp_tf[warp] = (uint32_t)((A + B) >> 32) | ((uint32_t)((A + B + 1) >> 32) << 1);
+            ds.warp_tf[warp] = (uint32_t)((A + B) >> 32) | ((uint32_t)((A + B + 1) >> 32) << 1);
         __syncthreads();
         if (tid == 0) {
-            uint32_t c = round_carry;
-            for (int w = 0; w < nwarps; ++w) { warp_cin[w] = c; c = (warp_tf[w] >> c) & 1u; }
-            round_carry = c;
+            uint32_t c = ds.round_carry;
+            for (int w = 0; w < nwarps; ++w) { ds.warp_cin[w] = c; c = (ds.warp_tf[w] >> c) & 1u; }
+            ds.round_carry = c;
         }
         __syncthreads();
-        const uint64_t cin = warp_cin[warp];
+        const uint64_t cin = ds.warp_cin[warp];
         const uint32_t carries = (uint32_t)((A + B + cin) ^ A ^ B);
         if (active) {
             const uint64_t cu = chunk + ((carries >> lane) & 1u);
@@ -182,197 +179,243 @@ __global__ void __launch_bounds__(256) k_convert_x(ConvertArgs a) {
             if (!top) {
                 dg = cu >= half ? -(int64_t)(beta - cu) : (int64_t)cu;
             } else if (neg) {
-                if (cu < half) atomicMin(&a.err[0], (int)min(r0 + r, (int64_t)0x7fffffff));
+                if (cu < half) atomicMin(&a.err[0], (int)min(ci, (int64_t)0x7fffffff));
                 dg = -(int64_t)(beta - cu);
             } else {
-                if (cu >= half) atomicMin(&a.err[0], (int)min(r0 + r, (int64_t)0x7fffffff));
+                if (cu >= half) atomicMin(&a.err[0], (int)min(ci, (int64_t)0x7fffffff));
                 dg = (int64_t)cu;
             }
             dig[idx] = dg;
         }
         __syncthreads();
     }
+}
 
-    if (a.digits_out) {
-        for (int64_t idx = tid; idx < (int64_t)nrows * a.K; idx += blockDim.x)
-            a.digits_out[r0 * a.K + idx] = dig[idx];
-        return;
-    }
-
-    const int L = 1 << a.lgL;
-    const int64_t nel = (int64_t)a.R * L;
-    for (int q = 0; q < a.P; ++q) {
-        const PrimeC pc = a.pcs[q];
-        const uint2* tw = a.twx + (int64_t)q * (L >> 1);
-        for (int64_t e = tid; e < nel; e += blockDim.x) {
-            const int r = (int)(e >> a.lgL);
-            const int64_t j = e & (L - 1);
-            tile[e] = (j < a.K && r < nrows) ? digit_residue(dig[(int64_t)r * a.K + j], pc) : 0u;
-        }
-        __syncthreads();
-        for (int t = a.lgL - 1; t >= 0; --t) {
-            const int h = 1 << t;
-            for (int64_t e = tid; e < (nel >> 1); e += blockDim.x) {
-                const int64_t r = e >> (a.lgL - 1);
-                const int pj = (int)(e & ((L >> 1) - 1));
-                const int jlo = ((pj >> t) << (t + 1)) | (pj & (h - 1));
-                const uint2 w = __ldg(&tw[(jlo & (h - 1)) << (a.lgL - 1 - t)]);
-                uint32_t* x = tile + r * L + jlo;
-                uint32_t u = x[0], v = x[h];
-                bfly_dif(u, v, w.x, w.y, pc.p, pc.two_p);
-                x[0] = u; x[h] = v;
-            }
-            __syncthreads();
-        }
-        uint32_t* g = a.grids + (int64_t)q * a.S + r0 * L;
-        for (int64_t e = tid; e < (int64_t)nrows * L; e += blockDim.x) g[e] = tile[e];
-        __syncthreads();
-    }
+// Parity seam: digits of coefficients [r0, r0+R) in natural order.
+__global__ void __launch_bounds__(256) k_digits(DigitSrc a, int R, int64_t* out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    int64_t* dig = reinterpret_cast<int64_t*>(smem_raw);
+    int64_t* coeff = dig + (int64_t)R * a.K;
+    __shared__ DigitScratch ds;
+    const int64_t r0 = (int64_t)blockIdx.x * R;
+    for (int r = threadIdx.x; r < R; r += blockDim.x) coeff[r] = r0 + r < a.d ? r0 + r : -1;
+    __syncthreads();
+    compute_digits(a, R, coeff, dig, ds);
+    const int64_t nrows = min((int64_t)R, a.d - r0);
+    for (int64_t idx = threadIdx.x; idx < nrows * a.K; idx += blockDim.x) out[r0 * a.K + idx] = dig[idx];
 }
 
 // ---------------------------------------------------------------------------
-// y-direction pass over stages u in [u0, u0+U) of the flattened transform.
-// DIR 0: forward DIF, stages descending (tc/_kernels.py:186-205).
-// DIR 1: inverse DIT, stages ascending (tc/_kernels.py:208-225).
-// Rows >= valid_rows load as zero (the zero padding above the input degree);
-// only rows < store_rows are written back.
+// Register-blocked rounds over a shared-memory tile.
+// A round applies NB consecutive radix-2 stages (tile bits [bit_lo,
+// bit_lo+NB)) to the 2^NB elements of each "group" (elements that differ only
+// in those bits), held in registers.  DIF runs the bits high-to-low, DIT
+// low-to-high.  The twiddle of a stage depends only on the lower element's
+// bits below the stage bit, so a level with 2^lv distinct twiddles loads each
+// once.  tw(e, bit) returns {w, w_shoup} for the lower element e at tile bit.
 // ---------------------------------------------------------------------------
-struct PassArgs {
-    uint32_t* grids; int64_t S;
-    int lgL, lgS, u0, U, cb;
-    const uint2* tw;  int64_t tw_stride;    // [P][s_y/2]
-    const PrimeC* pcs;
-    int64_t valid_rows, store_rows;
-    // k_ymid only:
-    const uint32_t* other;                  // fully transformed A grids
-    const uint2* tw_inv;
+template <int NB, bool DIF, class TW>
+__device__ __forceinline__ void round_exec(uint32_t* s, int tile_bits, int bit_lo, const TW& tw,
+                                           uint32_t p, uint32_t two_p) {
+    constexpr int R = 1 << NB;
+    const uint32_t ngroups = 1u << (tile_bits - NB);
+    const uint32_t lowmask = (1u << bit_lo) - 1;
+    for (uint32_t g = threadIdx.x; g < ngroups; g += blockDim.x) {
+        const uint32_t e0 = ((g & ~lowmask) << NB) | (g & lowmask);
+        uint32_t x[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) x[k] = s[padi(e0 + ((uint32_t)k << bit_lo))];
+#pragma unroll
+        for (int it = 0; it < NB; ++it) {
+            const int lv = DIF ? NB - 1 - it : it;
+#pragma unroll
+            for (int m = 0; m < (1 << lv); ++m) {
+                const uint2 w = tw(e0 + ((uint32_t)m << bit_lo), bit_lo + lv);
+#pragma unroll
+                for (int jj = 0; jj < R / (2 << lv); ++jj) {
+                    const int k = m + jj * (2 << lv);
+                    if (DIF) bfly_dif(x[k], x[k + (1 << lv)], w.x, w.y, p, two_p);
+                    else bfly_dit(x[k], x[k + (1 << lv)], w.x, w.y, p, two_p);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) s[padi(e0 + ((uint32_t)k << bit_lo))] = x[k];
+    }
+    __syncthreads();
+}
+
+template <bool DIF, class TW>
+__device__ __forceinline__ void round_dispatch(int nb, uint32_t* s, int tile_bits, int bit_lo, const TW& tw,
+                                               uint32_t p, uint32_t two_p) {
+    switch (nb) {
+        case 4: round_exec<4, DIF>(s, tile_bits, bit_lo, tw, p, two_p); break;
+        case 3: round_exec<3, DIF>(s, tile_bits, bit_lo, tw, p, two_p); break;
+        case 2: round_exec<2, DIF>(s, tile_bits, bit_lo, tw, p, two_p); break;
+        case 1: round_exec<1, DIF>(s, tile_bits, bit_lo, tw, p, two_p); break;
+        default: break;
+    }
+}
+
+// Stages on tile bits [lo, hi): DIT ascending in rounds of <= 4 bits, DIF descending.
+template <bool DIF, class TW>
+__device__ __forceinline__ void run_bits(uint32_t* s, int tile_bits, int lo, int hi, const TW& tw,
+                                         uint32_t p, uint32_t two_p) {
+    const int nbits = hi - lo;
+    if (nbits <= 0) return;
+    const int nr = (nbits + 3) / 4;
+    const int base = nbits / nr, extra = nbits % nr;
+    if (!DIF) {
+        int b = lo;
+        for (int r = 0; r < nr; ++r) {
+            const int nb = base + (r < extra ? 1 : 0);
+            round_dispatch<false>(nb, s, tile_bits, b, tw, p, two_p);
+            b += nb;
+        }
+    } else {
+        int b = hi;
+        for (int r = 0; r < nr; ++r) {
+            const int nb = base + (r < extra ? 1 : 0);
+            b -= nb;
+            round_dispatch<true>(nb, s, tile_bits, b, tw, p, two_p);
+        }
+    }
+}
+
+// Twiddles of a whole-row tile (k_low / k_final): tile index e = local_row*L + col.
+struct TwRows {
+    const uint2* twx; const uint2* twy; int lgL, lgS;
+    __device__ __forceinline__ uint2 operator()(uint32_t e, int bit) const {
+        if (bit < lgL) return __ldg(&twx[(e & ((1u << bit) - 1)) << (lgL - 1 - bit)]);
+        const int u = bit - lgL;
+        return __ldg(&twy[((e >> lgL) & ((1u << u) - 1)) << (lgS - 1 - u)]);
+    }
 };
 
-__device__ __forceinline__ int64_t pass_flat(int64_t base, int a, int b0, int c) {
-    return base | ((int64_t)a << b0) | c;
-}
+// Twiddles of a high-pass tile: e = (a << cb) | c, tile bit b >= cb is y level
+// u0 + (b - cb); the row bits below u0 come from the CTA's mid bits and c.
+struct TwHigh {
+    const uint2* twy; int lgL, lgS, u0, cb; uint32_t midc;
+    __device__ __forceinline__ uint2 operator()(uint32_t e, int bit) const {
+        const int l = bit - cb, u = u0 + l;
+        const uint32_t rb = (midc | (e & ((1u << cb) - 1))) >> lgL;
+        const uint32_t row = rb | (((e >> cb) & ((1u << l) - 1)) << u0);
+        return __ldg(&twy[row << (lgS - 1 - u)]);
+    }
+};
 
-template <int DIR>
-__device__ __forceinline__ void pass_stages(uint32_t* s, const PassArgs& A, int64_t base,
-                                            const uint2* tw, uint32_t p, uint32_t two_p) {
-    const int nC = 1 << A.cb, b0 = A.lgL + A.u0;
-    const int half_n = (1 << (A.U + A.cb)) >> 1;
-    for (int it = 0; it < A.U; ++it) {
-        const int ls = DIR == 0 ? A.U - 1 - it : it;
-        const int h = 1 << ls;
-        const int u = A.u0 + ls;
-        const int64_t umask = (1ll << u) - 1;
-        const int sh = A.lgS - 1 - u;
-        for (int e = threadIdx.x; e < half_n; e += blockDim.x) {
-            const int c = e & (nC - 1), pidx = e >> A.cb;
-            const int alo = ((pidx >> ls) << (ls + 1)) | (pidx & (h - 1));
-            const int64_t row = pass_flat(base, alo, b0, c) >> A.lgL;
-            const uint2 w = __ldg(&tw[(row & umask) << sh]);
-            uint32_t* x = s + ((alo << A.cb) | c);
-            uint32_t* y = x + (h << A.cb);
-            uint32_t xv = *x, yv = *y;
-            if (DIR == 0) bfly_dif(xv, yv, w.x, w.y, p, two_p);
-            else bfly_dit(xv, yv, w.x, w.y, p, two_p);
-            *x = xv; *y = yv;
+// ---------------------------------------------------------------------------
+// k_low: ConvertIn + x-direction forward NTT (DIF) + the low y stages (DIT) of
+// one operand, all primes.  CTA = 2^yl row positions x L columns.  The first
+// x-stage on a zero-padded row is (x_j, x_j * theta^j): the negacyclic twist.
+// ---------------------------------------------------------------------------
+struct LowArgs {
+    DigitSrc src;
+    int lgL, lgS, yl;
+    uint32_t* g; int64_t S;
+    const uint2* twx; const uint2* twy; int64_t twy_stride;
+    const PrimeC* pcs; int P;
+};
+
+__global__ void __launch_bounds__(512) k_low(LowArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int R = 1 << A.yl;
+    const int L = 1 << A.lgL;
+    const int tile_bits = A.lgL + A.yl;
+    const uint32_t n = 1u << tile_bits;
+    int64_t* dig = reinterpret_cast<int64_t*>(smem_raw);
+    int64_t* coeff = dig + (int64_t)R * A.src.K;
+    uint32_t* tile = reinterpret_cast<uint32_t*>(coeff + R);
+    __shared__ DigitScratch ds;
+    __shared__ int s_nvalid;
+    const uint32_t pos0 = blockIdx.x * (uint32_t)R;
+    if (threadIdx.x == 0) s_nvalid = 0;
+    __syncthreads();
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+        const int64_t i = bitrev(pos0 + r, A.lgS);
+        coeff[r] = i < A.src.d ? i : -1;
+        if (i < A.src.d) atomicAdd(&s_nvalid, 1);
+    }
+    __syncthreads();
+    if (s_nvalid == 0) {       // all rows of this tile are zero padding
+        for (int q = 0; q < A.P; ++q) {
+            uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)blockIdx.x * n;
+            for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) g[e] = 0u;
         }
+        return;
+    }
+    compute_digits(A.src, R, coeff, dig, ds);
+    for (int q = 0; q < A.P; ++q) {
+        const PrimeC pc = A.pcs[q];
+        for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
+            const uint32_t r = e >> A.lgL, j = e & (L - 1);
+            tile[padi(e)] = (j < A.src.K && coeff[r] >= 0) ? digit_residue(dig[(int64_t)r * A.src.K + j], pc) : 0u;
+        }
+        __syncthreads();
+        const TwRows tw{A.twx + (int64_t)q * (L >> 1), A.twy + (int64_t)q * A.twy_stride, A.lgL, A.lgS};
+        run_bits<true>(tile, tile_bits, 0, A.lgL, tw, pc.p, pc.two_p);          // x: DIF
+        run_bits<false>(tile, tile_bits, A.lgL, tile_bits, tw, pc.p, pc.two_p); // y low: DIT
+        uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)blockIdx.x * n;
+        for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) g[e] = tile[padi(e)];
         __syncthreads();
     }
 }
 
-__device__ __forceinline__ int64_t pass_base(const PassArgs& A) {
+// ---------------------------------------------------------------------------
+// k_high: y levels [u0, u0+U) over tiles of 2^U rows (stride 2^u0) x 2^cb
+// contiguous columns.  MODE_FWD: DIT with forward twiddles.  MODE_INV: DIF
+// with inverse twiddles.  MODE_MID: forward DIT, pointwise Montgomery product
+// with the finished A grid times (s_y L)^-1 (pointwise_rows + the constant of
+// scale_rows, tc/_kernels.py:228-242), then inverse DIF -- one read of each
+// grid and one write.
+// ---------------------------------------------------------------------------
+enum { MODE_FWD = 0, MODE_INV = 1, MODE_MID = 2 };
+
+struct HighArgs {
+    uint32_t* g; const uint32_t* other; int64_t S;
+    int lgL, lgS, u0, U, cb;
+    const uint2* twf; const uint2* twi; int64_t tw_stride;
+    const PrimeC* pcs;
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(512) k_high(HighArgs A) {
+    extern __shared__ __align__(16) uint32_t s[];
+    const int q = blockIdx.y;
+    uint32_t* g = A.g + (int64_t)q * A.S;
+    const PrimeC pc = A.pcs[q];
     const int b0 = A.lgL + A.u0;
     const int nmid = b0 - A.cb;
-    const int64_t cta = blockIdx.x;
-    const int64_t mid = cta & ((1ll << nmid) - 1);
-    const int64_t hi = cta >> nmid;
-    return (hi << (b0 + A.U)) | (mid << A.cb);
-}
-
-template <int DIR>
-__global__ void __launch_bounds__(512) k_ypass(PassArgs A) {
-    extern __shared__ __align__(16) uint32_t s[];
-    const int q = blockIdx.y;
-    uint32_t* g = A.grids + (int64_t)q * A.S;
-    const uint2* tw = A.tw + (int64_t)q * A.tw_stride;
-    const PrimeC pc = A.pcs[q];
-    const int64_t base = pass_base(A);
-    const int b0 = A.lgL + A.u0, nC = 1 << A.cb, n = 1 << (A.U + A.cb);
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const int64_t f = pass_flat(base, e >> A.cb, b0, e & (nC - 1));
-        s[e] = (f >> A.lgL) < A.valid_rows ? g[f] : 0u;
-    }
+    const uint32_t cta = blockIdx.x;
+    const uint32_t mid = cta & ((1u << nmid) - 1);
+    const uint32_t hi = cta >> nmid;
+    const uint32_t base = (hi << (b0 + A.U)) | (mid << A.cb);
+    const int tile_bits = A.U + A.cb;
+    const uint32_t n = 1u << tile_bits;
+    const uint32_t cmask = (1u << A.cb) - 1;
+    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x)
+        s[padi(e)] = g[base | ((e >> A.cb) << b0) | (e & cmask)];
     __syncthreads();
-    pass_stages<DIR>(s, A, base, tw, pc.p, pc.two_p);
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const int64_t f = pass_flat(base, e >> A.cb, b0, e & (nC - 1));
-        if ((f >> A.lgL) < A.store_rows) g[f] = s[e];
-    }
-}
-
-// Last forward pass of operand B, pointwise product with the fully
-// transformed A (Montgomery, tc/_kernels.py:228-233) times 1/(s_y L) (the
-// constant part of scale_rows, tc/_kernels.py:236-242), then the first
-// inverse pass -- one kernel, one read of each grid, one write.
-__global__ void __launch_bounds__(512) k_ymid(PassArgs A) {
-    extern __shared__ __align__(16) uint32_t s[];
-    const int q = blockIdx.y;
-    uint32_t* g = A.grids + (int64_t)q * A.S;
-    const uint32_t* ga = A.other + (int64_t)q * A.S;
-    const uint2* tw = A.tw + (int64_t)q * A.tw_stride;
-    const uint2* twi = A.tw_inv + (int64_t)q * A.tw_stride;
-    const PrimeC pc = A.pcs[q];
-    const int64_t base = pass_base(A);
-    const int b0 = A.lgL + A.u0, nC = 1 << A.cb, n = 1 << (A.U + A.cb);
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const int64_t f = pass_flat(base, e >> A.cb, b0, e & (nC - 1));
-        s[e] = (f >> A.lgL) < A.valid_rows ? g[f] : 0u;
-    }
-    __syncthreads();
-    pass_stages<0>(s, A, base, tw, pc.p, pc.two_p);
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const int64_t f = pass_flat(base, e >> A.cb, b0, e & (nC - 1));
-        uint32_t m = mont_mul(s[e], ga[f], pc.p, pc.pinv_neg);
-        s[e] = shoup_mul(m, pc.scale, pc.scale_sh, pc.p);
-    }
-    __syncthreads();
-    pass_stages<1>(s, A, base, twi, pc.p, pc.two_p);
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const int64_t f = pass_flat(base, e >> A.cb, b0, e & (nC - 1));
-        g[f] = s[e];
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Inverse x-direction NTT (DIT, tc/_kernels.py:167-183) over rows < rows.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_xinv(uint32_t* grids, int64_t S, int lgL, int R, int64_t rows,
-                                              const uint2* twx_inv, const PrimeC* pcs) {
-    extern __shared__ __align__(16) uint32_t tile[];
-    const int q = blockIdx.y;
-    const PrimeC pc = pcs[q];
-    const int L = 1 << lgL;
-    const uint2* tw = twx_inv + (int64_t)q * (L >> 1);
-    const int64_t r0 = (int64_t)blockIdx.x * R;
-    const int nrows = (int)min((int64_t)R, rows - r0);
-    uint32_t* g = grids + (int64_t)q * S + r0 * L;
-    const int64_t nel = (int64_t)nrows * L;
-    for (int64_t e = threadIdx.x; e < nel; e += blockDim.x) tile[e] = g[e];
-    __syncthreads();
-    for (int t = 0; t < lgL; ++t) {
-        const int h = 1 << t;
-        for (int64_t e = threadIdx.x; e < (nel >> 1); e += blockDim.x) {
-            const int64_t r = e >> (lgL - 1);
-            const int pj = (int)(e & ((L >> 1) - 1));
-            const int jlo = ((pj >> t) << (t + 1)) | (pj & (h - 1));
-            const uint2 w = __ldg(&tw[(jlo & (h - 1)) << (lgL - 1 - t)]);
-            uint32_t* x = tile + r * L + jlo;
-            uint32_t u = x[0], v = x[h];
-            bfly_dit(u, v, w.x, w.y, pc.p, pc.two_p);
-            x[0] = u; x[h] = v;
+    const TwHigh tf{A.twf + (int64_t)q * A.tw_stride, A.lgL, A.lgS, A.u0, A.cb, mid << A.cb};
+    if (MODE == MODE_FWD || MODE == MODE_MID)
+        run_bits<false>(s, tile_bits, A.cb, tile_bits, tf, pc.p, pc.two_p);
+    if (MODE == MODE_MID) {
+        const uint32_t* ga = A.other + (int64_t)q * A.S;
+        for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
+            const uint32_t f = base | ((e >> A.cb) << b0) | (e & cmask);
+            const uint32_t x = reduce_2p(s[padi(e)], pc.two_p);
+            const uint32_t y = reduce_2p(ga[f], pc.two_p);
+            s[padi(e)] = shoup_mul(mont_mul(x, y, pc.p, pc.pinv_neg), pc.scale, pc.scale_sh, pc.p);
         }
         __syncthreads();
     }
-    for (int64_t e = threadIdx.x; e < nel; e += blockDim.x) g[e] = tile[e];
+    if (MODE == MODE_INV || MODE == MODE_MID) {
+        TwHigh ti = tf;
+        ti.twy = A.twi + (int64_t)q * A.tw_stride;
+        run_bits<true>(s, tile_bits, A.cb, tile_bits, ti, pc.p, pc.two_p);
+    }
+    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x)
+        g[base | ((e >> A.cb) << b0) | (e & cmask)] = s[padi(e)];
 }
 
 // ---------------------------------------------------------------------------
@@ -412,14 +455,13 @@ __device__ __forceinline__ bool crt_term(const uint32_t (&r)[P], const CrtConst&
     for (int k = P - 2; k >= 0; --k) {
         uint64_t carry = v[k];
 #pragma unroll
-        for (int l = 0; l < P - 1 - k; ++l) {       // limbs in use before this step
+        for (int l = 0; l < P - 1 - k; ++l) {
             uint64_t t = (uint64_t)x[l] * cc.p[k] + carry;
             x[l] = (uint32_t)t;
             carry = t >> 32;
         }
         x[P - 1 - k] = (uint32_t)carry;
     }
-    // x > half ?  (lexicographic from the top)
     int gt = 0;
 #pragma unroll
     for (int l = P - 1; l >= 0; --l)
@@ -429,9 +471,9 @@ __device__ __forceinline__ bool crt_term(const uint32_t (&r)[P], const CrtConst&
         uint64_t br = 0, br2 = 0;
 #pragma unroll
         for (int l = 0; l < P; ++l) {
-            uint64_t d1 = (uint64_t)cc.prod[l] - x[l] - br;      // magnitude = prod - x
+            uint64_t d1 = (uint64_t)cc.prod[l] - x[l] - br;
             mag[l] = (uint32_t)d1; br = (d1 >> 63) & 1;
-            uint64_t d2 = (uint64_t)x[l] - cc.prod[l] - br2;     // value = x - prod
+            uint64_t d2 = (uint64_t)x[l] - cc.prod[l] - br2;
             x[l] = (uint32_t)d2; br2 = (d2 >> 63) & 1;
         }
     } else {
@@ -453,181 +495,174 @@ __device__ __forceinline__ uint32_t tf_of(int64_t x) {
     for (int c = -1; c <= 1; ++c) e |= (uint32_t)(((x + c) >> 32) + 1) << (2 * (c + 1));
     return e;
 }
-__device__ __forceinline__ uint32_t tf_apply(uint32_t f, int c) { return (int)((f >> (2 * (c + 1))) & 3u) - 1; }
+__device__ __forceinline__ int tf_apply(uint32_t f, int c) { return (int)((f >> (2 * (c + 1))) & 3u) - 1; }
 __device__ __forceinline__ uint32_t tf_compose(uint32_t g, uint32_t f) {
     uint32_t e = 0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) e |= ((g >> (2 * ((f >> (2 * c)) & 3u))) & 3u) << (2 * c);
     return e;
 }
+__device__ __forceinline__ uint32_t tf_const(int c) {   // f(x) = c for every x
+    const uint32_t v = (uint32_t)(c + 1);
+    return v | (v << 2) | (v << 4);
+}
 constexpr uint32_t kTfIdentity = 0u | (1u << 2) | (2u << 4);
 
-// ---------------------------------------------------------------------------
-// Fused CRT + ConvertOut (recover_rows, tc/_kernels.py:377-423, in the
-// equivalent form of SURVEY.md section 8(a): c_i = sum_j c_ij 2^(Mj) over the
-// 2K-1 exact bivariate coefficients).  Per output row the 32-bit output words
-// are split over `tpr` threads, WPT consecutive words each, processed in
-// chunks of tpr*WPT words:
-//   1. CRT every term j touching the chunk into shared memory (P limbs);
-//   2. per word, S_w = sum of the 32-bit pieces of the overlapping shifted
-//      terms (unsigned pieces + one signed top piece), split lo/hi;
-//      x_w = lo_w + hi_{w-1}, so every carry is in {-1, 0, +1};
-//   3. a segmented scan of 3-state transfer functions gives each word's
-//      incoming carry; out_w = x_w + carry mod 2^32.
-// The result is the product mod 2^(64*out_cw) = its two's-complement words.
-// ---------------------------------------------------------------------------
-constexpr int kWPT = 4;
+// floor(x / M) for 0 <= x < 2^31 with a precomputed reciprocal (no IDIV).
+__device__ __forceinline__ int div_m(int x, int M, uint32_t minv) {
+    int q = (int)__umulhi((uint32_t)x, minv);
+    if ((q + 1) * M <= x) ++q;
+    return q;
+}
 
-struct CrtOutArgs {
-    const uint32_t* grids; int64_t S; int lgL;
-    int64_t rows; int M; int W32;       // 32-bit output words per row
-    int tpr; int nchunks; int max_terms;
-    uint32_t* out;                      // rows x W32
-    int* err;                           // err[2]: first bad i*L+j (clamped)
+// ---------------------------------------------------------------------------
+// k_final: the inverse's last pass + CRT + ConvertOut, per tile of 2^yl row
+// positions x L columns, all P primes resident in shared memory.
+//   1. per prime: y low levels (DIF, inverse twiddles), x levels (DIT);
+//   2. CRT every slot in place: P residues -> P two's-complement limbs;
+//   3. ConvertOut (recover_rows, tc/_kernels.py:377-423, in the equivalent
+//      form c_i = sum_j c_ij 2^(Mj) over the 2K-1 exact terms of SURVEY.md
+//      section 8(a)): thread per 32-bit output word; S_w = sum of the 32-bit
+//      pieces of the overlapping shifted terms (unsigned pieces plus one signed
+//      top piece), x_w = lo(S_w) + hi(S_{w-1}) so every carry is in {-1,0,+1};
+//      a block-wide scan of 3-state transfer functions (reset at each row
+//      start) gives each word its incoming carry; out_w = x_w + carry.
+// The row at position pos is product row bitrev(pos); rows >= rows_out are
+// the zero padding and are skipped.  DUMP writes the exact c_ij instead.
+// ---------------------------------------------------------------------------
+struct FinalArgs {
+    const uint32_t* g; int64_t S;
+    int lgL, lgS, yl;
+    const uint2* twx; const uint2* twy; int64_t twy_stride;   // inverse tables
+    const PrimeC* pcs;
+    int64_t rows_out; int M; uint32_t minv; int W32;
+    uint32_t* out;                 // rows_out x W32 (or rows_out x L x P for DUMP)
+    int* err;                      // err[2]: first bad flat index i*L + j
 };
 
-template <int P>
-__global__ void __launch_bounds__(256) k_crt_out(CrtOutArgs A, const __grid_constant__ CrtConst cc) {
+template <int P, bool DUMP>
+__global__ void __launch_bounds__(512) k_final(FinalArgs A, const __grid_constant__ CrtConst cc) {
     extern __shared__ __align__(16) uint32_t sm[];
-    const int rpc = blockDim.x / A.tpr;
-    const int grp = threadIdx.x / A.tpr, tl = threadIdx.x % A.tpr;
-    const int64_t row = (int64_t)blockIdx.x * rpc + grp;
-    const bool rv = row < A.rows;
+    __shared__ uint32_t wtot[32];
+    __shared__ int64_t whi[32];
+    __shared__ int s_carry;
+    __shared__ int64_t s_hi;
+    __shared__ int s_any;
+    const int R = 1 << A.yl;
     const int L = 1 << A.lgL;
-    const int M = A.M;
-    uint32_t* T = sm + (int64_t)grp * A.max_terms * P;
-    int64_t* hlast = reinterpret_cast<int64_t*>(sm + (int64_t)rpc * A.max_terms * P);  // blockDim
-    uint32_t* ftot = reinterpret_cast<uint32_t*>(hlast + blockDim.x);                  // blockDim
-    int* gcarry = reinterpret_cast<int*>(ftot + blockDim.x);                            // rpc
-    int64_t* ghi = reinterpret_cast<int64_t*>(gcarry + rpc + (rpc & 1));                // rpc
-
-    if (tl == 0) { gcarry[grp] = 0; ghi[grp] = 0; }
+    const int tile_bits = A.lgL + A.yl;
+    const uint32_t n = 1u << tile_bits;
+    const uint32_t stride = padded_words(n);
+    const uint32_t pos0 = blockIdx.x * (uint32_t)R;
+    if (threadIdx.x == 0) s_any = 0;
     __syncthreads();
-    const int chunk_words = A.tpr * kWPT;
-    for (int ch = 0; ch < A.nchunks; ++ch) {
-        const int w0 = ch * chunk_words;
-        const int w1 = min(w0 + chunk_words, A.W32);
-        const int64_t lo_num = 32ll * (w0 - P);
-        const int64_t j_lo = lo_num <= 0 ? 0 : (lo_num + M - 1) / M;
-        const int64_t j_hi = min((int64_t)(L - 2), (int64_t)((32ll * w1 - 1) / M));
-        const int nt = (int)max((int64_t)0, j_hi - j_lo + 1);
-        // 1. CRT of the chunk's terms
-        for (int t = tl; t < nt; t += A.tpr) {
-            const int64_t j = j_lo + t;
-            uint32_t r[P], x[P];
+    for (int r = threadIdx.x; r < R; r += blockDim.x)
+        if (bitrev(pos0 + r, A.lgS) < A.rows_out) s_any = 1;
+    __syncthreads();
+    if (!s_any) return;      // every row of this tile is zero padding
+
+    for (int q = 0; q < P; ++q) {
+        const PrimeC pc = A.pcs[q];
+        uint32_t* t = sm + q * stride;
+        const uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)blockIdx.x * n;
+        for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) t[padi(e)] = g[e];
+        __syncthreads();
+        const TwRows tw{A.twx + (int64_t)q * (L >> 1), A.twy + (int64_t)q * A.twy_stride, A.lgL, A.lgS};
+        run_bits<true>(t, tile_bits, A.lgL, tile_bits, tw, pc.p, pc.two_p);   // y low: DIF
+        run_bits<false>(t, tile_bits, 0, A.lgL, tw, pc.p, pc.two_p);          // x: DIT
+    }
+    // CRT in place
+    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
+        uint32_t r[P], x[P];
 #pragma unroll
-            for (int q = 0; q < P; ++q)
-                r[q] = rv ? canon(A.grids[(int64_t)q * A.S + row * L + j], cc.p[q]) : 0u;
-            const bool bad = crt_term<P>(r, cc, x);
-            if (bad && rv) atomicMin(&A.err[2], (int)min(row * L + j, (int64_t)0x7fffffff));
+        for (int q = 0; q < P; ++q) r[q] = canon(sm[q * stride + padi(e)], cc.p[q]);
+        const bool bad = crt_term<P>(r, cc, x);
+        const uint32_t row = bitrev(pos0 + (e >> A.lgL), A.lgS);
+        const uint32_t j = e & (L - 1);
+        if (row < A.rows_out) {
+            if (bad) atomicMin(&A.err[2], (int)min((int64_t)row * L + j, (int64_t)0x7fffffff));
+            if (DUMP) {
 #pragma unroll
-            for (int l = 0; l < P; ++l) T[t * P + l] = x[l];
+                for (int l = 0; l < P; ++l) A.out[((int64_t)row * L + j) * P + l] = x[l];
+            }
+        }
+#pragma unroll
+        for (int l = 0; l < P; ++l) sm[l * stride + padi(e)] = x[l];
+    }
+    if (DUMP) return;
+    __syncthreads();
+
+    // ConvertOut over the tile's rows, words flattened as gi = r * W32 + w.
+    const int M = A.M, W32 = A.W32;
+    const int64_t total = (int64_t)R * W32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (threadIdx.x == 0) { s_carry = 0; s_hi = 0; }
+    __syncthreads();
+    for (int64_t gb = 0; gb < total; gb += blockDim.x) {
+        const int64_t gi = gb + threadIdx.x;
+        const bool valid = gi < total;
+        const int r = valid ? (int)(gi / W32) : R;
+        const int w = valid ? (int)(gi - (int64_t)r * W32) : 0;
+        int64_t sum = 0;
+        if (valid) {
+            const int lo_n = 32 * (w - P);
+            const int jf = lo_n <= 0 ? 0 : div_m(lo_n + M - 1, M, A.minv);
+            const int jl = min(L - 2, div_m(32 * w + 31, M, A.minv));
+            const uint32_t rowbase = (uint32_t)r << A.lgL;
+            int bit = M * jf;
+            for (int j = jf; j <= jl; ++j, bit += M) {
+                const int k = w - (bit >> 5);
+                const int rr = bit & 31;
+                const uint32_t e = padi(rowbase + j);
+                const uint32_t top = sm[(P - 1) * stride + e];
+                const uint32_t sgn = (top >> 31) ? 0xffffffffu : 0u;
+                const uint32_t cur = k < P ? sm[k * stride + e] : sgn;
+                const uint32_t prv = k > 0 ? sm[(k - 1) * stride + e] : 0u;
+                const uint32_t piece = rr ? ((cur << rr) | (prv >> (32 - rr))) : cur;
+                sum += k < P ? (int64_t)piece : (int64_t)(int32_t)piece;
+            }
+        }
+        // x_w = lo(S_w) + hi(S_{w-1}) within a row
+        const int64_t hi = sum >> 32;
+        int64_t hprev = __shfl_up_sync(0xffffffffu, hi, 1);
+        if (lane == 31) whi[warp] = hi;
+        __syncthreads();
+        if (lane == 0) hprev = warp > 0 ? whi[warp - 1] : s_hi;
+        const int64_t x = (sum & 0xffffffffll) + (w == 0 ? 0 : hprev);
+        const uint32_t f = !valid ? kTfIdentity : (w == 0 ? tf_const(tf_apply(tf_of(x), 0)) : tf_of(x));
+        // block-wide inclusive scan of f (later o earlier)
+        uint32_t incl = f;
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl = tf_compose(incl, o);
+        }
+        if (lane == 31) wtot[warp] = incl;
+        __syncthreads();
+        uint32_t pre = kTfIdentity;
+        for (int k = 0; k < warp; ++k) pre = tf_compose(wtot[k], pre);
+        uint32_t excl = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) excl = kTfIdentity;
+        excl = tf_compose(excl, pre);
+        const int c_in = w == 0 ? 0 : tf_apply(excl, s_carry);   // no carry into a row's word 0
+        if (valid) {
+            const uint32_t prow = bitrev(pos0 + r, A.lgS);
+            if (prow < A.rows_out) A.out[(int64_t)prow * W32 + w] = (uint32_t)(x + c_in);
         }
         __syncthreads();
-        // 2. word sums
-        int64_t xs[kWPT];
-        int64_t hi_prev_local = 0;
-#pragma unroll
-        for (int u = 0; u < kWPT; ++u) {
-            const int w = w0 + tl * kWPT + u;
-            int64_t sum = 0;
-            if (w < w1) {
-                const int64_t lo_n = 32ll * (w - P);
-                int64_t jf = lo_n <= 0 ? 0 : (lo_n + M - 1) / M;
-                int64_t jl = min((int64_t)(L - 2), (int64_t)((32ll * w + 31) / M));
-                for (int64_t j = jf; j <= jl; ++j) {
-                    const int64_t bit = (int64_t)M * j;
-                    const int k = (int)(w - (bit >> 5));     // piece index 0..P
-                    const int rr = (int)(bit & 31);
-                    const uint32_t* c = T + (j - j_lo) * P;
-                    const uint32_t sgn = (c[P - 1] >> 31) ? 0xffffffffu : 0u;
-                    const uint32_t cur = k < P ? c[k] : sgn;
-                    const uint32_t prv = k > 0 ? c[k - 1] : 0u;
-                    const uint32_t piece = rr ? ((cur << rr) | (prv >> (32 - rr))) : cur;
-                    sum += k < P ? (int64_t)piece : (int64_t)(int32_t)piece;
-                }
-            }
-            xs[u] = sum;
-        }
-        // lo/hi split: x_w = lo_w + hi_{w-1}
-        int64_t his[kWPT];
-#pragma unroll
-        for (int u = 0; u < kWPT; ++u) { his[u] = xs[u] >> 32; xs[u] &= 0xffffffffll; }
-        hlast[threadIdx.x] = his[kWPT - 1];
-        __syncthreads();
-        hi_prev_local = tl > 0 ? hlast[threadIdx.x - 1] : ghi[grp];
-#pragma unroll
-        for (int u = kWPT - 1; u >= 1; --u) xs[u] += his[u - 1];
-        xs[0] += hi_prev_local;
-        // 3. transfer functions and the segmented scan over the group
-        uint32_t F = kTfIdentity;
-#pragma unroll
-        for (int u = 0; u < kWPT; ++u) {
-            const int w = w0 + tl * kWPT + u;
-            if (w < w1) F = tf_compose(tf_of(xs[u]), F);
-        }
-        uint32_t incl = F;
-        if (A.tpr <= 32) {
-            for (int off = 1; off < A.tpr; off <<= 1) {
-                uint32_t n = __shfl_up_sync(0xffffffffu, incl, off, A.tpr);
-                if (tl >= off) incl = tf_compose(incl, n);
-            }
-            ftot[threadIdx.x] = incl;
-            __syncthreads();
-        } else {
-            const int lane = threadIdx.x & 31;
-            for (int off = 1; off < 32; off <<= 1) {
-                uint32_t n = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= off) incl = tf_compose(incl, n);
-            }
-            ftot[threadIdx.x] = incl;
-            __syncthreads();
-            // prefix over warps of this group (one group per CTA here)
-            const int wg = tl >> 5;
-            uint32_t pre = kTfIdentity;
-            for (int w = 0; w < wg; ++w) pre = tf_compose(ftot[grp * A.tpr + w * 32 + 31], pre);
-            incl = tf_compose(incl, pre);
-            __syncthreads();
-            ftot[threadIdx.x] = incl;
-            __syncthreads();
-        }
-        const uint32_t excl = tl > 0 ? ftot[threadIdx.x - 1] : kTfIdentity;
-        const int cin_chunk = gcarry[grp];
-        int c = (int)tf_apply(excl, cin_chunk);
-#pragma unroll
-        for (int u = 0; u < kWPT; ++u) {
-            const int w = w0 + tl * kWPT + u;
-            if (w < w1) {
-                const int64_t v = xs[u] + c;
-                if (rv) A.out[row * A.W32 + w] = (uint32_t)v;
-                c = (int)(v >> 32);
-            }
-        }
-        __syncthreads();
-        if (tl == A.tpr - 1) {
-            gcarry[grp] = c;
-            ghi[grp] = his[kWPT - 1];
+        if (threadIdx.x == blockDim.x - 1) {
+            uint32_t all = kTfIdentity;
+            for (int k = 0; k < nw; ++k) all = tf_compose(wtot[k], all);
+            s_carry = tf_apply(all, s_carry);
+            s_hi = hi;
         }
         __syncthreads();
     }
 }
 
-// Debug / parity seam: exact c_ij (P limbs) for i < rows, j < L.
-template <int P>
-__global__ void k_crt_dump(const uint32_t* grids, int64_t S, int lgL, int64_t rows, uint32_t* out,
-                           int* err, const __grid_constant__ CrtConst cc) {
-    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t L = 1ll << lgL;
-    if (idx >= rows * L) return;
-    uint32_t r[P], x[P];
-#pragma unroll
-    for (int q = 0; q < P; ++q) r[q] = canon(grids[(int64_t)q * S + idx], cc.p[q]);
-    if (crt_term<P>(r, cc, x)) atomicMin(&err[2], (int)min(idx, (int64_t)0x7fffffff));
-#pragma unroll
-    for (int l = 0; l < P; ++l) out[idx * P + l] = x[l];
-}
-
-// Probes: the kernels' own modular products and a standalone length-n NTT.
+// ---------------------------------------------------------------------------
+// Probes: the kernels' own modular products, a standalone transform, and the
+// INT-pipe peak.
+// ---------------------------------------------------------------------------
 __global__ void k_modmul_probe(uint32_t p, uint32_t pinv_neg, const uint32_t* a, const uint32_t* b,
                                uint32_t* out, int64_t n, int mode) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -641,6 +676,19 @@ __global__ void k_modmul_probe(uint32_t p, uint32_t pinv_neg, const uint32_t* a,
         r = mont_mul(x, w, p, pinv_neg);
     }
     out[i] = canon(r, p);
+}
+
+// One length-2^lg transform on one tile (tc_ntt_probe): forward = DIF
+// natural -> bit-reversed, inverse = DIT bit-reversed -> natural (unscaled).
+__global__ void k_ntt_probe(uint32_t* data, int lg, const uint2* twf, const uint2* twi, PrimeC pc, int dir) {
+    extern __shared__ __align__(16) uint32_t s[];
+    const uint32_t n = 1u << lg;
+    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) s[padi(e)] = data[e];
+    __syncthreads();
+    const TwRows tw{dir ? twi : twf, nullptr, lg, 0};
+    if (dir == 0) run_bits<true>(s, lg, 0, lg, tw, pc.p, pc.two_p);
+    else run_bits<false>(s, lg, 0, lg, tw, pc.p, pc.two_p);
+    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) data[e] = canon(s[padi(e)], pc.p);
 }
 
 // INT-pipe peak: 8 independent register chains per thread of the exact

@@ -232,8 +232,33 @@ def _primes_for_bound(bound2: int, need_len: int):
     return None
 
 
-def _y_passes(lgS: int) -> int:
-    return 0 if lgS == 0 else _ceil_div(lgS, 9)
+def pass_layout(lgL: int, lgS: int, P: int):
+    """(yl, [(u0, U), ...]) exactly as make_geometry in csrc/tc_api.cu lays out
+    the passes: k_low/k_final tiles of 2^(lgL+yl) slots (P of them <= 96 KiB in
+    k_final when possible), k_high passes over the remaining y levels in
+    balanced chunks of <= 14 - cb levels."""
+    tb = 0
+    while 4 * P * (2 << tb) <= 96 * 1024:
+        tb += 1
+    tb = min(tb, 13)
+    yl = max(0, min(tb - lgL, lgS))
+    high = []
+    nlev = lgS - yl
+    if nlev > 0:
+        cb = min(4, lgL + yl)
+        uh = 14 - cb
+        npass = _ceil_div(nlev, uh)
+        base, extra = nlev // npass, nlev % npass
+        u = yl
+        for i in range(npass):
+            U = base + (1 if i < extra else 0)
+            high.append((u, U))
+            u += U
+    return yl, high
+
+
+def _y_passes(lgS: int, lgL: int = 0, P: int = 1) -> int:
+    return len(pass_layout(lgL, lgS, P)[1])
 
 
 def plan_cost(d: int, dmin: int, K: int, M: int, P: int, out_words: int) -> float:
@@ -246,8 +271,8 @@ def plan_cost(d: int, dmin: int, K: int, M: int, P: int, out_words: int) -> floa
     S = s_y * 2 * K
     lgS = S.bit_length() - 1
     bfly = 3 * (S // 2) * lgS * P
-    npy = _y_passes(s_y.bit_length() - 1)
-    sweeps = 2 * (2 * npy) + 3 + 2 * max(npy - 1, 0) + 2
+    npy = _y_passes(s_y.bit_length() - 1, (2 * K).bit_length() - 1, P)
+    sweeps = 1 + 2 * npy + 1 + 2 * max(npy - 1, 0) + 1 + 2 * max(npy - 1, 0) + 1
     mem = 4 * S * P * sweeps
     rows = 2 * d - 1
     crt = rows * 2 * K * (P * P * 8 + 40) * 3
