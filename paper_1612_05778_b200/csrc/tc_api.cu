@@ -151,7 +151,7 @@ int ensure_twiddles(Ctx* c, const tc_plan_t* pl) {
     std::vector<uint32_t> key(pl->p, pl->p + pl->P);
     if (key == c->tw_primes && c->tw_L == L && c->tw_sy == sy) return TC_OK;
     int rc;
-    const int64_t hx = L / 2, hy = sy > 1 ? sy / 2 : 1;
+    const int64_t hx = L, hy = sy;      // level-major tables: n entries per length n
     if ((rc = c->twx_f.ensure(sizeof(uint2) * hx * pl->P))) return rc;
     if ((rc = c->twx_i.ensure(sizeof(uint2) * hx * pl->P))) return rc;
     if ((rc = c->twy_f.ensure(sizeof(uint2) * hy * pl->P))) return rc;
@@ -160,19 +160,17 @@ int ensure_twiddles(Ctx* c, const tc_plan_t* pl) {
         const uint32_t p = pl->p[q], g = pl->g[q];
         for (int dim = 0; dim < 2; ++dim) {
             const int64_t n = dim == 0 ? L : sy;
-            const int64_t half = n / 2;
-            if (half < 1) continue;
+            if (n < 2) continue;
             PowTable pw;
             const uint64_t w = powmod(g, (p - 1) / n, p), wi = inv_mod((uint32_t)w, p);
             uint64_t cf = w, ci = wi;
-            const int nb = ilog2(half) + 1;
             for (int b = 0; b < 32; ++b) {
                 pw.f[b] = (uint32_t)cf; pw.i[b] = (uint32_t)ci;
                 cf = cf * cf % p; ci = ci * ci % p;
             }
             uint2* f = (dim == 0 ? c->twx_f.as<uint2>() : c->twy_f.as<uint2>()) + q * (dim == 0 ? hx : hy);
             uint2* iv = (dim == 0 ? c->twx_i.as<uint2>() : c->twy_i.as<uint2>()) + q * (dim == 0 ? hx : hy);
-            k_twiddles<<<(unsigned)((half + 255) / 256), 256, 0, c->st>>>(f, iv, half, p, pw, nb);
+            k_twiddles<<<(unsigned)((n + 255) / 256), 256, 0, c->st>>>(f, iv, n, p, pw, ilog2(n));
             c->launches++;
             CKL();
         }
@@ -289,7 +287,7 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     a.lgL = G.lgL; a.lgS = G.lgS; a.yl = G.yl;
     a.g = grids; a.S = G.S;
     a.twx = c->twx_f.as<uint2>(); a.twy = c->twy_f.as<uint2>();
-    a.twy_stride = G.s_y > 1 ? G.s_y / 2 : 1;
+    a.twy_stride = G.s_y;
     a.pcs = c->pcs.as<PrimeC>(); a.P = G.P;
     const int R = 1 << G.yl;
     const uint32_t n = 1u << (G.lgL + G.yl);
@@ -308,7 +306,7 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
     A.lgL = G.lgL; A.lgS = G.lgS; A.u0 = u0; A.U = U;
     A.cb = G.lgL + u0 < 4 ? G.lgL + u0 : 4;
     A.twf = c->twy_f.as<uint2>(); A.twi = c->twy_i.as<uint2>();
-    A.tw_stride = G.s_y > 1 ? G.s_y / 2 : 1;
+    A.tw_stride = G.s_y;
     A.pcs = c->pcs.as<PrimeC>();
     const uint32_t n = 1u << (U + A.cb);
     const size_t smem = (size_t)padded_words(n) * 4;
@@ -346,7 +344,7 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
     FinalArgs A{};
     A.g = grids; A.S = G.S; A.lgL = G.lgL; A.lgS = G.lgS; A.yl = G.yl;
     A.twx = c->twx_i.as<uint2>(); A.twy = c->twy_i.as<uint2>();
-    A.twy_stride = G.s_y > 1 ? G.s_y / 2 : 1;
+    A.twy_stride = G.s_y;
     A.pcs = c->pcs.as<PrimeC>();
     A.rows_out = rows; A.M = M; A.minv = (uint32_t)(0xffffffffu / (uint32_t)M); A.W32 = W32;
     A.out = out; A.err = c->flags.as<int>();

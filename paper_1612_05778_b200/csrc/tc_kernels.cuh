@@ -61,28 +61,35 @@ __global__ void k_width(const uint64_t* __restrict__ words, int64_t d, int cw, i
     }
 }
 
-// Twiddle tables: entry m < n/2 is {w^m, floor(w^m 2^32 / p)} for the order-n
-// root w (forward) and w^-1 (inverse) -- the roles of tc/modfield.py:78-99.
+// Twiddle tables, level-major: entry 2^l + m (l < lg n, m < 2^l) is
+// {w_l^m, floor(w_l^m 2^32 / p)} with w_l the root of order 2^(l+1), i.e.
+// the twiddle of radix-2 level l (half-size 2^l) for index m; the inverse
+// table holds w_l^-m.  Same values as tc/modfield.py:78-99's per-length
+// tables, laid out so a stage's twiddles are contiguous.
 struct PowTable { uint32_t f[32]; uint32_t i[32]; };
 
-__global__ void k_twiddles(uint2* fwd, uint2* inv, int64_t half, uint32_t p, PowTable pw, int nb) {
-    int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (m >= half) return;
+__global__ void k_twiddles(uint2* fwd, uint2* inv, int64_t n, uint32_t p, PowTable pw, int lg) {
+    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= n) return;
+    if (idx == 0) { fwd[0] = make_uint2(1u, 0u); inv[0] = make_uint2(1u, 0u); return; }
+    const int l = 63 - __clzll(idx);
+    const uint64_t e = (uint64_t)(idx - (1ll << l)) << (lg - 1 - l);   // exponent of w_n
     uint64_t wf = 1, wi = 1;
-    for (int b = 0; b < nb; ++b)
-        if ((m >> b) & 1) { wf = wf * pw.f[b] % p; wi = wi * pw.i[b] % p; }
-    fwd[m] = make_uint2((uint32_t)wf, (uint32_t)((wf << 32) / p));
-    inv[m] = make_uint2((uint32_t)wi, (uint32_t)((wi << 32) / p));
+    for (int b = 0; b < lg; ++b)
+        if ((e >> b) & 1) { wf = wf * pw.f[b] % p; wi = wi * pw.i[b] % p; }
+    fwd[idx] = make_uint2((uint32_t)wf, (uint32_t)((wf << 32) / p));
+    inv[idx] = make_uint2((uint32_t)wi, (uint32_t)((wi << 32) / p));
 }
 
 __device__ __forceinline__ uint32_t bitrev(uint32_t x, int bits) {
     return bits ? __brev(x) >> (32 - bits) : 0u;
 }
 
-// Padded shared-memory index: one spare word per 32 keeps the stride-16
-// accesses of radix-16 rounds on low bits conflict-free.
-__device__ __forceinline__ uint32_t padi(uint32_t e) { return e + (e >> 5); }
-__host__ __device__ constexpr uint32_t padded_words(uint32_t n) { return n + (n >> 5) + 1; }
+// Padded shared-memory index: one spare word per 16 keeps the stride-16
+// accesses of radix-16 rounds on low bits conflict-free, and is linear inside
+// any round that does not straddle bit 4 (run_bits never lets one).
+__device__ __forceinline__ uint32_t padi(uint32_t e) { return e + (e >> 4); }
+__host__ __device__ constexpr uint32_t padded_words(uint32_t n) { return n + (n >> 4) + 1; }
 
 // ---------------------------------------------------------------------------
 // Balanced digits (tc/_kernels.py:78-119) for up to R rows of one CTA.
@@ -220,17 +227,22 @@ __device__ __forceinline__ void round_exec(uint32_t* s, int tile_bits, int bit_l
     constexpr int R = 1 << NB;
     const uint32_t ngroups = 1u << (tile_bits - NB);
     const uint32_t lowmask = (1u << bit_lo) - 1;
+    const uint32_t astep = bit_lo >= 4 ? (1u << bit_lo) + (1u << (bit_lo - 4)) : (1u << bit_lo);
+    const uint2* tp = tw.table(bit_lo);
+    const int tsh = tw.shift(bit_lo);
     for (uint32_t g = threadIdx.x; g < ngroups; g += blockDim.x) {
-        const uint32_t e0 = ((g & ~lowmask) << NB) | (g & lowmask);
+        const uint32_t lo = g & lowmask;
+        const uint32_t a0 = padi(((g & ~lowmask) << NB) | lo);
         uint32_t x[R];
 #pragma unroll
-        for (int k = 0; k < R; ++k) x[k] = s[padi(e0 + ((uint32_t)k << bit_lo))];
+        for (int k = 0; k < R; ++k) x[k] = s[a0 + k * astep];
 #pragma unroll
         for (int it = 0; it < NB; ++it) {
             const int lv = DIF ? NB - 1 - it : it;
+            const uint32_t tb = tw.base(lo, bit_lo + lv);
 #pragma unroll
             for (int m = 0; m < (1 << lv); ++m) {
-                const uint2 w = tw(e0 + ((uint32_t)m << bit_lo), bit_lo + lv);
+                const uint2 w = __ldg(&tp[tb + ((uint32_t)m << tsh)]);
 #pragma unroll
                 for (int jj = 0; jj < R / (2 << lv); ++jj) {
                     const int k = m + jj * (2 << lv);
@@ -240,7 +252,7 @@ __device__ __forceinline__ void round_exec(uint32_t* s, int tile_bits, int bit_l
             }
         }
 #pragma unroll
-        for (int k = 0; k < R; ++k) s[padi(e0 + ((uint32_t)k << bit_lo))] = x[k];
+        for (int k = 0; k < R; ++k) s[a0 + k * astep] = x[k];
     }
     __syncthreads();
 }
@@ -257,10 +269,11 @@ __device__ __forceinline__ void round_dispatch(int nb, uint32_t* s, int tile_bit
     }
 }
 
-// Stages on tile bits [lo, hi): DIT ascending in rounds of <= 4 bits, DIF descending.
+// Stages on tile bits [lo, hi): DIT ascending in rounds of <= 4 bits, DIF
+// descending; rounds never straddle bit 4 (linear padded addressing).
 template <bool DIF, class TW>
-__device__ __forceinline__ void run_bits(uint32_t* s, int tile_bits, int lo, int hi, const TW& tw,
-                                         uint32_t p, uint32_t two_p) {
+__device__ __forceinline__ void run_segment(uint32_t* s, int tile_bits, int lo, int hi, const TW& tw,
+                                            uint32_t p, uint32_t two_p) {
     const int nbits = hi - lo;
     if (nbits <= 0) return;
     const int nr = (nbits + 3) / 4;
@@ -282,25 +295,45 @@ __device__ __forceinline__ void run_bits(uint32_t* s, int tile_bits, int lo, int
     }
 }
 
-// Twiddles of a whole-row tile (k_low / k_final): tile index e = local_row*L + col.
+template <bool DIF, class TW>
+__device__ __forceinline__ void run_bits(uint32_t* s, int tile_bits, int lo, int hi, const TW& tw,
+                                         uint32_t p, uint32_t two_p) {
+    const int mid = lo < 4 && hi > 4 ? 4 : lo;
+    if (mid == lo) { run_segment<DIF>(s, tile_bits, lo, hi, tw, p, two_p); return; }
+    if (!DIF) {
+        run_segment<false>(s, tile_bits, lo, mid, tw, p, two_p);
+        run_segment<false>(s, tile_bits, mid, hi, tw, p, two_p);
+    } else {
+        run_segment<true>(s, tile_bits, mid, hi, tw, p, two_p);
+        run_segment<true>(s, tile_bits, lo, mid, tw, p, two_p);
+    }
+}
+
+// Twiddle addressing of a round.  table(bit_lo): the level-major table of the
+// round's dimension; base(lo, bit): index of the m = 0 twiddle of level `bit`
+// for a group whose bits below bit_lo are `lo`; shift(bit_lo): twiddle m sits
+// at base + (m << shift).
+// Whole-row tiles (k_low / k_final): tile index e = local_row * L + col; a
+// round lies entirely in the x bits [0, lgL) or the y bits.
 struct TwRows {
-    const uint2* twx; const uint2* twy; int lgL, lgS;
-    __device__ __forceinline__ uint2 operator()(uint32_t e, int bit) const {
-        if (bit < lgL) return __ldg(&twx[(e & ((1u << bit) - 1)) << (lgL - 1 - bit)]);
-        const int u = bit - lgL;
-        return __ldg(&twy[((e >> lgL) & ((1u << u) - 1)) << (lgS - 1 - u)]);
+    const uint2* twx; const uint2* twy; int lgL;
+    __device__ __forceinline__ const uint2* table(int bit_lo) const { return bit_lo < lgL ? twx : twy; }
+    __device__ __forceinline__ int shift(int bit_lo) const { return bit_lo < lgL ? bit_lo : bit_lo - lgL; }
+    __device__ __forceinline__ uint32_t base(uint32_t lo, int bit) const {
+        return bit < lgL ? (1u << bit) + lo : (1u << (bit - lgL)) + (lo >> lgL);
     }
 };
 
-// Twiddles of a high-pass tile: e = (a << cb) | c, tile bit b >= cb is y level
-// u0 + (b - cb); the row bits below u0 come from the CTA's mid bits and c.
+// High-pass tiles: e = (a << cb) | c; tile bit b >= cb is y level u0 + b - cb,
+// whose row is rb | (a mod 2^(b-cb)) << u0 with rb the row bits below u0
+// (from the CTA's mid bits and c).
 struct TwHigh {
-    const uint2* twy; int lgL, lgS, u0, cb; uint32_t midc;
-    __device__ __forceinline__ uint2 operator()(uint32_t e, int bit) const {
-        const int l = bit - cb, u = u0 + l;
-        const uint32_t rb = (midc | (e & ((1u << cb) - 1))) >> lgL;
-        const uint32_t row = rb | (((e >> cb) & ((1u << l) - 1)) << u0);
-        return __ldg(&twy[row << (lgS - 1 - u)]);
+    const uint2* twy; int lgL, u0, cb; uint32_t midc;
+    __device__ __forceinline__ const uint2* table(int) const { return twy; }
+    __device__ __forceinline__ int shift(int bit_lo) const { return bit_lo - cb + u0; }
+    __device__ __forceinline__ uint32_t base(uint32_t lo, int bit) const {
+        const uint32_t rb = (midc | (lo & ((1u << cb) - 1))) >> lgL;
+        return (1u << (u0 + bit - cb)) + rb + ((lo >> cb) << u0);
     }
 };
 
@@ -317,7 +350,7 @@ struct LowArgs {
     const PrimeC* pcs; int P;
 };
 
-__global__ void __launch_bounds__(512) k_low(LowArgs A) {
+__global__ void __launch_bounds__(512, 2) k_low(LowArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int R = 1 << A.yl;
     const int L = 1 << A.lgL;
@@ -352,7 +385,7 @@ __global__ void __launch_bounds__(512) k_low(LowArgs A) {
             tile[padi(e)] = (j < A.src.K && coeff[r] >= 0) ? digit_residue(dig[(int64_t)r * A.src.K + j], pc) : 0u;
         }
         __syncthreads();
-        const TwRows tw{A.twx + (int64_t)q * (L >> 1), A.twy + (int64_t)q * A.twy_stride, A.lgL, A.lgS};
+        const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
         run_bits<true>(tile, tile_bits, 0, A.lgL, tw, pc.p, pc.two_p);          // x: DIF
         run_bits<false>(tile, tile_bits, A.lgL, tile_bits, tw, pc.p, pc.two_p); // y low: DIT
         uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)blockIdx.x * n;
@@ -379,7 +412,7 @@ struct HighArgs {
 };
 
 template <int MODE>
-__global__ void __launch_bounds__(512) k_high(HighArgs A) {
+__global__ void __launch_bounds__(512, 2) k_high(HighArgs A) {
     extern __shared__ __align__(16) uint32_t s[];
     const int q = blockIdx.y;
     uint32_t* g = A.g + (int64_t)q * A.S;
@@ -396,7 +429,7 @@ __global__ void __launch_bounds__(512) k_high(HighArgs A) {
     for (uint32_t e = threadIdx.x; e < n; e += blockDim.x)
         s[padi(e)] = g[base | ((e >> A.cb) << b0) | (e & cmask)];
     __syncthreads();
-    const TwHigh tf{A.twf + (int64_t)q * A.tw_stride, A.lgL, A.lgS, A.u0, A.cb, mid << A.cb};
+    const TwHigh tf{A.twf + (int64_t)q * A.tw_stride, A.lgL, A.u0, A.cb, mid << A.cb};
     if (MODE == MODE_FWD || MODE == MODE_MID)
         run_bits<false>(s, tile_bits, A.cb, tile_bits, tf, pc.p, pc.two_p);
     if (MODE == MODE_MID) {
@@ -487,27 +520,6 @@ __device__ __forceinline__ bool crt_term(const uint32_t (&r)[P], const CrtConst&
     return over > 0;
 }
 
-// 3-state carry transfer functions f: {-1,0,1} -> {-1,0,1}, packed as three
-// 2-bit fields (f(c)+1 at bit 2(c+1)).  compose(g, f) = g o f.
-__device__ __forceinline__ uint32_t tf_of(int64_t x) {
-    uint32_t e = 0;
-#pragma unroll
-    for (int c = -1; c <= 1; ++c) e |= (uint32_t)(((x + c) >> 32) + 1) << (2 * (c + 1));
-    return e;
-}
-__device__ __forceinline__ int tf_apply(uint32_t f, int c) { return (int)((f >> (2 * (c + 1))) & 3u) - 1; }
-__device__ __forceinline__ uint32_t tf_compose(uint32_t g, uint32_t f) {
-    uint32_t e = 0;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) e |= ((g >> (2 * ((f >> (2 * c)) & 3u))) & 3u) << (2 * c);
-    return e;
-}
-__device__ __forceinline__ uint32_t tf_const(int c) {   // f(x) = c for every x
-    const uint32_t v = (uint32_t)(c + 1);
-    return v | (v << 2) | (v << 4);
-}
-constexpr uint32_t kTfIdentity = 0u | (1u << 2) | (2u << 4);
-
 // floor(x / M) for 0 <= x < 2^31 with a precomputed reciprocal (no IDIV).
 __device__ __forceinline__ int div_m(int x, int M, uint32_t minv) {
     int q = (int)__umulhi((uint32_t)x, minv);
@@ -524,9 +536,8 @@ __device__ __forceinline__ int div_m(int x, int M, uint32_t minv) {
 //      form c_i = sum_j c_ij 2^(Mj) over the 2K-1 exact terms of SURVEY.md
 //      section 8(a)): thread per 32-bit output word; S_w = sum of the 32-bit
 //      pieces of the overlapping shifted terms (unsigned pieces plus one signed
-//      top piece), x_w = lo(S_w) + hi(S_{w-1}) so every carry is in {-1,0,+1};
-//      a block-wide scan of 3-state transfer functions (reset at each row
-//      start) gives each word its incoming carry; out_w = x_w + carry.
+//      top piece); the lo/hi halves of the S_w are added by two binary
+//      generate/propagate carry chains (ballot + add per warp).
 // The row at position pos is product row bitrev(pos); rows >= rows_out are
 // the zero padding and are skipped.  DUMP writes the exact c_ij instead.
 // ---------------------------------------------------------------------------
@@ -541,11 +552,11 @@ struct FinalArgs {
 };
 
 template <int P, bool DUMP>
-__global__ void __launch_bounds__(512) k_final(FinalArgs A, const __grid_constant__ CrtConst cc) {
+__global__ void __launch_bounds__(512, 2) k_final(FinalArgs A, const __grid_constant__ CrtConst cc) {
     extern __shared__ __align__(16) uint32_t sm[];
-    __shared__ uint32_t wtot[32];
+    __shared__ uint32_t wtf1[32], wtf2[32], wcin1[32], wcin2[32];
     __shared__ int64_t whi[32];
-    __shared__ int s_carry;
+    __shared__ uint32_t s_c1, s_c2;
     __shared__ int64_t s_hi;
     __shared__ int s_any;
     const int R = 1 << A.yl;
@@ -567,7 +578,7 @@ __global__ void __launch_bounds__(512) k_final(FinalArgs A, const __grid_constan
         const uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)blockIdx.x * n;
         for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) t[padi(e)] = g[e];
         __syncthreads();
-        const TwRows tw{A.twx + (int64_t)q * (L >> 1), A.twy + (int64_t)q * A.twy_stride, A.lgL, A.lgS};
+        const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
         run_bits<true>(t, tile_bits, A.lgL, tile_bits, tw, pc.p, pc.two_p);   // y low: DIF
         run_bits<false>(t, tile_bits, 0, A.lgL, tw, pc.p, pc.two_p);          // x: DIT
     }
@@ -593,16 +604,24 @@ __global__ void __launch_bounds__(512) k_final(FinalArgs A, const __grid_constan
     __syncthreads();
 
     // ConvertOut over the tile's rows, words flattened as gi = r * W32 + w.
+    // value(row) = sum_w lo_w 2^(32w) + sum_w hi_{w-1} 2^(32w), hi small signed
+    //            = A + B+ - B-  (B+ / B- the positive / negative hi parts):
+    // chain 1 adds B+ (carries), chain 2 subtracts B- (borrows); each is a
+    // binary generate/propagate chain resolved per warp by one 64-bit add of
+    // ballot masks and across warps by a serial scan of per-warp transfer bits.
+    // The last word of a row never generates or propagates, so chains never
+    // cross rows; carries out of a row's top word are the mod 2^(32 W32) wrap.
     const int M = A.M, W32 = A.W32;
     const int64_t total = (int64_t)R * W32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    if (threadIdx.x == 0) { s_carry = 0; s_hi = 0; }
+    if (threadIdx.x == 0) { s_c1 = 0; s_c2 = 0; s_hi = 0; }
     __syncthreads();
     for (int64_t gb = 0; gb < total; gb += blockDim.x) {
         const int64_t gi = gb + threadIdx.x;
         const bool valid = gi < total;
         const int r = valid ? (int)(gi / W32) : R;
         const int w = valid ? (int)(gi - (int64_t)r * W32) : 0;
+        const bool last = w == W32 - 1;
         int64_t sum = 0;
         if (valid) {
             const int lo_n = 32 * (w - P);
@@ -622,40 +641,46 @@ __global__ void __launch_bounds__(512) k_final(FinalArgs A, const __grid_constan
                 sum += k < P ? (int64_t)piece : (int64_t)(int32_t)piece;
             }
         }
-        // x_w = lo(S_w) + hi(S_{w-1}) within a row
         const int64_t hi = sum >> 32;
         int64_t hprev = __shfl_up_sync(0xffffffffu, hi, 1);
         if (lane == 31) whi[warp] = hi;
         __syncthreads();
         if (lane == 0) hprev = warp > 0 ? whi[warp - 1] : s_hi;
-        const int64_t x = (sum & 0xffffffffll) + (w == 0 ? 0 : hprev);
-        const uint32_t f = !valid ? kTfIdentity : (w == 0 ? tf_const(tf_apply(tf_of(x), 0)) : tf_of(x));
-        // block-wide inclusive scan of f (later o earlier)
-        uint32_t incl = f;
-        for (int off = 1; off < 32; off <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= off) incl = tf_compose(incl, o);
-        }
-        if (lane == 31) wtot[warp] = incl;
+        const int64_t bb = w == 0 ? 0 : hprev;
+        const uint32_t bp = bb > 0 ? (uint32_t)bb : 0u, bm = bb < 0 ? (uint32_t)(-bb) : 0u;
+        // chain 1: lo + B+
+        const uint64_t t1 = (uint64_t)(uint32_t)sum + bp;
+        uint32_t w1 = (uint32_t)t1;
+        const unsigned G1 = __ballot_sync(0xffffffffu, valid && !last && (t1 >> 32));
+        const unsigned P1 = __ballot_sync(0xffffffffu, valid && !last && w1 == 0xffffffffu);
+        const uint64_t A1 = (uint64_t)(G1 | P1), B1 = (uint64_t)G1;
+        if (lane == 0) wtf1[warp] = (uint32_t)((A1 + B1) >> 32) | ((uint32_t)((A1 + B1 + 1) >> 32) << 1);
         __syncthreads();
-        uint32_t pre = kTfIdentity;
-        for (int k = 0; k < warp; ++k) pre = tf_compose(wtot[k], pre);
-        uint32_t excl = __shfl_up_sync(0xffffffffu, incl, 1);
-        if (lane == 0) excl = kTfIdentity;
-        excl = tf_compose(excl, pre);
-        const int c_in = w == 0 ? 0 : tf_apply(excl, s_carry);   // no carry into a row's word 0
+        if (threadIdx.x == 0) {
+            uint32_t c = s_c1;
+            for (int k = 0; k < nw; ++k) { wcin1[k] = c; c = (wtf1[k] >> c) & 1u; }
+            s_c1 = c;
+            s_hi = whi[nw - 1];
+        }
+        __syncthreads();
+        w1 += (uint32_t)(((A1 + B1 + wcin1[warp]) ^ A1 ^ B1) >> lane) & 1u;
+        // chain 2: - B-
+        const unsigned G2 = __ballot_sync(0xffffffffu, valid && !last && w1 < bm);
+        const unsigned P2 = __ballot_sync(0xffffffffu, valid && !last && w1 == bm);
+        const uint64_t A2 = (uint64_t)(G2 | P2), B2 = (uint64_t)G2;
+        if (lane == 0) wtf2[warp] = (uint32_t)((A2 + B2) >> 32) | ((uint32_t)((A2 + B2 + 1) >> 32) << 1);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t c = s_c2;
+            for (int k = 0; k < nw; ++k) { wcin2[k] = c; c = (wtf2[k] >> c) & 1u; }
+            s_c2 = c;
+        }
+        __syncthreads();
+        const uint32_t bor = (uint32_t)(((A2 + B2 + wcin2[warp]) ^ A2 ^ B2) >> lane) & 1u;
         if (valid) {
             const uint32_t prow = bitrev(pos0 + r, A.lgS);
-            if (prow < A.rows_out) A.out[(int64_t)prow * W32 + w] = (uint32_t)(x + c_in);
+            if (prow < A.rows_out) A.out[(int64_t)prow * W32 + w] = w1 - bm - bor;
         }
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) {
-            uint32_t all = kTfIdentity;
-            for (int k = 0; k < nw; ++k) all = tf_compose(wtot[k], all);
-            s_carry = tf_apply(all, s_carry);
-            s_hi = hi;
-        }
-        __syncthreads();
     }
 }
 
@@ -685,7 +710,7 @@ __global__ void k_ntt_probe(uint32_t* data, int lg, const uint2* twf, const uint
     const uint32_t n = 1u << lg;
     for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) s[padi(e)] = data[e];
     __syncthreads();
-    const TwRows tw{dir ? twi : twf, nullptr, lg, 0};
+    const TwRows tw{dir ? twi : twf, nullptr, lg};
     if (dir == 0) run_bits<true>(s, lg, 0, lg, tw, pc.p, pc.two_p);
     else run_bits<false>(s, lg, 0, lg, tw, pc.p, pc.two_p);
     for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) data[e] = canon(s[padi(e)], pc.p);
