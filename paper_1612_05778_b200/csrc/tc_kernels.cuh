@@ -91,6 +91,60 @@ __device__ __forceinline__ uint32_t bitrev(uint32_t x, int bits) {
 __device__ __forceinline__ uint32_t padi(uint32_t e) { return e + (e >> 4); }
 __host__ __device__ constexpr uint32_t padded_words(uint32_t n) { return n + (n >> 4) + 1; }
 
+// Tile copies between global and (padded) shared memory.  Slots come in
+// aligned runs of 4 that are contiguous in both layouts (tile index e..e+3 ->
+// grid index gidx(e)..gidx(e)+3, and padi is linear inside an aligned run of
+// 16), so each thread moves 16 bytes per LDG.128 / STG.128; kBatch vector
+// loads stay in flight per thread.  Requires n % 4 == 0 and gidx(e) % 4 == 0
+// for e % 4 == 0 (callers fall back to tile_*_scalar otherwise).
+constexpr int kBatch = 4;
+
+template <class F>
+__device__ __forceinline__ void tile_load(uint32_t* s, const uint32_t* g, uint32_t n, F gidx) {
+    const uint32_t nv = n >> 2, st = blockDim.x;
+    for (uint32_t v0 = threadIdx.x; v0 < nv; v0 += kBatch * st) {
+        uint4 v[kBatch];
+#pragma unroll
+        for (int k = 0; k < kBatch; ++k) {
+            const uint32_t vi = v0 + k * st;
+            v[k] = vi < nv ? *reinterpret_cast<const uint4*>(g + gidx(vi << 2)) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int k = 0; k < kBatch; ++k) {
+            const uint32_t vi = v0 + k * st;
+            if (vi < nv) {
+                uint32_t* d = s + padi(vi << 2);
+                d[0] = v[k].x; d[1] = v[k].y; d[2] = v[k].z; d[3] = v[k].w;
+            }
+        }
+    }
+}
+
+template <class F>
+__device__ __forceinline__ void tile_store(uint32_t* g, const uint32_t* s, uint32_t n, F gidx) {
+    const uint32_t nv = n >> 2;
+    for (uint32_t vi = threadIdx.x; vi < nv; vi += blockDim.x) {
+        const uint32_t* d = s + padi(vi << 2);
+        *reinterpret_cast<uint4*>(g + gidx(vi << 2)) = make_uint4(d[0], d[1], d[2], d[3]);
+    }
+}
+
+template <class F>
+__device__ __forceinline__ void tile_load_scalar(uint32_t* s, const uint32_t* g, uint32_t n, F gidx) {
+    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) s[padi(e)] = g[gidx(e)];
+}
+
+template <class F>
+__device__ __forceinline__ void tile_store_scalar(uint32_t* g, const uint32_t* s, uint32_t n, F gidx) {
+    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) g[gidx(e)] = s[padi(e)];
+}
+
+struct Contig { __device__ __forceinline__ uint32_t operator()(uint32_t e) const { return e; } };
+struct HighIdx {
+    uint32_t base; int cb, b0; uint32_t cmask;
+    __device__ __forceinline__ uint32_t operator()(uint32_t e) const { return base | ((e >> cb) << b0) | (e & cmask); }
+};
+
 // ---------------------------------------------------------------------------
 // Balanced digits (tc/_kernels.py:78-119) for up to R rows of one CTA.
 // chunk j of coefficient i = bits [jM, jM+M) of its N-bit sign-extended
@@ -104,6 +158,21 @@ __host__ __device__ constexpr uint32_t padded_words(uint32_t n) { return n + (n 
 // err[0]: first coefficient whose top digit overflows; err[1]: first
 // coefficient outside the plan's N-bit range (tc/codec.py:78-83).
 // ---------------------------------------------------------------------------
+// Two-level carry lookahead across the warps of a CTA, run by warp 0: tf[w]
+// bit 0 = carry out of warp w for carry-in 0, bit 1 = for carry-in 1.  Writes
+// the carry into every warp and advances *carry (the carry into the next round).
+__device__ __forceinline__ void warp_carry_scan(const uint32_t* tf, uint32_t* cin, uint32_t* carry,
+                                                int nwarps, int lane) {
+    const uint32_t t = lane < nwarps ? tf[lane] : 0u;
+    const unsigned G = __ballot_sync(0xffffffffu, t & 1u);
+    const unsigned Pm = __ballot_sync(0xffffffffu, (t >> 1) & ~t & 1u);
+    const uint64_t A = (uint64_t)(G | Pm), B = (uint64_t)G;
+    const uint64_t sum = A + B + *carry;
+    if (lane < nwarps) cin[lane] = (uint32_t)(((sum ^ A ^ B) >> lane) & 1u);
+    __syncwarp();
+    if (lane == 0) *carry = (uint32_t)(sum >> nwarps) & 1u;
+}
+
 struct DigitSrc {
     const uint64_t* words; int64_t d; int cw;
     int64_t K; int lgK; int M; int64_t N;
@@ -172,11 +241,7 @@ __device__ void compute_digits(const DigitSrc& a, int R, const int64_t* coeff, i
         if (lane == 0)
             ds.warp_tf[warp] = (uint32_t)((A + B) >> 32) | ((uint32_t)((A + B + 1) >> 32) << 1);
         __syncthreads();
-        if (tid == 0) {
-            uint32_t c = ds.round_carry;
-            for (int w = 0; w < nwarps; ++w) { ds.warp_cin[w] = c; c = (ds.warp_tf[w] >> c) & 1u; }
-            ds.round_carry = c;
-        }
+        if (warp == 0) warp_carry_scan(ds.warp_tf, ds.warp_cin, &ds.round_carry, nwarps, lane);
         __syncthreads();
         const uint64_t cin = ds.warp_cin[warp];
         const uint32_t carries = (uint32_t)((A + B + cin) ^ A ^ B);
@@ -229,7 +294,7 @@ __device__ __forceinline__ void round_exec(uint32_t* s, int tile_bits, int bit_l
     const uint32_t lowmask = (1u << bit_lo) - 1;
     const uint32_t astep = bit_lo >= 4 ? (1u << bit_lo) + (1u << (bit_lo - 4)) : (1u << bit_lo);
     const uint2* tp = tw.table(bit_lo);
-    const int tsh = tw.shift(bit_lo);
+    const uint32_t tstep = 1u << tw.shift(bit_lo);
     for (uint32_t g = threadIdx.x; g < ngroups; g += blockDim.x) {
         const uint32_t lo = g & lowmask;
         const uint32_t a0 = padi(((g & ~lowmask) << NB) | lo);
@@ -239,10 +304,10 @@ __device__ __forceinline__ void round_exec(uint32_t* s, int tile_bits, int bit_l
 #pragma unroll
         for (int it = 0; it < NB; ++it) {
             const int lv = DIF ? NB - 1 - it : it;
-            const uint32_t tb = tw.base(lo, bit_lo + lv);
+            const uint2* tq = tp + tw.base(lo, bit_lo + lv);   // one 64-bit address per level
 #pragma unroll
             for (int m = 0; m < (1 << lv); ++m) {
-                const uint2 w = __ldg(&tp[tb + ((uint32_t)m << tsh)]);
+                const uint2 w = __ldg(tq + m * tstep);
 #pragma unroll
                 for (int jj = 0; jj < R / (2 << lv); ++jj) {
                     const int k = m + jj * (2 << lv);
@@ -389,7 +454,8 @@ __global__ void __launch_bounds__(512, 2) k_low(LowArgs A) {
         run_bits<true>(tile, tile_bits, 0, A.lgL, tw, pc.p, pc.two_p);          // x: DIF
         run_bits<false>(tile, tile_bits, A.lgL, tile_bits, tw, pc.p, pc.two_p); // y low: DIT
         uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)blockIdx.x * n;
-        for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) g[e] = tile[padi(e)];
+        if (n >= 4) tile_store(g, tile, n, Contig{});
+        else tile_store_scalar(g, tile, n, Contig{});
         __syncthreads();
     }
 }
@@ -426,19 +492,32 @@ __global__ void __launch_bounds__(512, 2) k_high(HighArgs A) {
     const int tile_bits = A.U + A.cb;
     const uint32_t n = 1u << tile_bits;
     const uint32_t cmask = (1u << A.cb) - 1;
-    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x)
-        s[padi(e)] = g[base | ((e >> A.cb) << b0) | (e & cmask)];
+    const HighIdx hidx{base, A.cb, b0, cmask};
+    if (A.cb >= 2) tile_load(s, g, n, hidx);
+    else tile_load_scalar(s, g, n, hidx);
     __syncthreads();
     const TwHigh tf{A.twf + (int64_t)q * A.tw_stride, A.lgL, A.u0, A.cb, mid << A.cb};
     if (MODE == MODE_FWD || MODE == MODE_MID)
         run_bits<false>(s, tile_bits, A.cb, tile_bits, tf, pc.p, pc.two_p);
     if (MODE == MODE_MID) {
         const uint32_t* ga = A.other + (int64_t)q * A.S;
-        for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
-            const uint32_t f = base | ((e >> A.cb) << b0) | (e & cmask);
-            const uint32_t x = reduce_2p(s[padi(e)], pc.two_p);
-            const uint32_t y = reduce_2p(ga[f], pc.two_p);
-            s[padi(e)] = shoup_mul(mont_mul(x, y, pc.p, pc.pinv_neg), pc.scale, pc.scale_sh, pc.p);
+        const uint32_t st = blockDim.x;
+        for (uint32_t e0 = threadIdx.x; e0 < n; e0 += 8 * st) {
+            uint32_t y[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t e = e0 + k * st;
+                y[k] = e < n ? ga[hidx(e)] : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t e = e0 + k * st;
+                if (e < n) {
+                    const uint32_t x = reduce_2p(s[padi(e)], pc.two_p);
+                    s[padi(e)] = shoup_mul(mont_mul(x, reduce_2p(y[k], pc.two_p), pc.p, pc.pinv_neg),
+                                           pc.scale, pc.scale_sh, pc.p);
+                }
+            }
         }
         __syncthreads();
     }
@@ -447,8 +526,8 @@ __global__ void __launch_bounds__(512, 2) k_high(HighArgs A) {
         ti.twy = A.twi + (int64_t)q * A.tw_stride;
         run_bits<true>(s, tile_bits, A.cb, tile_bits, ti, pc.p, pc.two_p);
     }
-    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x)
-        g[base | ((e >> A.cb) << b0) | (e & cmask)] = s[padi(e)];
+    if (A.cb >= 2) tile_store(g, s, n, hidx);
+    else tile_store_scalar(g, s, n, hidx);
 }
 
 // ---------------------------------------------------------------------------
@@ -554,7 +633,7 @@ struct FinalArgs {
 template <int P, bool DUMP>
 __global__ void __launch_bounds__(512, 2) k_final(FinalArgs A, const __grid_constant__ CrtConst cc) {
     extern __shared__ __align__(16) uint32_t sm[];
-    __shared__ uint32_t wtf1[32], wtf2[32], wcin1[32], wcin2[32];
+    __shared__ uint32_t wtf[32], warp_tf1[32], wcin1[32], wcin2[32];
     __shared__ int64_t whi[32];
     __shared__ uint32_t s_c1, s_c2;
     __shared__ int64_t s_hi;
@@ -576,7 +655,8 @@ __global__ void __launch_bounds__(512, 2) k_final(FinalArgs A, const __grid_cons
         const PrimeC pc = A.pcs[q];
         uint32_t* t = sm + q * stride;
         const uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)blockIdx.x * n;
-        for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) t[padi(e)] = g[e];
+        if (n >= 4) tile_load(t, g, n, Contig{});
+        else tile_load_scalar(t, g, n, Contig{});
         __syncthreads();
         const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
         run_bits<true>(t, tile_bits, A.lgL, tile_bits, tw, pc.p, pc.two_p);   // y low: DIF
@@ -608,7 +688,9 @@ __global__ void __launch_bounds__(512, 2) k_final(FinalArgs A, const __grid_cons
     //            = A + B+ - B-  (B+ / B- the positive / negative hi parts):
     // chain 1 adds B+ (carries), chain 2 subtracts B- (borrows); each is a
     // binary generate/propagate chain resolved per warp by one 64-bit add of
-    // ballot masks and across warps by a serial scan of per-warp transfer bits.
+    // ballot masks and across warps by warp 0's ballot scan of per-warp
+    // transfer bits (chain 2's per-warp masks are kept for both chain-1
+    // carry-ins, so one pass of warp 0 resolves both chains).
     // The last word of a row never generates or propagates, so chains never
     // cross rows; carries out of a row's top word are the mod 2^(32 W32) wrap.
     const int M = A.M, W32 = A.W32;
@@ -648,38 +730,45 @@ __global__ void __launch_bounds__(512, 2) k_final(FinalArgs A, const __grid_cons
         if (lane == 0) hprev = warp > 0 ? whi[warp - 1] : s_hi;
         const int64_t bb = w == 0 ? 0 : hprev;
         const uint32_t bp = bb > 0 ? (uint32_t)bb : 0u, bm = bb < 0 ? (uint32_t)(-bb) : 0u;
-        // chain 1: lo + B+
+        const bool live = valid && !last;
+        // chain 1: lo + B+, carries inside the warp for warp carry-in 0 and 1
         const uint64_t t1 = (uint64_t)(uint32_t)sum + bp;
-        uint32_t w1 = (uint32_t)t1;
-        const unsigned G1 = __ballot_sync(0xffffffffu, valid && !last && (t1 >> 32));
-        const unsigned P1 = __ballot_sync(0xffffffffu, valid && !last && w1 == 0xffffffffu);
+        const uint32_t w1 = (uint32_t)t1;
+        const unsigned G1 = __ballot_sync(0xffffffffu, live && (t1 >> 32));
+        const unsigned P1 = __ballot_sync(0xffffffffu, live && w1 == 0xffffffffu);
         const uint64_t A1 = (uint64_t)(G1 | P1), B1 = (uint64_t)G1;
-        if (lane == 0) wtf1[warp] = (uint32_t)((A1 + B1) >> 32) | ((uint32_t)((A1 + B1 + 1) >> 32) << 1);
+        const uint32_t w1v[2] = {w1 + (uint32_t)((((A1 + B1) ^ A1 ^ B1) >> lane) & 1u),
+                                 w1 + (uint32_t)((((A1 + B1 + 1) ^ A1 ^ B1) >> lane) & 1u)};
+        // chain 2: - B-, masks for both chain-1 variants
+        uint64_t A2[2], B2[2];
+        uint32_t tf = (uint32_t)((A1 + B1) >> 32) | ((uint32_t)((A1 + B1 + 1) >> 32) << 1);
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            const unsigned G2 = __ballot_sync(0xffffffffu, live && w1v[v] < bm);
+            const unsigned P2 = __ballot_sync(0xffffffffu, live && w1v[v] == bm);
+            A2[v] = (uint64_t)(G2 | P2); B2[v] = (uint64_t)G2;
+            tf |= ((uint32_t)((A2[v] + B2[v]) >> 32) | ((uint32_t)((A2[v] + B2[v] + 1) >> 32) << 1)) << (2 + 2 * v);
+        }
+        if (lane == 0) wtf[warp] = tf;
         __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t c = s_c1;
-            for (int k = 0; k < nw; ++k) { wcin1[k] = c; c = (wtf1[k] >> c) & 1u; }
-            s_c1 = c;
-            s_hi = whi[nw - 1];
+        if (warp == 0) {
+            const uint32_t t = lane < nw ? wtf[lane] : 0u;
+            warp_tf1[lane] = t & 3u;
+            __syncwarp();
+            warp_carry_scan(warp_tf1, wcin1, &s_c1, nw, lane);
+            __syncwarp();
+            const uint32_t c1 = lane < nw ? wcin1[lane] : 0u;
+            warp_tf1[lane] = (t >> (2 + 2 * c1)) & 3u;
+            __syncwarp();
+            warp_carry_scan(warp_tf1, wcin2, &s_c2, nw, lane);
+            if (lane == 0) s_hi = whi[nw - 1];
         }
         __syncthreads();
-        w1 += (uint32_t)(((A1 + B1 + wcin1[warp]) ^ A1 ^ B1) >> lane) & 1u;
-        // chain 2: - B-
-        const unsigned G2 = __ballot_sync(0xffffffffu, valid && !last && w1 < bm);
-        const unsigned P2 = __ballot_sync(0xffffffffu, valid && !last && w1 == bm);
-        const uint64_t A2 = (uint64_t)(G2 | P2), B2 = (uint64_t)G2;
-        if (lane == 0) wtf2[warp] = (uint32_t)((A2 + B2) >> 32) | ((uint32_t)((A2 + B2 + 1) >> 32) << 1);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t c = s_c2;
-            for (int k = 0; k < nw; ++k) { wcin2[k] = c; c = (wtf2[k] >> c) & 1u; }
-            s_c2 = c;
-        }
-        __syncthreads();
-        const uint32_t bor = (uint32_t)(((A2 + B2 + wcin2[warp]) ^ A2 ^ B2) >> lane) & 1u;
+        const uint32_t c1 = wcin1[warp];
+        const uint32_t bor = (uint32_t)(((A2[c1] + B2[c1] + wcin2[warp]) ^ A2[c1] ^ B2[c1]) >> lane) & 1u;
         if (valid) {
             const uint32_t prow = bitrev(pos0 + r, A.lgS);
-            if (prow < A.rows_out) A.out[(int64_t)prow * W32 + w] = w1 - bm - bor;
+            if (prow < A.rows_out) A.out[(int64_t)prow * W32 + w] = w1v[c1] - bm - bor;
         }
     }
 }

@@ -44,11 +44,16 @@ def report(path):
             if key in idx:
                 print(f"   {label:22s} {r[idx[key]]} {units[idx[key]]}")
         stalls = [(h, r[i]) for h, i in idx.items()
-                  if h.startswith("smsp__average_warp_latency_issue_stalled_") or
-                  (h.startswith("smsp__warp_issue_stalled_") and h.endswith("_per_warp_active.pct"))]
-        top = sorted(((float(v or 0), h) for h, v in stalls if v.replace('.', '', 1).isdigit()), reverse=True)[:8]
-        for v, h in top:
-            print(f"   stall {h.split('stalled_')[-1]:40s} {v}")
+                  if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("_not_issued")]
+        vals = []
+        for h, v in stalls:
+            try:
+                vals.append((float(v.replace(",", "")), h))
+            except ValueError:
+                pass
+        tot = sum(v for v, _ in vals) or 1.0
+        for v, h in sorted(vals, reverse=True)[:8]:
+            print(f"   stall {h.split('stalled_')[-1]:28s} {v / tot:6.1%}")
 
 
 def launches(path):
