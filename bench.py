@@ -64,14 +64,20 @@ class ClockSampler:
         self.proc = None
         self.lines = []
 
-    def start(self):
+    def start(self, wait_s: float = 5.0):
+        """Start sampling every 50 ms and wait for the first sample, so the
+        measurement that follows is covered from its first step."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < wait_s:
+                time.sleep(0.01)
+            self.skip = len(self.lines)
         except (OSError, FileNotFoundError):
             self.proc = None
 
@@ -88,7 +94,7 @@ class ClockSampler:
                 self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        for ln in self.lines[getattr(self, "skip", 0):]:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -208,18 +214,17 @@ def run_ours(args, rank, world, local):
         _lib.check(lib.tc_event_elapsed(h, 0, 1, ctypes.byref(ms)), "elapsed")
         return ms.value
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         step_timed(resident_step)
     _barrier(world)
-    clocks = ClockSampler(local)
-    clocks.start()
     l0 = ctx.launches()
     times = [step_timed(resident_step) for _ in range(args.steps)]
     launches = ctx.launches() - l0
     # per-stage profile of one more step (same work) for the roofline
     prof = (ctypes.c_double * 8)()
     lib.tc_last_profile(h, prof, None)
-    clock_info = clocks.stop()
     dev_ms = float(np.sum(times))
     dev_ms_max = _max_over_ranks(dev_ms, world)
 
@@ -242,6 +247,8 @@ def run_ours(args, rank, world, local):
         prod = tc.multiply(tc.MulRequest(A, B))
         e2e.append(time.perf_counter() - t0)
         del prod
+    clock_info = clocks.stop()
+    clock_info["window"] = "sampled every 50 ms over the warm-up, timed and e2e loops"
     e2e_s = _max_over_ranks(float(np.sum(e2e)), world)
 
     out_gbit = rows * out_bits / 1e9

@@ -67,7 +67,7 @@ def launches(path):
         if len(r) <= vi:
             continue
         v = float(r[vi].replace(",", ""))
-        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[mi], 1.0)
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[mi], 1.0)
         name = r[ki].split("(")[0]
         tot[name] += v * scale
         cnt[name] += 1
