@@ -289,9 +289,9 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     a.twx = c->twx_f.as<uint2>(); a.twy = c->twy_f.as<uint2>();
     a.twy_stride = G.s_y;
     a.pcs = c->pcs.as<PrimeC>(); a.P = G.P;
-    const int R = 1 << G.yl;
+    const int Rc = G.yl >= 1 ? 1 << (G.yl - 1) : 1;      // computed (even) rows, see k_low
     const uint32_t n = 1u << (G.lgL + G.yl);
-    const size_t smem = (size_t)R * G.K * 8 + (size_t)R * 8 + (size_t)padded_words(n) * 4;
+    const size_t smem = (size_t)Rc * G.K * 8 + (size_t)Rc * 8 + (size_t)padded_words(n) * 4;
     if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_low, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t ctas = G.S / n;
     k_low<<<(unsigned)ctas, 512, smem, c->st>>>(a);

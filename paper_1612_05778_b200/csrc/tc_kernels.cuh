@@ -417,20 +417,26 @@ struct LowArgs {
 
 __global__ void __launch_bounds__(512, 2) k_low(LowArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int R = 1 << A.yl;
+    const int R = 1 << A.yl;                 // row positions in the tile
+    // Odd positions hold coefficients >= s_y/2 >= d: zero rows.  With yl >= 1
+    // only the even rows are converted and x-transformed; the first y level
+    // (DIT on (x, 0) pairs) then is a duplication x -> (x, x).
+    const bool prune = A.yl >= 1;
+    const int Rc = prune ? R >> 1 : R;
     const int L = 1 << A.lgL;
     const int tile_bits = A.lgL + A.yl;
-    const uint32_t n = 1u << tile_bits;
+    const int cbits = tile_bits - (prune ? 1 : 0);
+    const uint32_t n = 1u << tile_bits, nc = 1u << cbits;
     int64_t* dig = reinterpret_cast<int64_t*>(smem_raw);
-    int64_t* coeff = dig + (int64_t)R * A.src.K;
-    uint32_t* tile = reinterpret_cast<uint32_t*>(coeff + R);
+    int64_t* coeff = dig + (int64_t)Rc * A.src.K;
+    uint32_t* tile = reinterpret_cast<uint32_t*>(coeff + Rc);
     __shared__ DigitScratch ds;
     __shared__ int s_nvalid;
     const uint32_t pos0 = blockIdx.x * (uint32_t)R;
     if (threadIdx.x == 0) s_nvalid = 0;
     __syncthreads();
-    for (int r = threadIdx.x; r < R; r += blockDim.x) {
-        const int64_t i = bitrev(pos0 + r, A.lgS);
+    for (int r = threadIdx.x; r < Rc; r += blockDim.x) {
+        const int64_t i = bitrev(pos0 + (prune ? 2 * r : r), A.lgS);
         coeff[r] = i < A.src.d ? i : -1;
         if (i < A.src.d) atomicAdd(&s_nvalid, 1);
     }
@@ -442,17 +448,40 @@ __global__ void __launch_bounds__(512, 2) k_low(LowArgs A) {
         }
         return;
     }
-    compute_digits(A.src, R, coeff, dig, ds);
+    compute_digits(A.src, Rc, coeff, dig, ds);
     for (int q = 0; q < A.P; ++q) {
         const PrimeC pc = A.pcs[q];
-        for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
+        for (uint32_t e = threadIdx.x; e < nc; e += blockDim.x) {
             const uint32_t r = e >> A.lgL, j = e & (L - 1);
             tile[padi(e)] = (j < A.src.K && coeff[r] >= 0) ? digit_residue(dig[(int64_t)r * A.src.K + j], pc) : 0u;
         }
         __syncthreads();
         const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
-        run_bits<true>(tile, tile_bits, 0, A.lgL, tw, pc.p, pc.two_p);          // x: DIF
-        run_bits<false>(tile, tile_bits, A.lgL, tile_bits, tw, pc.p, pc.two_p); // y low: DIT
+        run_bits<true>(tile, cbits, 0, A.lgL, tw, pc.p, pc.two_p);               // x: DIF, computed rows
+        if (prune) {
+            // expand in place, highest chunk first: compact e -> rows 2r', 2r'+1
+            const uint32_t chunk = 8u * blockDim.x;
+            for (int64_t c0 = (int64_t)((nc - 1) / chunk) * chunk; c0 >= 0; c0 -= chunk) {
+                uint32_t v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t e = (uint32_t)c0 + k * blockDim.x + threadIdx.x;
+                    v[k] = e < nc ? tile[padi(e)] : 0u;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t e = (uint32_t)c0 + k * blockDim.x + threadIdx.x;
+                    if (e < nc) {
+                        const uint32_t d0 = ((e >> A.lgL) << (A.lgL + 1)) | (e & (L - 1));
+                        tile[padi(d0)] = v[k];
+                        tile[padi(d0 + L)] = v[k];
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        run_bits<false>(tile, tile_bits, A.lgL + (prune ? 1 : 0), tile_bits, tw, pc.p, pc.two_p);  // y: DIT
         uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)blockIdx.x * n;
         if (n >= 4) tile_store(g, tile, n, Contig{});
         else tile_store_scalar(g, tile, n, Contig{});
@@ -698,54 +727,88 @@ __global__ void __launch_bounds__(512, 2) k_final(FinalArgs A, const __grid_cons
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (threadIdx.x == 0) { s_c1 = 0; s_c2 = 0; s_hi = 0; }
     __syncthreads();
-    for (int64_t gb = 0; gb < total; gb += blockDim.x) {
-        const int64_t gi = gb + threadIdx.x;
-        const bool valid = gi < total;
-        const int r = valid ? (int)(gi / W32) : R;
-        const int w = valid ? (int)(gi - (int64_t)r * W32) : 0;
-        const bool last = w == W32 - 1;
+    // S_w of output word w of tile row r: the 32-bit pieces of every shifted
+    // term c_rj 2^(Mj) overlapping w (unsigned pieces, signed top piece).
+    auto word_sum = [&](int r, int w) -> int64_t {
+        const int lo_n = 32 * (w - P);
+        const int jf = lo_n <= 0 ? 0 : div_m(lo_n + M - 1, M, A.minv);
+        const int jl = min(L - 2, div_m(32 * w + 31, M, A.minv));
+        const uint32_t rowbase = (uint32_t)r << A.lgL;
         int64_t sum = 0;
-        if (valid) {
-            const int lo_n = 32 * (w - P);
-            const int jf = lo_n <= 0 ? 0 : div_m(lo_n + M - 1, M, A.minv);
-            const int jl = min(L - 2, div_m(32 * w + 31, M, A.minv));
-            const uint32_t rowbase = (uint32_t)r << A.lgL;
-            int bit = M * jf;
-            for (int j = jf; j <= jl; ++j, bit += M) {
-                const int k = w - (bit >> 5);
-                const int rr = bit & 31;
-                const uint32_t e = padi(rowbase + j);
-                const uint32_t top = sm[(P - 1) * stride + e];
-                const uint32_t sgn = (top >> 31) ? 0xffffffffu : 0u;
-                const uint32_t cur = k < P ? sm[k * stride + e] : sgn;
-                const uint32_t prv = k > 0 ? sm[(k - 1) * stride + e] : 0u;
-                const uint32_t piece = rr ? ((cur << rr) | (prv >> (32 - rr))) : cur;
-                sum += k < P ? (int64_t)piece : (int64_t)(int32_t)piece;
+        int bit = M * jf;
+        for (int j = jf; j <= jl; ++j, bit += M) {
+            const int k = w - (bit >> 5);
+            const int rr = bit & 31;
+            const uint32_t e = padi(rowbase + j);
+            const uint32_t top = sm[(P - 1) * stride + e];
+            const uint32_t sgn = (top >> 31) ? 0xffffffffu : 0u;
+            const uint32_t cur = k < P ? sm[k * stride + e] : sgn;
+            const uint32_t prv = k > 0 ? sm[(k - 1) * stride + e] : 0u;
+            const uint32_t piece = rr ? ((cur << rr) | (prv >> (32 - rr))) : cur;
+            sum += k < P ? (int64_t)piece : (int64_t)(int32_t)piece;
+        }
+        return sum;
+    };
+    constexpr int kW = 4;                     // consecutive words per thread per round
+    for (int64_t gb = 0; gb < total; gb += (int64_t)blockDim.x * kW) {
+        const int64_t g0 = gb + (int64_t)threadIdx.x * kW;
+        int rw[kW], ww[kW];
+        bool valid[kW], live[kW];
+        int64_t sum[kW];
+        {
+            int r = (int)(min(g0, total) / W32), w = (int)(min(g0, total) - (int64_t)r * W32);
+#pragma unroll
+            for (int k = 0; k < kW; ++k) {
+                valid[k] = g0 + k < total;
+                rw[k] = r; ww[k] = w;
+                live[k] = valid[k] && w != W32 - 1;     // a row's top word never carries on
+                sum[k] = valid[k] ? word_sum(r, w) : 0;
+                if (++w == W32) { w = 0; ++r; }
             }
         }
-        const int64_t hi = sum >> 32;
-        int64_t hprev = __shfl_up_sync(0xffffffffu, hi, 1);
-        if (lane == 31) whi[warp] = hi;
+        // hi of the word before each word
+        const int64_t hlast = sum[kW - 1] >> 32;
+        int64_t hprev0 = __shfl_up_sync(0xffffffffu, hlast, 1);
+        if (lane == 31) whi[warp] = hlast;
         __syncthreads();
-        if (lane == 0) hprev = warp > 0 ? whi[warp - 1] : s_hi;
-        const int64_t bb = w == 0 ? 0 : hprev;
-        const uint32_t bp = bb > 0 ? (uint32_t)bb : 0u, bm = bb < 0 ? (uint32_t)(-bb) : 0u;
-        const bool live = valid && !last;
-        // chain 1: lo + B+, carries inside the warp for warp carry-in 0 and 1
-        const uint64_t t1 = (uint64_t)(uint32_t)sum + bp;
-        const uint32_t w1 = (uint32_t)t1;
-        const unsigned G1 = __ballot_sync(0xffffffffu, live && (t1 >> 32));
-        const unsigned P1 = __ballot_sync(0xffffffffu, live && w1 == 0xffffffffu);
+        if (lane == 0) hprev0 = warp > 0 ? whi[warp - 1] : s_hi;
+        uint32_t w1[kW], bm[kW];
+        bool g1[kW], p1[kW];
+#pragma unroll
+        for (int k = 0; k < kW; ++k) {
+            const int64_t bb = ww[k] == 0 ? 0 : (k == 0 ? hprev0 : (sum[k - 1] >> 32));
+            const uint32_t bp = bb > 0 ? (uint32_t)bb : 0u;
+            bm[k] = bb < 0 ? (uint32_t)(-bb) : 0u;
+            const uint64_t t1 = (uint64_t)(uint32_t)sum[k] + bp;
+            w1[k] = (uint32_t)t1;
+            g1[k] = live[k] && (t1 >> 32);
+            p1[k] = live[k] && w1[k] == 0xffffffffu;
+        }
+        // chain 1 (carries of lo + B+): thread block transfer, then warp ballot add
+        uint32_t c0 = 0, c1 = 1;
+#pragma unroll
+        for (int k = 0; k < kW; ++k) { c0 = g1[k] | (p1[k] & c0); c1 = g1[k] | (p1[k] & c1); }
+        const unsigned G1 = __ballot_sync(0xffffffffu, c0);
+        const unsigned P1 = __ballot_sync(0xffffffffu, c1 & !c0);
         const uint64_t A1 = (uint64_t)(G1 | P1), B1 = (uint64_t)G1;
-        const uint32_t w1v[2] = {w1 + (uint32_t)((((A1 + B1) ^ A1 ^ B1) >> lane) & 1u),
-                                 w1 + (uint32_t)((((A1 + B1 + 1) ^ A1 ^ B1) >> lane) & 1u)};
-        // chain 2: - B-, masks for both chain-1 variants
-        uint64_t A2[2], B2[2];
         uint32_t tf = (uint32_t)((A1 + B1) >> 32) | ((uint32_t)((A1 + B1 + 1) >> 32) << 1);
+        // chain 2 (borrows of - B-), for both warp carry-ins of chain 1
+        uint32_t w1v[2][kW];
+        uint64_t A2[2], B2[2];
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-            const unsigned G2 = __ballot_sync(0xffffffffu, live && w1v[v] < bm);
-            const unsigned P2 = __ballot_sync(0xffffffffu, live && w1v[v] == bm);
+            uint32_t c = (uint32_t)(((A1 + B1 + v) ^ A1 ^ B1) >> lane) & 1u;   // carry into this thread
+            uint32_t b0 = 0, b1 = 1;
+#pragma unroll
+            for (int k = 0; k < kW; ++k) {
+                w1v[v][k] = w1[k] + c;
+                c = g1[k] | (p1[k] & c);
+                const uint32_t g2 = live[k] && w1v[v][k] < bm[k];
+                const uint32_t p2 = live[k] && w1v[v][k] == bm[k];
+                b0 = g2 | (p2 & b0); b1 = g2 | (p2 & b1);
+            }
+            const unsigned G2 = __ballot_sync(0xffffffffu, b0);
+            const unsigned P2 = __ballot_sync(0xffffffffu, b1 & !b0);
             A2[v] = (uint64_t)(G2 | P2); B2[v] = (uint64_t)G2;
             tf |= ((uint32_t)((A2[v] + B2[v]) >> 32) | ((uint32_t)((A2[v] + B2[v] + 1) >> 32) << 1)) << (2 + 2 * v);
         }
@@ -757,18 +820,25 @@ __global__ void __launch_bounds__(512, 2) k_final(FinalArgs A, const __grid_cons
             __syncwarp();
             warp_carry_scan(warp_tf1, wcin1, &s_c1, nw, lane);
             __syncwarp();
-            const uint32_t c1 = lane < nw ? wcin1[lane] : 0u;
-            warp_tf1[lane] = (t >> (2 + 2 * c1)) & 3u;
+            const uint32_t cc = lane < nw ? wcin1[lane] : 0u;
+            warp_tf1[lane] = (t >> (2 + 2 * cc)) & 3u;
             __syncwarp();
             warp_carry_scan(warp_tf1, wcin2, &s_c2, nw, lane);
             if (lane == 0) s_hi = whi[nw - 1];
         }
         __syncthreads();
-        const uint32_t c1 = wcin1[warp];
-        const uint32_t bor = (uint32_t)(((A2[c1] + B2[c1] + wcin2[warp]) ^ A2[c1] ^ B2[c1]) >> lane) & 1u;
-        if (valid) {
-            const uint32_t prow = bitrev(pos0 + r, A.lgS);
-            if (prow < A.rows_out) A.out[(int64_t)prow * W32 + w] = w1v[c1] - bm - bor;
+        const uint32_t cv = wcin1[warp];
+        uint32_t bin = (uint32_t)(((A2[cv] + B2[cv] + wcin2[warp]) ^ A2[cv] ^ B2[cv]) >> lane) & 1u;
+#pragma unroll
+        for (int k = 0; k < kW; ++k) {
+            const uint32_t x = w1v[cv][k];
+            if (valid[k]) {
+                const uint32_t prow = bitrev(pos0 + rw[k], A.lgS);
+                if (prow < A.rows_out) A.out[(int64_t)prow * W32 + ww[k]] = x - bm[k] - bin;
+            }
+            const uint32_t g2 = live[k] && x < bm[k];
+            const uint32_t p2 = live[k] && x == bm[k];
+            bin = g2 | (p2 & bin);
         }
     }
 }
