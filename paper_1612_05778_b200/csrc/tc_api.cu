@@ -292,9 +292,15 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     const int Rc = G.yl >= 1 ? 1 << (G.yl - 1) : 1;      // computed (even) rows, see k_low
     const uint32_t n = 1u << (G.lgL + G.yl);
     const size_t smem = (size_t)Rc * G.K * 8 + (size_t)Rc * 8 + (size_t)padded_words(n) * 4;
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_low, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t ctas = G.S / n;
-    k_low<<<(unsigned)ctas, 512, smem, c->st>>>(a);
+    // a tile too large for two CTAs per SM gets 32 warps in one CTA
+    if (smem > 112 * 1024) {
+        CK(cudaFuncSetAttribute(k_low<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_low<1024><<<(unsigned)ctas, 1024, smem, c->st>>>(a);
+    } else {
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_low<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_low<512><<<(unsigned)ctas, 512, smem, c->st>>>(a);
+    }
     c->launches++;
     CKL();
     return TC_OK;
@@ -332,8 +338,13 @@ template <int P, bool DUMP>
 int launch_final_p(Ctx* c, const Geometry& G, const FinalArgs& A, const CrtConst& cc) {
     const uint32_t n = 1u << (G.lgL + G.yl);
     const size_t smem = (size_t)P * padded_words(n) * 4;
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_final<P, DUMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_final<P, DUMP><<<(unsigned)(G.S / n), 512, smem, c->st>>>(A, cc);
+    if (smem > 112 * 1024) {
+        CK(cudaFuncSetAttribute(k_final<P, DUMP, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_final<P, DUMP, 1024><<<(unsigned)(G.S / n), 1024, smem, c->st>>>(A, cc);
+    } else {
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_final<P, DUMP, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_final<P, DUMP, 512><<<(unsigned)(G.S / n), 512, smem, c->st>>>(A, cc);
+    }
     c->launches++;
     CKL();
     return TC_OK;
