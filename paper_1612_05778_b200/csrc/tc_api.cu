@@ -20,6 +20,13 @@
 
 using namespace tc;
 
+namespace tc {   // k_final launchers, one translation unit per prime-count range (tc_final_*.cu)
+cudaError_t launch_final_p1_4(int P, bool dump, const FinalArgs& A, const CrtConst& cc, unsigned grid, size_t smem, cudaStream_t st);
+cudaError_t launch_final_p5_8(int P, bool dump, const FinalArgs& A, const CrtConst& cc, unsigned grid, size_t smem, cudaStream_t st);
+cudaError_t launch_final_p9_12(int P, bool dump, const FinalArgs& A, const CrtConst& cc, unsigned grid, size_t smem, cudaStream_t st);
+cudaError_t launch_final_p13_16(int P, bool dump, const FinalArgs& A, const CrtConst& cc, unsigned grid, size_t smem, cudaStream_t st);
+}
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -334,22 +341,6 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
     return TC_OK;
 }
 
-template <int P, bool DUMP>
-int launch_final_p(Ctx* c, const Geometry& G, const FinalArgs& A, const CrtConst& cc) {
-    const uint32_t n = 1u << (G.lgL + G.yl);
-    const size_t smem = (size_t)P * padded_words(n) * 4;
-    if (smem > 112 * 1024) {
-        CK(cudaFuncSetAttribute(k_final<P, DUMP, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_final<P, DUMP, 1024><<<(unsigned)(G.S / n), 1024, smem, c->st>>>(A, cc);
-    } else {
-        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_final<P, DUMP, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_final<P, DUMP, 512><<<(unsigned)(G.S / n), 512, smem, c->st>>>(A, cc);
-    }
-    c->launches++;
-    CKL();
-    return TC_OK;
-}
-
 int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows, int M, int W32,
                  uint32_t* out, const CrtConst& cc, bool dump) {
     FinalArgs A{};
@@ -359,13 +350,17 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
     A.pcs = c->pcs.as<PrimeC>();
     A.rows_out = rows; A.M = M; A.minv = (uint32_t)(0xffffffffu / (uint32_t)M); A.W32 = W32;
     A.out = out; A.err = c->flags.as<int>();
-#define CASE(k) case k: return dump ? launch_final_p<k, true>(c, G, A, cc) : launch_final_p<k, false>(c, G, A, cc);
-    switch (G.P) {
-        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
-        CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
-    }
-#undef CASE
-    return set_err(TC_ERR_BAD_ARG, "P=%d unsupported", G.P);
+    const uint32_t n = 1u << (G.lgL + G.yl);
+    const size_t smem = (size_t)G.P * padded_words(n) * 4;
+    const unsigned grid = (unsigned)(G.S / n);
+    cudaError_t e;
+    if (G.P <= 4) e = launch_final_p1_4(G.P, dump, A, cc, grid, smem, c->st);
+    else if (G.P <= 8) e = launch_final_p5_8(G.P, dump, A, cc, grid, smem, c->st);
+    else if (G.P <= 12) e = launch_final_p9_12(G.P, dump, A, cc, grid, smem, c->st);
+    else e = launch_final_p13_16(G.P, dump, A, cc, grid, smem, c->st);
+    c->launches++;
+    if (e != cudaSuccess) return set_err(TC_ERR_CUDA, "k_final launch failed: %s", cudaGetErrorString(e));
+    return TC_OK;
 }
 
 // The whole product on the device: leaves the product words (or, with

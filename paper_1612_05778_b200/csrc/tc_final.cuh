@@ -1,0 +1,28 @@
+// tc_final.cuh -- k_final launcher template, instantiated for prime-count
+// ranges in tc_final_*.cu (separate translation units compile in parallel).
+#pragma once
+#include <cuda_runtime.h>
+#include "tc_kernels.cuh"
+
+namespace tc {
+
+template <int P>
+cudaError_t launch_final_t(bool dump, const FinalArgs& A, const CrtConst& cc, unsigned grid, size_t smem,
+                           cudaStream_t st) {
+    // a tile too large for two CTAs per SM gets 32 warps in one CTA
+    const bool big = smem > 112 * 1024;
+    cudaError_t e = cudaSuccess;
+#define TC_LAUNCH(DUMP, NT)                                                                       \
+    do {                                                                                          \
+        if (smem > 48 * 1024)                                                                     \
+            e = cudaFuncSetAttribute(k_final<P, DUMP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e != cudaSuccess) return e;                                                           \
+        k_final<P, DUMP, NT><<<grid, NT, smem, st>>>(A, cc);                                     \
+    } while (0)
+    if (dump) { if (big) TC_LAUNCH(true, 1024); else TC_LAUNCH(true, 512); }
+    else { if (big) TC_LAUNCH(false, 1024); else TC_LAUNCH(false, 512); }
+#undef TC_LAUNCH
+    return cudaGetLastError();
+}
+
+}  // namespace tc

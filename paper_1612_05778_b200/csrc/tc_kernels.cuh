@@ -38,7 +38,7 @@ constexpr int kMaxPrimes = 16;
 // Width scan: max two's-complement width and non-zero flag of a polynomial
 // (replaces the Python-int scans tc/params.py:290-293, tc/zpoly.py:103-114).
 // ---------------------------------------------------------------------------
-__global__ void k_width(const uint64_t* __restrict__ words, int64_t d, int cw, int* out) {
+static __global__ void k_width(const uint64_t* __restrict__ words, int64_t d, int cw, int* out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int width = 0, nz = 0;
     if (i < d) {
@@ -68,7 +68,7 @@ __global__ void k_width(const uint64_t* __restrict__ words, int64_t d, int cw, i
 // tables, laid out so a stage's twiddles are contiguous.
 struct PowTable { uint32_t f[32]; uint32_t i[32]; };
 
-__global__ void k_twiddles(uint2* fwd, uint2* inv, int64_t n, uint32_t p, PowTable pw, int lg) {
+static __global__ void k_twiddles(uint2* fwd, uint2* inv, int64_t n, uint32_t p, PowTable pw, int lg) {
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (idx >= n) return;
     if (idx == 0) { fwd[0] = make_uint2(1u, 0u); inv[0] = make_uint2(1u, 0u); return; }
@@ -187,7 +187,7 @@ __device__ __forceinline__ uint64_t limb_at(const uint64_t* row, int cw, int64_t
 struct DigitScratch { uint32_t warp_tf[32]; uint32_t warp_cin[32]; uint32_t round_carry; };
 
 // coeff[r] (r < R) is the coefficient index held by tile row r, or -1.
-__device__ void compute_digits(const DigitSrc& a, int R, const int64_t* coeff, int64_t* dig,
+static __device__ void compute_digits(const DigitSrc& a, int R, const int64_t* coeff, int64_t* dig,
                                DigitScratch& ds) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const int M = a.M;
@@ -264,7 +264,7 @@ __device__ void compute_digits(const DigitSrc& a, int R, const int64_t* coeff, i
 }
 
 // Parity seam: digits of coefficients [r0, r0+R) in natural order.
-__global__ void __launch_bounds__(256) k_digits(DigitSrc a, int R, int64_t* out) {
+static __global__ void __launch_bounds__(256) k_digits(DigitSrc a, int R, int64_t* out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     int64_t* dig = reinterpret_cast<int64_t*>(smem_raw);
     int64_t* coeff = dig + (int64_t)R * a.K;
@@ -531,23 +531,30 @@ __global__ void __launch_bounds__(512, 2) k_high(HighArgs A) {
         run_bits<false>(s, tile_bits, A.cb, tile_bits, tf, pc.p, pc.two_p);
     if (MODE == MODE_MID) {
         const uint32_t* ga = A.other + (int64_t)q * A.S;
-        const uint32_t st = blockDim.x;
-        for (uint32_t e0 = threadIdx.x; e0 < n; e0 += 8 * st) {
-            uint32_t y[8];
+        auto pw = [&](uint32_t e, uint32_t y) {
+            const uint32_t x = reduce_2p(s[padi(e)], pc.two_p);
+            s[padi(e)] = shoup_mul(mont_mul(x, reduce_2p(y, pc.two_p), pc.p, pc.pinv_neg),
+                                   pc.scale, pc.scale_sh, pc.p);
+        };
+        if (A.cb >= 2) {                       // 16-byte loads of A, 4 in flight per thread
+            const uint32_t nv = n >> 2, st = blockDim.x;
+            for (uint32_t v0 = threadIdx.x; v0 < nv; v0 += 4 * st) {
+                uint4 y[4];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const uint32_t e = e0 + k * st;
-                y[k] = e < n ? ga[hidx(e)] : 0u;
-            }
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t vi = v0 + k * st;
+                    y[k] = vi < nv ? *reinterpret_cast<const uint4*>(ga + hidx(vi << 2)) : make_uint4(0, 0, 0, 0);
+                }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const uint32_t e = e0 + k * st;
-                if (e < n) {
-                    const uint32_t x = reduce_2p(s[padi(e)], pc.two_p);
-                    s[padi(e)] = shoup_mul(mont_mul(x, reduce_2p(y[k], pc.two_p), pc.p, pc.pinv_neg),
-                                           pc.scale, pc.scale_sh, pc.p);
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t vi = v0 + k * st;
+                    if (vi < nv) {
+                        pw(vi * 4, y[k].x); pw(vi * 4 + 1, y[k].y); pw(vi * 4 + 2, y[k].z); pw(vi * 4 + 3, y[k].w);
+                    }
                 }
             }
+        } else {
+            for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) pw(e, ga[hidx(e)]);
         }
         __syncthreads();
     }
@@ -738,15 +745,17 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_final(FinalArgs A, c
         int64_t sum = 0;
         int bit = M * jf;
         for (int j = jf; j <= jl; ++j, bit += M) {
-            const int k = w - (bit >> 5);
+            const int k = w - (bit >> 5);              // piece index 0..P of term j
             const int rr = bit & 31;
             const uint32_t e = padi(rowbase + j);
-            const uint32_t top = sm[(P - 1) * stride + e];
-            const uint32_t sgn = (top >> 31) ? 0xffffffffu : 0u;
-            const uint32_t cur = k < P ? sm[k * stride + e] : sgn;
             const uint32_t prv = k > 0 ? sm[(k - 1) * stride + e] : 0u;
-            const uint32_t piece = rr ? ((cur << rr) | (prv >> (32 - rr))) : cur;
-            sum += k < P ? (int64_t)piece : (int64_t)(int32_t)piece;
+            if (k < P) {
+                const uint32_t cur = sm[k * stride + e];
+                sum += __funnelshift_l(prv, cur, rr);             // (cur:prv) << rr, high word
+            } else {                                               // signed top piece
+                const uint32_t sgn = (uint32_t)((int32_t)prv >> 31);
+                sum += (int64_t)(int32_t)__funnelshift_l(prv, sgn, rr);
+            }
         }
         return sum;
     };
@@ -757,7 +766,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_final(FinalArgs A, c
         bool valid[kW], live[kW];
         int64_t sum[kW];
         {
-            int r = (int)(min(g0, total) / W32), w = (int)(min(g0, total) - (int64_t)r * W32);
+            const uint32_t gc = (uint32_t)min(g0, total);
+            int r = (int)(gc / (uint32_t)W32), w = (int)(gc - (uint32_t)r * (uint32_t)W32);
 #pragma unroll
             for (int k = 0; k < kW; ++k) {
                 valid[k] = g0 + k < total;
@@ -848,7 +858,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_final(FinalArgs A, c
 // Probes: the kernels' own modular products, a standalone transform, and the
 // INT-pipe peak.
 // ---------------------------------------------------------------------------
-__global__ void k_modmul_probe(uint32_t p, uint32_t pinv_neg, const uint32_t* a, const uint32_t* b,
+static __global__ void k_modmul_probe(uint32_t p, uint32_t pinv_neg, const uint32_t* a, const uint32_t* b,
                                uint32_t* out, int64_t n, int mode) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -865,7 +875,7 @@ __global__ void k_modmul_probe(uint32_t p, uint32_t pinv_neg, const uint32_t* a,
 
 // One length-2^lg transform on one tile (tc_ntt_probe): forward = DIF
 // natural -> bit-reversed, inverse = DIT bit-reversed -> natural (unscaled).
-__global__ void k_ntt_probe(uint32_t* data, int lg, const uint2* twf, const uint2* twi, PrimeC pc, int dir) {
+static __global__ void k_ntt_probe(uint32_t* data, int lg, const uint2* twf, const uint2* twi, PrimeC pc, int dir) {
     extern __shared__ __align__(16) uint32_t s[];
     const uint32_t n = 1u << lg;
     for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) s[padi(e)] = data[e];
@@ -878,7 +888,7 @@ __global__ void k_ntt_probe(uint32_t* data, int lg, const uint2* twf, const uint
 
 // INT-pipe peak: 8 independent register chains per thread of the exact
 // butterfly (mode 0: DIF with Shoup twiddle) or Montgomery product (mode 1).
-__global__ void k_int_peak(uint32_t* sink, int iters, uint32_t p, uint32_t pinv_neg, int mode) {
+static __global__ void k_int_peak(uint32_t* sink, int iters, uint32_t p, uint32_t pinv_neg, int mode) {
     const uint32_t two_p = 2 * p;
     uint32_t x[8], y[8];
 #pragma unroll
