@@ -759,6 +759,32 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_final(FinalArgs A, c
         }
         return sum;
     };
+    // M >= 32: word w takes at most one piece from each piece index k = 0..P,
+    // from term j_k = ceil(32(w-k)/M) when M j_k < 32(w-k+1) -- a fixed,
+    // unrolled, divergence-free loop.
+    auto word_sum_wide = [&](int r, int w) -> int64_t {
+        const uint32_t rowbase = (uint32_t)r << A.lgL;
+        int64_t sum = 0;
+#pragma unroll
+        for (int k = 0; k <= P; ++k) {
+            const int base = 32 * (w - k);
+            if (base < 0) break;
+            const int j = div_m(base + M - 1, M, A.minv);
+            const int bit = M * j;
+            if (bit < base + 32 && j <= L - 2) {
+                const uint32_t e = padi(rowbase + j);
+                const int rr = bit & 31;
+                const uint32_t prv = k > 0 ? sm[(k - 1) * stride + e] : 0u;
+                if (k < P) {
+                    sum += __funnelshift_l(prv, sm[k * stride + e], rr);
+                } else {
+                    sum += (int64_t)(int32_t)__funnelshift_l(prv, (uint32_t)((int32_t)prv >> 31), rr);
+                }
+            }
+        }
+        return sum;
+    };
+    const bool wide = M >= 32;
     constexpr int kW = 4;                     // consecutive words per thread per round
     for (int64_t gb = 0; gb < total; gb += (int64_t)blockDim.x * kW) {
         const int64_t g0 = gb + (int64_t)threadIdx.x * kW;
@@ -773,7 +799,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_final(FinalArgs A, c
                 valid[k] = g0 + k < total;
                 rw[k] = r; ww[k] = w;
                 live[k] = valid[k] && w != W32 - 1;     // a row's top word never carries on
-                sum[k] = valid[k] ? word_sum(r, w) : 0;
+                sum[k] = valid[k] ? (wide ? word_sum_wide(r, w) : word_sum(r, w)) : 0;
                 if (++w == W32) { w = 0; ++r; }
             }
         }
