@@ -24,8 +24,9 @@ reference hashes in tests/golden/configs.json.
              numba kernels) on this host, all cores, one full C2 product.
 
 `--impl reference` times that same CPU restatement as the reference arm.
-N > 1 (torchrun): every rank runs its own product on its own GPU (replicas,
-weak scaling; no collective on the data path in this round), max over ranks.
+N > 1 (torchrun): ONE product sharded over the N GPUs (shard.py: row tiles <->
+column groups, two NCCL all-to-all transposes per product, gather to rank 0);
+"scaling": "strong", time = max over ranks of CUDA-event time on each rank.
 """
 from __future__ import annotations
 
@@ -314,6 +315,83 @@ def run_ours(args, rank, world, local):
         print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, rank, world, local):
+    """N > 1: one product over all ranks (strong scaling)."""
+    import torch
+    import paper_1612_05778_b200 as tc
+    from paper_1612_05778_b200 import _lib, shard, workloads
+    torch.cuda.set_device(local)
+    (aw, ab), (bw, bb) = workloads.make_inputs(args.config)
+    pa = _lib.pinned.empty(aw.shape, np.uint64)
+    pb = _lib.pinned.empty(bw.shape, np.uint64)
+    pa[...] = aw
+    pb[...] = bw
+    A, B = tc.IntPolynomial._trusted(pa, ab), tc.IntPolynomial._trusted(pb, bb)
+    dm = shard.DistributedMultiplier(local)
+    rows = aw.shape[0] + bw.shape[0] - 1
+    # correctness gate on rank 0
+    out, plan = dm.multiply(A, B)
+    verified = None
+    if rank == 0:
+        golden = json.load(open(os.path.join(ROOT, "tests", "golden", "configs.json"))).get(args.config)
+        if golden:
+            verified = workloads.words_sha256(out.words) == golden["out_sha256"]
+            if not verified:
+                raise SystemExit(f"bench: sharded product mismatch vs the reference hash for {args.config}")
+        out_bits = out.bit_width
+    else:
+        out_bits = 0
+    del out
+    clocks = ClockSampler(local)
+    clocks.start()
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        _barrier(world)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        fn()
+        torch.cuda.synchronize()
+        dm._sync()
+        ev1.record()
+        ev1.synchronize()
+        return ev0.elapsed_time(ev1)
+
+    for _ in range(args.warmup):
+        timed(lambda: dm.multiply(A, B, to_host=False))
+    l0 = dm.ctx.launches()
+    dev = [timed(lambda: dm.multiply(A, B, to_host=False)) for _ in range(args.steps)]
+    launches = dm.ctx.launches() - l0
+    e2e = [timed(lambda: dm.multiply(A, B, to_host=True)) for _ in range(args.steps)]
+    clock_info = clocks.stop()
+    dev_ms = _max_over_ranks(float(np.sum(dev)), world)
+    e2e_ms = _max_over_ranks(float(np.sum(e2e)), world)
+    out_bits = int(_max_over_ranks(float(out_bits), world))
+    out_gbit = rows * out_bits / 1e9
+    if rank != 0:
+        return
+    out_cw = -(-out_bits // 64)
+    line = {
+        "metric": METRIC, "value": round(args.steps * out_gbit / (dev_ms / 1e3), 3), "unit": "Gbit/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dev_ms / args.steps, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded PCG64, BASELINE.md section 4 recipe)",
+        "config": {"workload": f"{args.config}: {workloads.CONFIGS[args.config].text}",
+                   "plan": plan.describe(), "parallelism": f"sharded x{world} (row tiles / column groups, "
+                   f"NCCL all-to-all per prime, gather to rank 0)",
+                   "l2": "working set per product > L2 only for C3; not flushed between steps",
+                   "verified_vs_reference_sha256": verified},
+        "e2e": {"value": round(args.steps * out_gbit / (e2e_ms / 1e3), 3), "unit": "Gbit/s",
+                "ms_per_step": round(e2e_ms / args.steps, 4),
+                "h2d_bytes_per_step": int(world * (aw.nbytes + bw.nbytes)),
+                "d2h_bytes_per_step": int(rows * out_cw * 8),
+                "api": "shard.DistributedMultiplier.multiply on pinned host arrays (inputs to every rank)"},
+        "gpu_launches": int(launches), "clocks": clock_info,
+        "roofline": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def cpu_baseline(config, aw, ab, bw, bb, out_gbit, samples=1):
     """The oracle (C restatement of the reference kernels) on this host's cores."""
     from oracle import port
@@ -412,7 +490,10 @@ def main():
         run_reference(args, rank, world)
         return
     _init_dist(world, local)
-    run_ours(args, rank, world, local)
+    if world > 1:
+        run_sharded(args, rank, world, local)
+    else:
+        run_ours(args, rank, world, local)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -139,6 +139,36 @@ int tc_modmul_probe(uint32_t p, const uint32_t* a, const uint32_t* b, uint32_t* 
  * (natural -> bit-reversed), dir 1 = inverse DIT including the 1/n scaling. */
 int tc_ntt_probe(uint32_t p, uint32_t g, uint32_t* data, int64_t n, int32_t dir);
 
+/* ---- multi-GPU sharding ----
+ * One product over `world` ranks (a power of two), all P primes on every rank:
+ *   tc_shard_low   (A and B)  ConvertIn + x + low y stages of this rank's row
+ *                             tiles, written packed for exchange 1;
+ *   [all-to-all per prime]    rank r sends words [t*peer, (t+1)*peer) of each
+ *                             prime region to rank t (equal splits);
+ *   tc_shard_high             every y pass on this rank's column groups
+ *                             (forward A, forward B, pointwise, inverse);
+ *   [all-to-all per prime]    exchange 2, same layout, midB -> recvB;
+ *   tc_shard_final            inverse low stages + CRT + ConvertOut of this
+ *                             rank's row tiles -> rows_per_rank compact rows;
+ *   [gather to one rank]      tc_unshard permutes them into product rows.
+ * Every exchange buffer holds `primes` regions of `shard_words` words. */
+typedef struct {
+    int64_t tiles_per_rank, rows_per_rank;  /* low-phase tiles / row positions per rank */
+    int64_t shard_words;                    /* words per prime region of every buffer  */
+    int64_t peer_words;                     /* words per prime sent to each peer       */
+    int32_t primes, lgS;
+} tc_shard_info_t;
+
+int tc_shard_info(const tc_plan_t* plan, int32_t world, tc_shard_info_t* info);
+int tc_shard_low(void* ctx, const tc_plan_t* plan, int32_t rank, int32_t world, int32_t which,
+                 int32_t bits, uint32_t* send);
+int tc_shard_high(void* ctx, const tc_plan_t* plan, int32_t rank, int32_t world, uint32_t* midA,
+                  uint32_t* midB);
+int tc_shard_final(void* ctx, const tc_plan_t* plan, int32_t rank, int32_t world, const uint32_t* recvB,
+                   int64_t rows, int32_t out_cw, uint32_t* out_rows, int64_t* err_index);
+int tc_unshard(void* ctx, const tc_plan_t* plan, const uint32_t* gathered, int64_t rows, int32_t out_cw,
+               uint64_t* out);
+
 /* Device memory helpers for device-resident callers (bench, tests). */
 int tc_device_alloc(void* ctx, int64_t bytes, void** dptr);
 int tc_device_free(void* ctx, void* dptr);

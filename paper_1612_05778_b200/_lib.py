@@ -33,7 +33,7 @@ EXPORTED_SYMBOLS = (
     "tc_device_alloc", "tc_device_free", "tc_memcpy", "tc_synchronize",
     "tc_kernel_launches", "tc_set_profiling", "tc_last_profile", "tc_last_error", "tc_version",
     "tc_host_alloc", "tc_host_free", "tc_record_event", "tc_event_elapsed", "tc_flush_l2",
-    "tc_int_peak",
+    "tc_int_peak", "tc_shard_info", "tc_shard_low", "tc_shard_high", "tc_shard_final", "tc_unshard",
 )
 
 

@@ -252,7 +252,7 @@ struct Geometry {
 // Pass layout: k_final keeps P tiles of 2^(lgL+yl) words in shared memory
 // (<= 96 KiB when possible), k_low tiles are the same size, and the remaining
 // y levels go to balanced k_high passes of <= 2^14-word tiles.
-int make_geometry(const tc_plan_t* pl, Geometry& G) {
+int make_geometry(const tc_plan_t* pl, Geometry& G, int world = 1) {
     G.K = pl->K; G.L = 2 * pl->K; G.s_y = pl->s_y; G.S = G.s_y * G.L;
     G.lgL = ilog2(G.L); G.lgK = ilog2(G.K); G.lgS = ilog2(G.s_y); G.P = pl->P;
     if (G.lgL + G.lgS > 31) return set_err(TC_ERR_BAD_ARG, "grid of 2^%d slots exceeds 2^31", G.lgL + G.lgS);
@@ -263,6 +263,9 @@ int make_geometry(const tc_plan_t* pl, Geometry& G) {
     int yl = tb - G.lgL;
     if (yl < 0) yl = 0;
     if (yl > G.lgS) yl = G.lgS;
+    // sharded: at least `world` row tiles
+    const int lw = ilog2(world);
+    if (world > 1 && yl > G.lgS - lw) yl = G.lgS - lw > 0 ? G.lgS - lw : 0;
     G.yl = yl;
     const int64_t fin = (int64_t)4 * G.P * padded_words((uint32_t)(1u << (G.lgL + yl)));
     if (fin > 220 * 1024)
@@ -286,8 +289,9 @@ int make_geometry(const tc_plan_t* pl, Geometry& G) {
 }
 
 int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* words, int64_t d, int cw,
-               int check_range, uint32_t* grids) {
+               int check_range, uint32_t* grids, const ShardArgs& sh) {
     LowArgs a{};
+    a.sh = sh;
     a.src.words = words; a.src.d = d; a.src.cw = cw;
     a.src.K = G.K; a.src.lgK = G.lgK; a.src.M = (int)pl->M; a.src.N = pl->N;
     a.src.check_range = check_range; a.src.err = c->flags.as<int>();
@@ -299,7 +303,7 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     const int Rc = G.yl >= 1 ? 1 << (G.yl - 1) : 1;      // computed (even) rows, see k_low
     const uint32_t n = 1u << (G.lgL + G.yl);
     const size_t smem = (size_t)Rc * G.K * 8 + (size_t)Rc * 8 + (size_t)padded_words(n) * 4;
-    const int64_t ctas = G.S / n;
+    const int64_t ctas = sh.world > 1 ? sh.Tl : G.S / n;
     // a tile too large for two CTAs per SM gets 32 warps in one CTA
     if (smem > 112 * 1024) {
         CK(cudaFuncSetAttribute(k_low<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -313,8 +317,10 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     return TC_OK;
 }
 
-int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint32_t* other, int u0, int U) {
+int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint32_t* other, int u0, int U,
+                const ShardArgs& sh) {
     HighArgs A{};
+    A.sh = sh;
     A.g = grids; A.other = other; A.S = G.S;
     A.lgL = G.lgL; A.lgS = G.lgS; A.u0 = u0; A.U = U;
     A.cb = G.lgL + u0 < 4 ? G.lgL + u0 : 4;
@@ -325,7 +331,7 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
     const size_t smem = (size_t)padded_words(n) * 4;
     int threads = (int)(n / 16 > 512 ? 512 : n / 16);
     if (threads < 32) threads = 32;
-    dim3 grid((unsigned)(G.S / n), (unsigned)G.P);
+    dim3 grid((unsigned)(G.S / n / sh.world), (unsigned)G.P);
     if (mode == MODE_FWD) {
         if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_high<MODE_FWD><<<grid, threads, smem, c->st>>>(A);
@@ -342,8 +348,9 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
 }
 
 int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows, int M, int W32,
-                 uint32_t* out, const CrtConst& cc, bool dump) {
+                 uint32_t* out, const CrtConst& cc, bool dump, const ShardArgs& sh) {
     FinalArgs A{};
+    A.sh = sh;
     A.g = grids; A.S = G.S; A.lgL = G.lgL; A.lgS = G.lgS; A.yl = G.yl;
     A.twx = c->twx_i.as<uint2>(); A.twy = c->twy_i.as<uint2>();
     A.twy_stride = G.s_y;
@@ -352,7 +359,7 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
     A.out = out; A.err = c->flags.as<int>();
     const uint32_t n = 1u << (G.lgL + G.yl);
     const size_t smem = (size_t)G.P * padded_words(n) * 4;
-    const unsigned grid = (unsigned)(G.S / n);
+    const unsigned grid = (unsigned)(sh.world > 1 ? sh.Tl : G.S / n);
     cudaError_t e;
     if (G.P <= 4) e = launch_final_p1_4(G.P, dump, A, cc, grid, smem, c->st);
     else if (G.P <= 8) e = launch_final_p5_8(G.P, dump, A, cc, grid, smem, c->st);
@@ -365,10 +372,52 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
 
 // The whole product on the device: leaves the product words (or, with
 // dump, the exact c_ij limbs) in `out`.  Events 0..5 bracket the stages.
+ShardArgs single_gpu() {
+    ShardArgs sh{};
+    sh.world = 1; sh.rank = 0; sh.h0 = 0; sh.Tl = 0; sh.m0 = 0; sh.lchunk = 0; sh.lmloc = 0; sh.TB = 0;
+    return sh;
+}
+
+// Sharding over `world` ranks (a power of two): rank owns low-phase tiles
+// [rank*Tl, (rank+1)*Tl) and partition-mid values [rank*Mloc, (rank+1)*Mloc).
+int make_shard(const Geometry& G, int rank, int world, ShardArgs& sh) {
+    sh = single_gpu();
+    if (world <= 1) return TC_OK;
+    if (world & (world - 1)) return set_err(TC_ERR_BAD_ARG, "world=%d must be a power of two", world);
+    if (rank < 0 || rank >= world) return set_err(TC_ERR_BAD_ARG, "rank %d outside [0, %d)", rank, world);
+    const int TB = G.lgL + G.yl;
+    if (TB < 4) return set_err(TC_ERR_BAD_ARG, "grid tile of 2^%d slots too small to shard", TB);
+    const int64_t T = 1ll << (G.lgL + G.lgS - TB);
+    const int64_t Mtot = 1ll << (TB - 4);
+    if (T % world || Mtot % world)
+        return set_err(TC_ERR_BAD_ARG, "grid (%lld tiles, %lld column groups) does not split over %d ranks",
+                       (long long)T, (long long)Mtot, world);
+    sh.world = world; sh.rank = rank; sh.TB = TB;
+    sh.Tl = T / world; sh.h0 = (int64_t)rank * sh.Tl;
+    const int64_t Mloc = Mtot / world;
+    sh.m0 = (uint32_t)(rank * Mloc); sh.lmloc = ilog2(Mloc); sh.lchunk = sh.lmloc + 4;
+    return TC_OK;
+}
+
+// Per-plan device state shared by every phase: twiddles, prime constants.
+int prepare(Ctx* c, const tc_plan_t* pl, Geometry& G, bool reset_flags, int world = 1) {
+    int rc;
+    if ((rc = make_geometry(pl, G, world))) return rc;
+    if ((rc = ensure_twiddles(c, pl))) return rc;
+    std::vector<PrimeC> pcs(G.P);
+    for (int q = 0; q < G.P; ++q) pcs[q] = make_prime_const(pl->p[q], G.S);
+    if ((rc = c->pcs.ensure(sizeof(PrimeC) * G.P))) return rc;
+    CK(cudaMemcpyAsync(c->pcs.p, pcs.data(), sizeof(PrimeC) * G.P, cudaMemcpyHostToDevice, c->st));
+    if ((rc = c->flags.ensure(64))) return rc;
+    if (reset_flags) CK(cudaMemsetAsync(c->flags.p, 0x7f, 64, c->st));
+    return TC_OK;
+}
+
 int run_pipeline(Ctx* c, const tc_plan_t* pl, int a_bits, int b_bits, int64_t rows, int W32,
                  uint32_t* out, bool dump, const CrtConst& cc) {
     int rc;
     Geometry G;
+    const ShardArgs one = single_gpu();
     if ((rc = make_geometry(pl, G))) return rc;
     if ((rc = ensure_twiddles(c, pl))) return rc;
     if ((rc = c->grids.ensure((size_t)2 * G.P * G.S * 4))) return rc;
@@ -385,26 +434,26 @@ int run_pipeline(Ctx* c, const tc_plan_t* pl, int a_bits, int b_bits, int64_t ro
     int64_t l0 = c->launches;
 
     CK(cudaEventRecord(c->ev[0], c->st));
-    if ((rc = launch_low(c, G, pl, c->a_dev, c->da, c->a_cw, a_bits > pl->N, GA))) return rc;
-    if ((rc = launch_low(c, G, pl, c->b_dev, c->db, c->b_cw, b_bits > pl->N, GB))) return rc;
+    if ((rc = launch_low(c, G, pl, c->a_dev, c->da, c->a_cw, a_bits > pl->N, GA, one))) return rc;
+    if ((rc = launch_low(c, G, pl, c->b_dev, c->db, c->b_cw, b_bits > pl->N, GB, one))) return rc;
     c->stage_launches[0] = c->launches - l0; l0 = c->launches;
     CK(cudaEventRecord(c->ev[1], c->st));
     for (int i = 0; i < nh; ++i)
-        if ((rc = launch_high(c, MODE_FWD, G, GA, nullptr, G.high[i].first, G.high[i].second))) return rc;
+        if ((rc = launch_high(c, MODE_FWD, G, GA, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
     for (int i = 0; i + 1 < nh; ++i)
-        if ((rc = launch_high(c, MODE_FWD, G, GB, nullptr, G.high[i].first, G.high[i].second))) return rc;
+        if ((rc = launch_high(c, MODE_FWD, G, GB, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
     c->stage_launches[1] = c->launches - l0; l0 = c->launches;
     CK(cudaEventRecord(c->ev[2], c->st));
-    if (nh > 0) rc = launch_high(c, MODE_MID, G, GB, GA, G.high[nh - 1].first, G.high[nh - 1].second);
-    else rc = launch_high(c, MODE_MID, G, GB, GA, G.lgS, 0);
+    if (nh > 0) rc = launch_high(c, MODE_MID, G, GB, GA, G.high[nh - 1].first, G.high[nh - 1].second, one);
+    else rc = launch_high(c, MODE_MID, G, GB, GA, G.lgS, 0, one);
     if (rc) return rc;
     c->stage_launches[2] = c->launches - l0; l0 = c->launches;
     CK(cudaEventRecord(c->ev[3], c->st));
     for (int i = nh - 2; i >= 0; --i)
-        if ((rc = launch_high(c, MODE_INV, G, GB, nullptr, G.high[i].first, G.high[i].second))) return rc;
+        if ((rc = launch_high(c, MODE_INV, G, GB, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
     c->stage_launches[3] = c->launches - l0; l0 = c->launches;
     CK(cudaEventRecord(c->ev[4], c->st));
-    if ((rc = launch_final(c, G, GB, rows, (int)pl->M, W32, out, cc, dump))) return rc;
+    if ((rc = launch_final(c, G, GB, rows, (int)pl->M, W32, out, cc, dump, one))) return rc;
     c->stage_launches[4] = c->launches - l0;
     CK(cudaEventRecord(c->ev[5], c->st));
     return TC_OK;
@@ -605,6 +654,96 @@ int tc_bivariate_product(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32
     if (f[1] != 0x7f7f7f7f) { if (err_index) *err_index = f[1]; return set_err(TC_ERR_RANGE, "coefficient outside the plan's range"); }
     if (f[0] != 0x7f7f7f7f) { if (err_index) *err_index = f[0]; return set_err(TC_ERR_ENCODING, "coefficient %d exceeds the digit capacity", f[0]); }
     if (f[2] != 0x7f7f7f7f) { if (err_index) *err_index = f[2]; return set_err(TC_ERR_BOUND, "coefficient bound exceeded at flat index %d", f[2]); }
+    return TC_OK;
+}
+
+int tc_shard_info(const tc_plan_t* plan, int32_t world, tc_shard_info_t* info) {
+    if (!plan || !info) return set_err(TC_ERR_BAD_ARG, "NULL argument");
+    Geometry G;
+    int rc;
+    if ((rc = make_geometry(plan, G, world))) return rc;
+    ShardArgs sh;
+    if ((rc = make_shard(G, 0, world, sh))) return rc;
+    const int64_t R = 1ll << G.yl;
+    const int64_t T = 1ll << (G.lgL + G.lgS - (G.lgL + G.yl));
+    info->tiles_per_rank = world > 1 ? sh.Tl : T;
+    info->rows_per_rank = info->tiles_per_rank * R;
+    info->shard_words = info->tiles_per_rank << (G.lgL + G.yl);
+    info->peer_words = world > 1 ? info->shard_words / world : info->shard_words;
+    info->primes = G.P;
+    info->lgS = G.lgS;
+    return TC_OK;
+}
+
+int tc_shard_low(void* ctx, const tc_plan_t* plan, int32_t rank, int32_t world, int32_t which, int32_t bits,
+                 uint32_t* send) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || !c->staged || !send) return set_err(TC_ERR_BAD_ARG, "no staged inputs / send buffer");
+    CK(cudaSetDevice(c->device));
+    int rc;
+    if ((rc = validate_plan(plan, c->da, c->db))) return rc;
+    Geometry G;
+    if ((rc = prepare(c, plan, G, which == 0, world))) return rc;
+    ShardArgs sh;
+    if ((rc = make_shard(G, rank, world, sh))) return rc;
+    return launch_low(c, G, plan, which ? c->b_dev : c->a_dev, which ? c->db : c->da,
+                      which ? c->b_cw : c->a_cw, bits > plan->N, send, sh);
+}
+
+int tc_shard_high(void* ctx, const tc_plan_t* plan, int32_t rank, int32_t world, uint32_t* midA, uint32_t* midB) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || !midA || !midB) return set_err(TC_ERR_BAD_ARG, "NULL argument");
+    CK(cudaSetDevice(c->device));
+    int rc;
+    Geometry G;
+    if ((rc = prepare(c, plan, G, false, world))) return rc;
+    ShardArgs sh;
+    if ((rc = make_shard(G, rank, world, sh))) return rc;
+    const int nh = (int)G.high.size();
+    for (int i = 0; i < nh; ++i)
+        if ((rc = launch_high(c, MODE_FWD, G, midA, nullptr, G.high[i].first, G.high[i].second, sh))) return rc;
+    for (int i = 0; i + 1 < nh; ++i)
+        if ((rc = launch_high(c, MODE_FWD, G, midB, nullptr, G.high[i].first, G.high[i].second, sh))) return rc;
+    if (nh > 0) rc = launch_high(c, MODE_MID, G, midB, midA, G.high[nh - 1].first, G.high[nh - 1].second, sh);
+    else rc = launch_high(c, MODE_MID, G, midB, midA, G.lgS, 0, sh);
+    if (rc) return rc;
+    for (int i = nh - 2; i >= 0; --i)
+        if ((rc = launch_high(c, MODE_INV, G, midB, nullptr, G.high[i].first, G.high[i].second, sh))) return rc;
+    return TC_OK;
+}
+
+int tc_shard_final(void* ctx, const tc_plan_t* plan, int32_t rank, int32_t world, const uint32_t* recvB,
+                   int64_t rows, int32_t out_cw, uint32_t* out_rows, int64_t* err_index) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || !recvB || !out_rows) return set_err(TC_ERR_BAD_ARG, "NULL argument");
+    if (err_index) *err_index = -1;
+    CK(cudaSetDevice(c->device));
+    int rc;
+    Geometry G;
+    if ((rc = prepare(c, plan, G, false, world))) return rc;
+    ShardArgs sh;
+    if ((rc = make_shard(G, rank, world, sh))) return rc;
+    CrtConst cc;
+    const int64_t dmin = c->staged ? (c->da < c->db ? c->da : c->db) : plan->d;
+    if ((rc = make_crt_const(plan, dmin, &cc))) return rc;
+    if ((rc = launch_final(c, G, recvB, rows, (int)plan->M, 2 * out_cw, out_rows, cc, false, sh))) return rc;
+    int f[4];
+    if ((rc = read_flags(c, f))) return rc;
+    if (f[1] != 0x7f7f7f7f) { if (err_index) *err_index = f[1]; return set_err(TC_ERR_RANGE, "coefficient outside the plan's range"); }
+    if (f[0] != 0x7f7f7f7f) { if (err_index) *err_index = f[0]; return set_err(TC_ERR_ENCODING, "coefficient %d exceeds the digit capacity", f[0]); }
+    if (f[2] != 0x7f7f7f7f) { if (err_index) *err_index = f[2]; return set_err(TC_ERR_BOUND, "coefficient bound exceeded at flat index %d", f[2]); }
+    return TC_OK;
+}
+
+int tc_unshard(void* ctx, const tc_plan_t* plan, const uint32_t* gathered, int64_t rows, int32_t out_cw, uint64_t* out) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || !gathered || !out) return set_err(TC_ERR_BAD_ARG, "NULL argument");
+    CK(cudaSetDevice(c->device));
+    const int lgS = ilog2(plan->s_y);
+    k_unshard<<<(unsigned)plan->s_y, 128, 0, c->st>>>(gathered, reinterpret_cast<uint32_t*>(out), lgS, rows,
+                                                      2 * out_cw, plan->s_y);
+    c->launches++;
+    CKL();
     return TC_OK;
 }
 

@@ -407,7 +407,31 @@ struct TwHigh {
 // one operand, all primes.  CTA = 2^yl row positions x L columns.  The first
 // x-stage on a zero-padded row is (x_j, x_j * theta^j): the negacyclic twist.
 // ---------------------------------------------------------------------------
+// Multi-GPU sharding (world > 1): rank r owns low-phase tiles [h0, h0+Tl)
+// (k_low / k_final, whole rows) and, for every k_high pass, the partition
+// "mid" values [m0, m0+Mloc) of flat bits [cb, TB).  Exchange buffers are
+// per prime [peer][tile-local][chunk] with chunk = Mloc << cb words, so each
+// exchange is one equal-split all-to-all per prime (see shard.py).
+// world == 1: full grids, contiguous tiles (the single-GPU path).
+struct ShardArgs {
+    int world, rank;
+    int64_t h0, Tl;        // first low-phase tile, tiles per rank
+    uint32_t m0;           // first partition-mid value
+    int lchunk, lmloc;     // log2(chunk words), log2(Mloc)
+    int TB;                // low-phase tile bits (lgL + yl)
+};
+
+// exchange layout index of tile-local slot l of local tile hl
+__device__ __forceinline__ uint32_t xchg_index(const ShardArgs& sh, uint32_t hl, uint32_t l) {
+    return ((((l >> sh.lchunk) * (uint32_t)sh.Tl) + hl) << sh.lchunk) | (l & ((1u << sh.lchunk) - 1));
+}
+struct XchgIdx {
+    ShardArgs sh; uint32_t hl;
+    __device__ __forceinline__ uint32_t operator()(uint32_t e) const { return xchg_index(sh, hl, e); }
+};
+
 struct LowArgs {
+    ShardArgs sh;
     DigitSrc src;
     int lgL, lgS, yl;
     uint32_t* g; int64_t S;
@@ -433,7 +457,13 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_low(LowArgs A) {
     uint32_t* tile = reinterpret_cast<uint32_t*>(coeff + Rc);
     __shared__ DigitScratch ds;
     __shared__ int s_nvalid;
-    const uint32_t pos0 = blockIdx.x * (uint32_t)R;
+    const uint32_t gtile = blockIdx.x + (uint32_t)A.sh.h0;     // global low-phase tile
+    const uint32_t pos0 = gtile * (uint32_t)R;
+    const bool sharded = A.sh.world > 1;
+    // per-prime destination: the full grid, or the packed exchange buffer
+    auto dst = [&](int q) -> uint32_t* {
+        return sharded ? A.g + (int64_t)q * (A.sh.Tl << A.sh.TB) : A.g + (int64_t)q * A.S + (int64_t)blockIdx.x * n;
+    };
     if (threadIdx.x == 0) s_nvalid = 0;
     __syncthreads();
     for (int r = threadIdx.x; r < Rc; r += blockDim.x) {
@@ -444,8 +474,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_low(LowArgs A) {
     __syncthreads();
     if (s_nvalid == 0) {       // all rows of this tile are zero padding
         for (int q = 0; q < A.P; ++q) {
-            uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)blockIdx.x * n;
-            for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) g[e] = 0u;
+            uint32_t* g = dst(q);
+            for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) g[sharded ? xchg_index(A.sh, blockIdx.x, e) : e] = 0u;
         }
         return;
     }
@@ -483,8 +513,9 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_low(LowArgs A) {
             }
         }
         run_bits<false>(tile, tile_bits, A.lgL + (prune ? 1 : 0), tile_bits, tw, pc.p, pc.two_p);  // y: DIT
-        uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)blockIdx.x * n;
-        if (n >= 4) tile_store(g, tile, n, Contig{});
+        uint32_t* g = dst(q);
+        if (sharded) tile_store(g, tile, n, XchgIdx{A.sh, blockIdx.x});
+        else if (n >= 4) tile_store(g, tile, n, Contig{});
         else tile_store_scalar(g, tile, n, Contig{});
         __syncthreads();
     }
@@ -501,6 +532,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_low(LowArgs A) {
 enum { MODE_FWD = 0, MODE_INV = 1, MODE_MID = 2 };
 
 struct HighArgs {
+    ShardArgs sh;
     uint32_t* g; const uint32_t* other; int64_t S;
     int lgL, lgS, u0, U, cb;
     const uint2* twf; const uint2* twi; int64_t tw_stride;
@@ -511,18 +543,31 @@ template <int MODE>
 __global__ void __launch_bounds__(512, 2) k_high(HighArgs A) {
     extern __shared__ __align__(16) uint32_t s[];
     const int q = blockIdx.y;
-    uint32_t* g = A.g + (int64_t)q * A.S;
+    const bool sharded = A.sh.world > 1;
+    const int64_t qstride = sharded ? (A.sh.Tl << A.sh.TB) : A.S;
+    uint32_t* g = A.g + (int64_t)q * qstride;
     const PrimeC pc = A.pcs[q];
     const int b0 = A.lgL + A.u0;
     const int nmid = b0 - A.cb;
     const uint32_t cta = blockIdx.x;
-    const uint32_t mid = cta & ((1u << nmid) - 1);
-    const uint32_t hi = cta >> nmid;
+    uint32_t mid, hi, pml = 0;
+    if (!sharded) {
+        mid = cta & ((1u << nmid) - 1);
+        hi = cta >> nmid;
+    } else {   // this rank's partition-mid values only
+        pml = cta & ((1u << A.sh.lmloc) - 1);
+        const uint32_t y = cta >> A.sh.lmloc;
+        const int rb = b0 - A.sh.TB;                       // row bits between TB and b0
+        mid = ((y & ((1u << rb) - 1)) << (A.sh.TB - A.cb)) | (A.sh.m0 + pml);
+        hi = y >> rb;
+    }
     const uint32_t base = (hi << (b0 + A.U)) | (mid << A.cb);
     const int tile_bits = A.U + A.cb;
     const uint32_t n = 1u << tile_bits;
     const uint32_t cmask = (1u << A.cb) - 1;
-    const HighIdx hidx{base, A.cb, b0, cmask};
+    const HighIdx hidx = sharded
+        ? HighIdx{((base >> A.sh.TB) << A.sh.lchunk) | (pml << A.cb), A.cb, b0 - A.sh.TB + A.sh.lchunk, cmask}
+        : HighIdx{base, A.cb, b0, cmask};
     if (A.cb >= 2) tile_load(s, g, n, hidx);
     else tile_load_scalar(s, g, n, hidx);
     __syncthreads();
@@ -530,7 +575,7 @@ __global__ void __launch_bounds__(512, 2) k_high(HighArgs A) {
     if (MODE == MODE_FWD || MODE == MODE_MID)
         run_bits<false>(s, tile_bits, A.cb, tile_bits, tf, pc.p, pc.two_p);
     if (MODE == MODE_MID) {
-        const uint32_t* ga = A.other + (int64_t)q * A.S;
+        const uint32_t* ga = A.other + (int64_t)q * qstride;
         auto pw = [&](uint32_t e, uint32_t y) {
             const uint32_t x = reduce_2p(s[padi(e)], pc.two_p);
             s[padi(e)] = shoup_mul(mont_mul(x, reduce_2p(y, pc.two_p), pc.p, pc.pinv_neg),
@@ -658,6 +703,7 @@ __device__ __forceinline__ int div_m(int x, int M, uint32_t minv) {
 // the zero padding and are skipped.  DUMP writes the exact c_ij instead.
 // ---------------------------------------------------------------------------
 struct FinalArgs {
+    ShardArgs sh;
     const uint32_t* g; int64_t S;
     int lgL, lgS, yl;
     const uint2* twx; const uint2* twy; int64_t twy_stride;   // inverse tables
@@ -680,7 +726,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_final(FinalArgs A, c
     const int tile_bits = A.lgL + A.yl;
     const uint32_t n = 1u << tile_bits;
     const uint32_t stride = padded_words(n);
-    const uint32_t pos0 = blockIdx.x * (uint32_t)R;
+    const bool sharded = A.sh.world > 1;
+    const uint32_t pos0 = (blockIdx.x + (uint32_t)A.sh.h0) * (uint32_t)R;
     if (threadIdx.x == 0) s_any = 0;
     __syncthreads();
     for (int r = threadIdx.x; r < R; r += blockDim.x)
@@ -691,9 +738,13 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_final(FinalArgs A, c
     for (int q = 0; q < P; ++q) {
         const PrimeC pc = A.pcs[q];
         uint32_t* t = sm + q * stride;
-        const uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)blockIdx.x * n;
-        if (n >= 4) tile_load(t, g, n, Contig{});
-        else tile_load_scalar(t, g, n, Contig{});
+        if (sharded) {
+            tile_load(t, A.g + (int64_t)q * (A.sh.Tl << A.sh.TB), n, XchgIdx{A.sh, blockIdx.x});
+        } else {
+            const uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)blockIdx.x * n;
+            if (n >= 4) tile_load(t, g, n, Contig{});
+            else tile_load_scalar(t, g, n, Contig{});
+        }
         __syncthreads();
         const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
         run_bits<true>(t, tile_bits, A.lgL, tile_bits, tw, pc.p, pc.two_p);   // y low: DIF
@@ -871,13 +922,25 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_final(FinalArgs A, c
             const uint32_t x = w1v[cv][k];
             if (valid[k]) {
                 const uint32_t prow = bitrev(pos0 + rw[k], A.lgS);
-                if (prow < A.rows_out) A.out[(int64_t)prow * W32 + ww[k]] = x - bm[k] - bin;
+                if (sharded)   // compact rows in position order; unshard() permutes
+                    A.out[((int64_t)blockIdx.x * R + rw[k]) * W32 + ww[k]] = x - bm[k] - bin;
+                else if (prow < A.rows_out) A.out[(int64_t)prow * W32 + ww[k]] = x - bm[k] - bin;
             }
             const uint32_t g2 = live[k] && x < bm[k];
             const uint32_t p2 = live[k] && x == bm[k];
             bin = g2 | (p2 & bin);
         }
     }
+}
+
+// Gathered compact rows (position order, world x rows-per-rank) -> product
+// rows in natural order: out[bitrev(pos)] = in[pos] for bitrev(pos) < rows.
+static __global__ void k_unshard(const uint32_t* in, uint32_t* out, int lgS, int64_t rows, int W32, int64_t npos) {
+    const int64_t pos = blockIdx.x;
+    if (pos >= npos) return;
+    const uint32_t prow = bitrev((uint32_t)pos, lgS);
+    if (prow >= rows) return;
+    for (int w = threadIdx.x; w < W32; w += blockDim.x) out[(int64_t)prow * W32 + w] = in[pos * W32 + w];
 }
 
 // ---------------------------------------------------------------------------

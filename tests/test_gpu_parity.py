@@ -264,3 +264,28 @@ def test_full_config_matches_reference_hash(name, oracle):
     # size-independent property: c(r) == a(r) b(r) mod q
     q, r = (1 << 61) - 1, 0x1234567890ABCDE
     assert oracle.eval_mod(out.words, q, r) == oracle.eval_mod(aw, q, r) * oracle.eval_mod(bw, q, r) % q
+
+
+# ---------------------------------------------------------------- sharded (multi-GPU) path
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_product_virtual_ranks(world, oracle):
+    # the multi-GPU decomposition (row tiles <-> column groups, two all-to-all
+    # exchanges) run as `world` virtual ranks on one GPU
+    from paper_1612_05778_b200 import shard
+    rng = random.Random(world)
+    for d, nbits in ((300, 500), (1000, 2000), (64, 4097)):
+        a = _random_poly(rng, d, nbits)
+        b = _random_poly(rng, d - 7, nbits)
+        out, plan = shard.multiply_local(a, b, world)
+        assert out == tc.multiply(tc.MulRequest(a, b)), plan.describe()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C5"])
+def test_sharded_full_config(name):
+    from paper_1612_05778_b200 import shard
+    cfg = json.load(open(os.path.join(GOLDEN, "configs.json")))[name]
+    (aw, ab), (bw, bb) = workloads.make_inputs(name)
+    a, b = tc.IntPolynomial._trusted(aw, ab), tc.IntPolynomial._trusted(bw, bb)
+    out, _ = shard.multiply_local(a, b, 4)
+    assert workloads.words_sha256(out.words) == cfg["out_sha256"]

@@ -1,0 +1,60 @@
+"""CPU, world_size 2 (gloo): the exchange plumbing of the sharded product.
+
+The sharded kernels themselves are tested on one GPU as virtual ranks
+(tests/test_gpu_parity.py::test_sharded_*); here the multi-process exchange
+(torch.distributed all_to_all_single per prime, shard.torch_all_to_all) is
+checked against the layout contract of shard.exchange_slices that the kernels
+and LocalExchange rely on.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+class _Info:
+    def __init__(self, primes, shard_words, world):
+        self.primes, self.shard_words, self.peer_words = primes, shard_words, shard_words // world
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _tags(rank, primes, shard_words):
+    return [[(rank << 24) | (q << 20) | i for i in range(shard_words)] for q in range(primes)]
+
+
+def _worker(rank, world, port, primes, shard_words, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1612_05778_b200.shard import torch_all_to_all
+    send = torch.tensor(_tags(rank, primes, shard_words), dtype=torch.int32)
+    recv = torch.empty_like(send)
+    torch_all_to_all(send, recv, world)
+    out[rank] = recv.numpy().copy()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,primes,shard_words", [(2, 3, 64), (2, 1, 16)])
+def test_torch_exchange_matches_layout_contract(world, primes, shard_words):
+    from paper_1612_05778_b200.shard import exchange_slices
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), primes, shard_words, out), nprocs=world, join=True)
+    info = _Info(primes, shard_words, world)
+    sends = [np.array(_tags(r, primes, shard_words), dtype=np.int32).reshape(-1) for r in range(world)]
+    exp = [np.zeros(primes * shard_words, dtype=np.int32) for _ in range(world)]
+    for s, t, q, so, do, w in exchange_slices(world, info):
+        exp[t][do:do + w] = sends[s][so:so + w]
+    for r in range(world):
+        assert np.array_equal(out[r].reshape(-1), exp[r])
