@@ -225,20 +225,33 @@ class DistributedMultiplier:
     def _sync(self):
         self.lib.tc_synchronize(self.ctx.handle)
 
-    def stage(self, aw: np.ndarray, bw: np.ndarray):
+    def stage(self, aw: np.ndarray, bw: np.ndarray, resident: bool = False):
+        """H2D of both operands (or, resident, the copies made by upload())."""
         info = _lib.TcInputInfo()
-        _lib.check(self.lib.tc_stage_inputs(self.ctx.handle, _lib.ptr(aw), aw.shape[0], aw.shape[1],
-                                            _lib.ptr(bw), bw.shape[0], bw.shape[1], 0, ctypes.byref(info)),
+        if resident:
+            pa, pb, on_dev = self._dev_a.data_ptr(), self._dev_b.data_ptr(), 1
+        else:
+            pa, pb, on_dev = _lib.ptr(aw), _lib.ptr(bw), 0
+        _lib.check(self.lib.tc_stage_inputs(self.ctx.handle, pa, aw.shape[0], aw.shape[1],
+                                            pb, bw.shape[0], bw.shape[1], on_dev, ctypes.byref(info)),
                    "stage")
         return info
 
-    def multiply(self, a: IntPolynomial, b: IntPolynomial, K=None, M=None, to_host: bool = True):
+    def upload(self, a: IntPolynomial, b: IntPolynomial):
+        """Keep device copies of the operands (device-resident timing)."""
+        t = self.torch
+        self._dev_a = t.from_numpy(np.ascontiguousarray(a.words).view(np.int64)).to(self.device)
+        self._dev_b = t.from_numpy(np.ascontiguousarray(b.words).view(np.int64)).to(self.device)
+        t.cuda.synchronize(self.device)
+
+    def multiply(self, a: IntPolynomial, b: IntPolynomial, K=None, M=None, to_host: bool = True,
+                 resident: bool = False):
         t, world, rank = self.torch, self.world, self.rank
         aw = np.ascontiguousarray(a.words)
         bw = np.ascontiguousarray(b.words)
         da, db = aw.shape[0], bw.shape[0]
         rows = da + db - 1
-        inf = self.stage(aw, bw)
+        inf = self.stage(aw, bw, resident)
         if not (inf.nonzero_a and inf.nonzero_b):
             raise EmptyInputError("empty input: zero polynomial")
         n_in = max(inf.n_in_a, inf.n_in_b)
