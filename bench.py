@@ -320,6 +320,7 @@ def run_sharded(args, rank, world, local):
     import torch
     import paper_1612_05778_b200 as tc
     from paper_1612_05778_b200 import _lib, shard, workloads
+    local = local if torch.cuda.device_count() > local else 0   # (single-GPU smoke of this path)
     torch.cuda.set_device(local)
     (aw, ab), (bw, bb) = workloads.make_inputs(args.config)
     pa = _lib.pinned.empty(aw.shape, np.uint64)
@@ -455,8 +456,9 @@ def _init_dist(world, local):
     if world > 1 and not _dist_ready:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local if torch.cuda.device_count() > local else 0)
+        # TC_DIST_BACKEND=gloo only to exercise the N > 1 code path on a single GPU
+        dist.init_process_group(os.environ.get("TC_DIST_BACKEND", "nccl"))
         _dist_ready = True
 
 
@@ -471,7 +473,8 @@ def _max_over_ranks(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

@@ -186,13 +186,36 @@ def multiply_local(a: IntPolynomial, b: IntPolynomial, world: int, K: int | None
 # One process per GPU (torchrun): exchanges through torch.distributed
 # ---------------------------------------------------------------------------
 
+def _host_staged() -> bool:
+    """gloo moves host tensors only: device buffers are staged through the host
+    (lets the multi-process path run on one GPU with no cross-process waits)."""
+    import torch.distributed as dist
+    return dist.get_backend() == "gloo"
+
+
 def torch_all_to_all(send, recv, world: int):
     """Exchange k of the sharded product: `send`/`recv` are (P, shard_words)
     int32 tensors; prime region q is split into `world` equal peer blocks.
     One all_to_all_single per prime (NCCL over NVLink for an "nccl" group)."""
     import torch.distributed as dist
+    staged = send.is_cuda and _host_staged()
+    s_, r_ = (send.cpu(), recv.cpu()) if staged else (send, recv)
     for q in range(send.shape[0]):
-        dist.all_to_all_single(recv[q], send[q])
+        dist.all_to_all_single(r_[q], s_[q])
+    if staged:
+        recv.copy_(r_)
+
+
+def torch_gather(t, out_list, dst: int = 0):
+    import torch.distributed as dist
+    if t.is_cuda and _host_staged():
+        lst = [x.cpu() for x in out_list] if out_list is not None else None
+        dist.gather(t.cpu(), lst, dst=dst)
+        if out_list is not None:
+            for x, y in zip(out_list, lst):
+                x.copy_(y)
+    else:
+        dist.gather(t, out_list, dst=dst)
 
 
 class DistributedMultiplier:
@@ -279,7 +302,7 @@ class DistributedMultiplier:
                                 self.rows_t.data_ptr(), ctypes.byref(err))
         if rc:
             _raise(rc, err.value, plan)
-        self.dist.gather(self.rows_t, self.gathered, dst=0)
+        torch_gather(self.rows_t, self.gathered, dst=0)
         if rank != 0:
             return None, plan
         t.cuda.synchronize(self.device)

@@ -289,3 +289,39 @@ def test_sharded_full_config(name):
     a, b = tc.IntPolynomial._trusted(aw, ab), tc.IntPolynomial._trusted(bw, bb)
     out, _ = shard.multiply_local(a, b, 4)
     assert workloads.words_sha256(out.words) == cfg["out_sha256"]
+
+
+def _dist_worker(rank, world, port, name, result):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1612_05778_b200 import shard
+    (aw, ab), (bw, bb) = workloads.make_inputs(name)
+    a, b = tc.IntPolynomial._trusted(aw, ab), tc.IntPolynomial._trusted(bw, bb)
+    dm = shard.DistributedMultiplier(0)
+    out, plan = dm.multiply(a, b)
+    dm.upload(a, b)
+    out2, _ = dm.multiply(a, b, resident=True)
+    if rank == 0:
+        result["sha"] = workloads.words_sha256(out.words)
+        result["sha2"] = workloads.words_sha256(out2.words)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_distributed_multiplier_two_processes(name):
+    # the real multi-process code path (DistributedMultiplier, torch.distributed
+    # exchanges) with 2 ranks sharing this one GPU; gloo stages the exchanges
+    # through host memory, so no kernel waits on another process
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    result = mp.Manager().dict()
+    mp.spawn(_dist_worker, args=(2, port, name, result), nprocs=2, join=True)
+    cfg = json.load(open(os.path.join(GOLDEN, "configs.json")))[name]
+    assert result["sha"] == cfg["out_sha256"] and result["sha2"] == cfg["out_sha256"]
