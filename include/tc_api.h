@@ -111,6 +111,19 @@ int tc_multiply(void* ctx,
                 uint64_t* out, int64_t rows, int32_t out_cw,
                 tc_times_t* times, int64_t* err_index);
 
+/* The end-to-end product from host buffers with transfers overlapped: B's
+ * upload runs beside operand A's first pass, and the last pass runs in chunks
+ * whose product rows are copied to the host while later chunks compute.  The
+ * plan may be made from the declared bit widths (any plan whose capacity
+ * covers the operands is exact); the real widths are reduced on the device
+ * and returned in *info with the product's out_bits / out_cw.  `out` is a
+ * pinned host buffer of out_capacity_words words, receiving rows x out_cw. */
+typedef struct { int32_t n_in, out_bits, out_cw, nonzero; } tc_product_info_t;
+int tc_multiply_host(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int32_t a_bits,
+                     const uint64_t* b, int64_t db, int32_t b_cw, int32_t b_bits,
+                     const tc_plan_t* plan, uint64_t* out, int64_t out_capacity_words,
+                     tc_product_info_t* info, tc_times_t* times, int64_t* err_index);
+
 /* ---- parity seams (device code shared with the fused product path) ---- */
 
 /* Balanced digits of the staged operand `which` (0 = a, 1 = b) under (K, M, N)

@@ -28,7 +28,7 @@ TC_ERR_RANGE = 7
 TC_ERR_EMPTY = 8
 
 EXPORTED_SYMBOLS = (
-    "tc_ctx_create", "tc_ctx_destroy", "tc_stage_inputs", "tc_execute", "tc_multiply",
+    "tc_ctx_create", "tc_ctx_destroy", "tc_stage_inputs", "tc_execute", "tc_multiply", "tc_multiply_host",
     "tc_digits", "tc_bivariate_product", "tc_modmul_probe", "tc_ntt_probe",
     "tc_device_alloc", "tc_device_free", "tc_memcpy", "tc_synchronize",
     "tc_kernel_launches", "tc_set_profiling", "tc_last_profile", "tc_last_error", "tc_version",
@@ -49,6 +49,11 @@ class TcTimes(ctypes.Structure):
                 ("pointwise", ctypes.c_double), ("ntt_inverse", ctypes.c_double),
                 ("crt", ctypes.c_double), ("recover", ctypes.c_double),
                 ("total", ctypes.c_double), ("gpus", ctypes.c_int32)]
+
+
+class TcProductInfo(ctypes.Structure):
+    _fields_ = [("n_in", ctypes.c_int32), ("out_bits", ctypes.c_int32), ("out_cw", ctypes.c_int32),
+                ("nonzero", ctypes.c_int32)]
 
 
 class TcInputInfo(ctypes.Structure):
@@ -78,6 +83,8 @@ def load(path: str = LIB_PATH):
             "tc_execute": (i32, [vp, P(TcPlan), i32, i32, vp, i64, i32, i32, P(TcTimes), P(i64)]),
             "tc_multiply": (i32, [vp, vp, i64, i32, i32, vp, i64, i32, i32, P(TcPlan), vp, i64, i32,
                                   P(TcTimes), P(i64)]),
+            "tc_multiply_host": (i32, [vp, vp, i64, i32, i32, vp, i64, i32, i32, P(TcPlan), vp, i64,
+                                       P(TcProductInfo), P(TcTimes), P(i64)]),
             "tc_digits": (i32, [vp, i32, i64, i64, i64, i32, vp, P(i64)]),
             "tc_bivariate_product": (i32, [vp, P(TcPlan), i32, i32, vp, i64, P(i64)]),
             "tc_modmul_probe": (i32, [u32, vp, vp, vp, i64, i32]),

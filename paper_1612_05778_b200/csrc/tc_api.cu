@@ -93,6 +93,9 @@ struct Ctx {
     int profiling = 0;
     cudaEvent_t user_ev[16] = {};
     DevBuf flush;
+    cudaStream_t aux = nullptr;          // H2D of operand B and the chunked D2H of the product
+    cudaEvent_t xev[16] = {};            // cross-stream events of tc_multiply_host
+    int* hinfo = nullptr;                // pinned: widths read back early
 };
 
 int ilog2(int64_t x) { int l = 0; while ((1ll << l) < x) ++l; return l; }
@@ -348,9 +351,11 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
 }
 
 int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows, int M, int W32,
-                 uint32_t* out, const CrtConst& cc, bool dump, const ShardArgs& sh) {
+                 uint32_t* out, const CrtConst& cc, bool dump, const ShardArgs& sh,
+                 int64_t x0 = 0, int64_t nx = -1) {
     FinalArgs A{};
     A.sh = sh;
+    A.x0 = (uint32_t)x0; A.lgT = G.lgL + G.lgS - (G.lgL + G.yl);
     A.g = grids; A.S = G.S; A.lgL = G.lgL; A.lgS = G.lgS; A.yl = G.yl;
     A.twx = c->twx_i.as<uint2>(); A.twy = c->twy_i.as<uint2>();
     A.twy_stride = G.s_y;
@@ -359,7 +364,7 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
     A.out = out; A.err = c->flags.as<int>();
     const uint32_t n = 1u << (G.lgL + G.yl);
     const size_t smem = (size_t)G.P * padded_words(n) * 4;
-    const unsigned grid = (unsigned)(sh.world > 1 ? sh.Tl : G.S / n);
+    const unsigned grid = (unsigned)(sh.world > 1 ? sh.Tl : (nx >= 0 ? nx : G.S / n));
     cudaError_t e;
     if (G.P <= 4) e = launch_final_p1_4(G.P, dump, A, cc, grid, smem, c->st);
     else if (G.P <= 8) e = launch_final_p5_8(G.P, dump, A, cc, grid, smem, c->st);
@@ -489,6 +494,9 @@ int tc_ctx_create(int device, void** out) {
     cudaError_t e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
     if (e != cudaSuccess) { delete c; return set_err(TC_ERR_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e)); }
     for (auto& ev : c->ev) cudaEventCreate(&ev);
+    for (auto& ev : c->xev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking);
+    cudaHostAlloc((void**)&c->hinfo, 64, cudaHostAllocDefault);
     *out = c;
     return TC_OK;
 }
@@ -502,6 +510,9 @@ int tc_ctx_destroy(void* ctx) {
                       &c->pcs, &c->flags, &c->outbuf, &c->dbg}) b->release();
     for (auto& ev : c->ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : c->user_ev) if (ev) cudaEventDestroy(ev);
+    for (auto& ev : c->xev) if (ev) cudaEventDestroy(ev);
+    if (c->aux) { cudaStreamSynchronize(c->aux); cudaStreamDestroy(c->aux); }
+    if (c->hinfo) cudaFreeHost(c->hinfo);
     c->flush.release();
     cudaStreamDestroy(c->st);
     delete c;
@@ -598,6 +609,134 @@ int tc_multiply(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int32_t 
     rc = tc_execute(ctx, plan, a_bits, b_bits, out, rows, out_cw, 0, times, err_index);
     if (times && rc == TC_OK) { times->convert += t1 - t0; times->total = now_s() - t0; }
     return rc;
+}
+
+int tc_multiply_host(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int32_t a_bits,
+                     const uint64_t* b, int64_t db, int32_t b_cw, int32_t b_bits,
+                     const tc_plan_t* plan, uint64_t* out, int64_t out_capacity_words,
+                     tc_product_info_t* pinfo, tc_times_t* times, int64_t* err_index) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    const double t_begin = now_s();
+    if (!c || !a || !b || !out || da < 1 || db < 1 || a_cw < 1 || b_cw < 1)
+        return set_err(TC_ERR_BAD_ARG, "bad operand arguments");
+    if (err_index) *err_index = -1;
+    CK(cudaSetDevice(c->device));
+    int rc;
+    if ((rc = validate_plan(plan, da, db))) return rc;
+    const int64_t rows = da + db - 1;
+    CrtConst cc;
+    if ((rc = make_crt_const(plan, da < db ? da : db, &cc))) return rc;
+    if ((rc = c->in_a.ensure((size_t)da * a_cw * 8))) return rc;
+    if ((rc = c->in_b.ensure((size_t)db * b_cw * 8))) return rc;
+    if ((rc = c->dbg.ensure(64))) return rc;
+    c->a_dev = c->in_a.as<uint64_t>(); c->b_dev = c->in_b.as<uint64_t>();
+    c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true;
+    Geometry G;
+    if ((rc = prepare(c, plan, G, true))) return rc;
+    if ((rc = c->grids.ensure((size_t)2 * G.P * G.S * 4))) return rc;
+    uint32_t* GA = c->grids.as<uint32_t>();
+    uint32_t* GB = GA + (size_t)G.P * G.S;
+    const ShardArgs one = single_gpu();
+    int* wf = c->dbg.as<int>();
+    // main: A in, its width, its first pass (planned from the declared widths)
+    CK(cudaEventRecord(c->ev[0], c->st));
+    CK(cudaMemsetAsync(wf, 0, 16, c->st));
+    CK(cudaMemcpyAsync(c->in_a.p, a, (size_t)da * a_cw * 8, cudaMemcpyHostToDevice, c->st));
+    k_width<<<(unsigned)((da + 255) / 256), 256, 0, c->st>>>(c->a_dev, da, a_cw, wf);
+    c->launches++;
+    CKL();
+    CK(cudaEventRecord(c->xev[0], c->st));
+    if ((rc = launch_low(c, G, plan, c->a_dev, da, a_cw, a_bits > plan->N, GA, one))) return rc;
+    // aux, concurrently: B in, its width, both widths back to the host
+    CK(cudaMemcpyAsync(c->in_b.p, b, (size_t)db * b_cw * 8, cudaMemcpyHostToDevice, c->aux));
+    CK(cudaStreamWaitEvent(c->aux, c->xev[0], 0));
+    k_width<<<(unsigned)((db + 255) / 256), 256, 0, c->aux>>>(c->b_dev, db, b_cw, wf + 2);
+    c->launches++;
+    CKL();
+    CK(cudaMemcpyAsync(c->hinfo, wf, 16, cudaMemcpyDeviceToHost, c->aux));
+    CK(cudaEventRecord(c->xev[1], c->aux));
+    CK(cudaEventSynchronize(c->xev[1]));
+    const int n_in = c->hinfo[0] > c->hinfo[2] ? c->hinfo[0] : c->hinfo[2];
+    const int64_t d = da > db ? da : db;
+    int bl = 0; while ((1ll << bl) <= d) ++bl;                       // bit length of d
+    const int out_bits = bl + (2 * n_in - 2 > 0 ? 2 * n_in - 2 : 0) + 1;   // tc/zpoly.py:103-114
+    const int out_cw = (out_bits + 63) / 64;
+    if (pinfo) { pinfo->n_in = n_in; pinfo->out_bits = out_bits; pinfo->out_cw = out_cw;
+                 pinfo->nonzero = (c->hinfo[1] && c->hinfo[3]) ? 1 : 0; }
+    if (!(c->hinfo[1] && c->hinfo[3])) {
+        CK(cudaStreamSynchronize(c->st));
+        return set_err(TC_ERR_EMPTY, "empty input: zero polynomial");
+    }
+    if ((int64_t)rows * out_cw > out_capacity_words) {
+        CK(cudaStreamSynchronize(c->st));
+        return set_err(TC_ERR_BAD_ARG, "output capacity %lld words < %lld", (long long)out_capacity_words,
+                       (long long)rows * out_cw);
+    }
+    CK(cudaStreamWaitEvent(c->st, c->xev[1], 0));
+    if ((rc = launch_low(c, G, plan, c->b_dev, db, b_cw, b_bits > plan->N, GB, one))) return rc;
+    CK(cudaEventRecord(c->ev[1], c->st));
+    const int nh = (int)G.high.size();
+    for (int i = 0; i < nh; ++i)
+        if ((rc = launch_high(c, MODE_FWD, G, GA, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
+    for (int i = 0; i + 1 < nh; ++i)
+        if ((rc = launch_high(c, MODE_FWD, G, GB, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
+    CK(cudaEventRecord(c->ev[2], c->st));
+    if (nh > 0) rc = launch_high(c, MODE_MID, G, GB, GA, G.high[nh - 1].first, G.high[nh - 1].second, one);
+    else rc = launch_high(c, MODE_MID, G, GB, GA, G.lgS, 0, one);
+    if (rc) return rc;
+    CK(cudaEventRecord(c->ev[3], c->st));
+    for (int i = nh - 2; i >= 0; --i)
+        if ((rc = launch_high(c, MODE_INV, G, GB, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
+    CK(cudaEventRecord(c->ev[4], c->st));
+    // k_final in chunks; chunk j's rows (k*T + x, x in the chunk) go to the host while later chunks run
+    const int W32 = 2 * out_cw;
+    if ((rc = c->outbuf.ensure((size_t)rows * out_cw * 8))) return rc;
+    uint32_t* dout = c->outbuf.as<uint32_t>();
+    const int64_t T = G.S >> (G.lgL + G.yl), R = 1ll << G.yl;
+    int nchunk = 1;                                   // >= one wave of CTAs per chunk
+    while (nchunk < 8 && T / (2 * nchunk) >= 148) nchunk *= 2;
+    const int64_t nx = T / nchunk;
+    const size_t rb = (size_t)out_cw * 8;
+    for (int ch = 0; ch < nchunk; ++ch) {
+        const int64_t x0 = ch * nx;
+        if ((rc = launch_final(c, G, GB, rows, (int)plan->M, W32, dout, cc, false, one, x0, nx))) return rc;
+        CK(cudaEventRecord(c->xev[2 + ch], c->st));
+        CK(cudaStreamWaitEvent(c->aux, c->xev[2 + ch], 0));
+        // rows k*T + [x0, x0+nx) for k < R, clipped to rows
+        int64_t kfull = 0;
+        while (kfull < R && kfull * T + x0 + nx <= rows) ++kfull;
+        if (kfull > 0)
+            CK(cudaMemcpy2DAsync((char*)out + x0 * rb, T * rb, (const char*)dout + x0 * rb, T * rb,
+                                 nx * rb, kfull, cudaMemcpyDeviceToHost, c->aux));
+        for (int64_t k = kfull; k < R; ++k) {
+            const int64_t r0 = k * T + x0, r1 = r0 + nx < rows ? r0 + nx : rows;
+            if (r1 > r0)
+                CK(cudaMemcpyAsync((char*)out + r0 * rb, (const char*)dout + r0 * rb, (r1 - r0) * rb,
+                                   cudaMemcpyDeviceToHost, c->aux));
+        }
+    }
+    CK(cudaEventRecord(c->ev[5], c->st));
+    CK(cudaEventRecord(c->ev[6], c->aux));
+    int f[4];
+    if ((rc = read_flags(c, f))) return rc;
+    CK(cudaStreamSynchronize(c->aux));
+    float ms[6] = {0};
+    for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&ms[i], c->ev[i], c->ev[i + 1]);
+    for (int i = 0; i < 6; ++i) c->stage_ms[i] = ms[i];
+    if (times) {
+        times->convert = ms[0] * 1e-3;
+        times->ntt_forward = ms[1] * 1e-3;
+        times->pointwise = ms[2] * 1e-3;
+        times->ntt_inverse = ms[3] * 1e-3;
+        times->crt = 0.0;
+        times->recover = (ms[4] + ms[5]) * 1e-3;
+        times->total = now_s() - t_begin;
+        times->gpus = 1;
+    }
+    if (f[1] != 0x7f7f7f7f) { if (err_index) *err_index = f[1]; return set_err(TC_ERR_RANGE, "coefficient outside the plan's %lld-bit range", (long long)plan->N); }
+    if (f[0] != 0x7f7f7f7f) { if (err_index) *err_index = f[0]; return set_err(TC_ERR_ENCODING, "coefficient %d exceeds the digit capacity", f[0]); }
+    if (f[2] != 0x7f7f7f7f) { if (err_index) *err_index = f[2]; return set_err(TC_ERR_BOUND, "coefficient bound exceeded at flat index %d", f[2]); }
+    return TC_OK;
 }
 
 int tc_digits(void* ctx, int32_t which, int64_t K, int64_t M, int64_t N, int32_t in_bits,

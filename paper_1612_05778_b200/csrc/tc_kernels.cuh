@@ -711,6 +711,10 @@ struct FinalArgs {
     int64_t rows_out; int M; uint32_t minv; int W32;
     uint32_t* out;                 // rows_out x W32 (or rows_out x L x P for DUMP)
     int* err;                      // err[2]: first bad flat index i*L + j
+    // unsharded: CTA x0 + blockIdx.x handles tile bitrev(x) over lgT bits, so
+    // a range of CTAs finishes a 2-D block of natural-order product rows
+    // (rows k*T + x): the host copies it while later chunks compute.
+    uint32_t x0; int lgT;
 };
 
 template <int P, bool DUMP, int NT>
@@ -727,7 +731,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_final(FinalArgs A, c
     const uint32_t n = 1u << tile_bits;
     const uint32_t stride = padded_words(n);
     const bool sharded = A.sh.world > 1;
-    const uint32_t pos0 = (blockIdx.x + (uint32_t)A.sh.h0) * (uint32_t)R;
+    const uint32_t tile = sharded ? blockIdx.x + (uint32_t)A.sh.h0 : bitrev(A.x0 + blockIdx.x, A.lgT);
+    const uint32_t pos0 = tile * (uint32_t)R;
     if (threadIdx.x == 0) s_any = 0;
     __syncthreads();
     for (int r = threadIdx.x; r < R; r += blockDim.x)
@@ -741,7 +746,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_final(FinalArgs A, c
         if (sharded) {
             tile_load(t, A.g + (int64_t)q * (A.sh.Tl << A.sh.TB), n, XchgIdx{A.sh, blockIdx.x});
         } else {
-            const uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)blockIdx.x * n;
+            const uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)tile * n;
             if (n >= 4) tile_load(t, g, n, Contig{});
             else tile_load_scalar(t, g, n, Contig{});
         }

@@ -4,10 +4,10 @@
 `multiply_with_stats` keep the reference's names, arguments, result type,
 error types and StageTimings layout.  The work runs in libtcgpu.so on a B200:
 
-  tc_stage_inputs  H2D copy + device width/zero scan   (tc/params.py:290-293, tc/zpoly.py:103-114)
-  plan_gpu         host planner (params.py)             (tc/params.py:225-313)
-  tc_execute       ConvertIn + 2-D NTTs + pointwise + CRT + ConvertOut + D2H
-                                                        (tc/multiplier.py:131-166)
+  plan_gpu          host planner (params.py)                  (tc/params.py:225-313)
+  tc_multiply_host  H2D + device width/zero scan + ConvertIn + 2-D NTTs + pointwise
+                    + CRT + ConvertOut + D2H, transfers overlapped with kernels
+                                                             (tc/multiplier.py:131-166)
 
 There is no CPU fallback: without the CUDA library or a device every call
 raises DeviceError.  `prime_count` keeps its reference meaning for validation
@@ -106,6 +106,12 @@ def _as_words(p: IntPolynomial) -> np.ndarray:
 
 
 def _run_pipeline(req: MulRequest, plan_override: dict | None = None, device: int = -1):
+    """tc_multiply_host: uploads, kernels and the product download overlapped.
+
+    The plan is made from the declared bit widths (valid for every operand of
+    that width, and the product does not depend on the plan); the true input
+    width -- which fixes the product's bit width, tc/zpoly.py:103-114 -- is
+    reduced on the device while the first pass runs."""
     t_begin = perf_counter()
     ctx = _lib.context(device)
     a, b = req.a, req.b
@@ -113,28 +119,27 @@ def _run_pipeline(req: MulRequest, plan_override: dict | None = None, device: in
     da, db = aw.shape[0], bw.shape[0]
     d = max(da, db)
     rows = da + db - 1
-    info = _lib.TcInputInfo()
+    _check_reference_planning(req, d)
+    n_decl = max(a.bit_width, b.bit_width)
+    po = plan_override or {}
+    plan = plan_gpu(d, min(da, db), max(n_decl, po.get("n_min", 1)), K=po.get("K"), M=po.get("M"))
+    cap_cw = -(-output_bit_width(d, n_decl) // WORD_BITS)
+    buf = _lib.pinned.empty((rows * cap_cw,), np.uint64)     # pinned: DMA at full PCIe rate
+    info = _lib.TcProductInfo()
+    times = _lib.TcTimes()
+    err = ctypes.c_int64(-1)
     lib = ctx.lib
     with ctx.lock:
-        _lib.check(lib.tc_stage_inputs(ctx.handle, _lib.ptr(aw), da, aw.shape[1],
-                                       _lib.ptr(bw), db, bw.shape[1], 0, ctypes.byref(info)),
-                   "tc_stage_inputs")
-        if not (info.nonzero_a and info.nonzero_b):
-            raise EmptyInputError("empty input: zero polynomial")
-        _check_reference_planning(req, d)
-        n_in = max(info.n_in_a, info.n_in_b)
-        po = plan_override or {}
-        plan = plan_gpu(d, min(da, db), max(n_in, po.get("n_min", 1)), K=po.get("K"), M=po.get("M"))
-        out_bits = output_bit_width(d, n_in)
-        out_cw = -(-out_bits // WORD_BITS)
-        out = _lib.pinned.empty((rows, out_cw), np.uint64)   # pinned: D2H at full PCIe rate
-        times = _lib.TcTimes()
-        err = ctypes.c_int64(-1)
-        rc = lib.tc_execute(ctx.handle, ctypes.byref(_lib.make_plan(plan)), a.bit_width, b.bit_width,
-                            _lib.ptr(out), rows, out_cw, 0, ctypes.byref(times), ctypes.byref(err))
+        rc = lib.tc_multiply_host(ctx.handle, _lib.ptr(aw), da, aw.shape[1], a.bit_width,
+                                  _lib.ptr(bw), db, bw.shape[1], b.bit_width,
+                                  ctypes.byref(_lib.make_plan(plan)), _lib.ptr(buf), buf.size,
+                                  ctypes.byref(info), ctypes.byref(times), ctypes.byref(err))
+    if rc == _lib.TC_ERR_EMPTY:
+        raise EmptyInputError("empty input: zero polynomial")
     if rc:
         _raise_status(rc, err.value, plan, a)
-    result = IntPolynomial._trusted(out, out_bits)
+    out = buf[: rows * info.out_cw].reshape(rows, info.out_cw)
+    result = IntPolynomial._trusted(out, info.out_bits)
     total = perf_counter() - t_begin
     stats = StageTimings(convert=times.convert, ntt_forward=times.ntt_forward,
                          pointwise=times.pointwise, ntt_inverse=times.ntt_inverse,
