@@ -59,7 +59,8 @@ typedef struct {
     int64_t M;        /* digit width in bits, 2 <= M <= 63                    */
     int64_t s_y;      /* least power of two >= 2d-1                           */
     int32_t P;        /* number of word primes, 1..TC_MAX_PRIMES              */
-    int32_t flags;    /* reserved, 0                                          */
+    int32_t flags;    /* 0; bit 0 = fault injection for tests: the residue of product
+                         slot (row flags>>16, column 1) is corrupted before the CRT */
     uint32_t p[TC_MAX_PRIMES];  /* primes p < 2^30, 2^k | p-1, 2^k >= max(s_y, 2K) */
     uint32_t g[TC_MAX_PRIMES];  /* a primitive root of each p                       */
 } tc_plan_t;

@@ -128,11 +128,11 @@ def ptr(a: np.ndarray):
     return ctypes.c_void_p(a.ctypes.data)
 
 
-def make_plan(gp) -> TcPlan:
+def make_plan(gp, flags: int = 0) -> TcPlan:
     pl = TcPlan()
     pl.d, pl.N, pl.K, pl.M, pl.s_y = gp.d, gp.N, gp.K, gp.M, gp.s_y
     pl.P = len(gp.primes)
-    pl.flags = 0
+    pl.flags = flags
     for i, s in enumerate(gp.primes):
         pl.p[i] = s.p
         pl.g[i] = s.generator

@@ -250,6 +250,7 @@ struct Geometry {
     int lgL, lgK, lgS, P;
     int yl;                                    // y levels inside k_low / k_final tiles
     std::vector<std::pair<int, int>> high;     // (u0, U) of the k_high passes, ascending
+    int64_t inject = -1;                       // fault injection slot (plan.flags & 1)
 };
 
 // Pass layout: k_final keeps P tiles of 2^(lgL+yl) words in shared memory
@@ -258,6 +259,9 @@ struct Geometry {
 int make_geometry(const tc_plan_t* pl, Geometry& G, int world = 1) {
     G.K = pl->K; G.L = 2 * pl->K; G.s_y = pl->s_y; G.S = G.s_y * G.L;
     G.lgL = ilog2(G.L); G.lgK = ilog2(G.K); G.lgS = ilog2(G.s_y); G.P = pl->P;
+    // flags bit 0: corrupt one residue of product slot (row = flags >> 16, col 1) before the CRT,
+    // so the CorruptedConvolutionError path of tc/multiplier.py:59-63 can be exercised
+    G.inject = (pl->flags & 1) ? (int64_t)((uint32_t)pl->flags >> 16) * G.L + 1 : -1;
     if (G.lgL + G.lgS > 31) return set_err(TC_ERR_BAD_ARG, "grid of 2^%d slots exceeds 2^31", G.lgL + G.lgS);
     const int64_t budget = 96 * 1024;
     int tb = 0;
@@ -356,6 +360,7 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
     FinalArgs A{};
     A.sh = sh;
     A.x0 = (uint32_t)x0; A.lgT = G.lgL + G.lgS - (G.lgL + G.yl);
+    A.inject = G.inject;
     A.g = grids; A.S = G.S; A.lgL = G.lgL; A.lgS = G.lgS; A.yl = G.yl;
     A.twx = c->twx_i.as<uint2>(); A.twy = c->twy_i.as<uint2>();
     A.twy_stride = G.s_y;

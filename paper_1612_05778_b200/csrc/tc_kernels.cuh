@@ -715,6 +715,7 @@ struct FinalArgs {
     // a range of CTAs finishes a 2-D block of natural-order product rows
     // (rows k*T + x): the host copies it while later chunks compute.
     uint32_t x0; int lgT;
+    int64_t inject;                // >= 0: corrupt the residue of flat slot row*L + j (plan.flags)
 };
 
 template <int P, bool DUMP, int NT>
@@ -760,6 +761,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_final(FinalArgs A, c
         uint32_t r[P], x[P];
 #pragma unroll
         for (int q = 0; q < P; ++q) r[q] = canon(sm[q * stride + padi(e)], cc.p[q]);
+        if (A.inject >= 0 && (int64_t)bitrev(pos0 + (e >> A.lgL), A.lgS) * L + (e & (L - 1)) == A.inject)
+            r[0] = r[0] ? r[0] - 1 : cc.p[0] - 1;     // fault injection (tests of the bound check)
         const bool bad = crt_term<P>(r, cc, x);
         const uint32_t row = bitrev(pos0 + (e >> A.lgL), A.lgS);
         const uint32_t j = e & (L - 1);

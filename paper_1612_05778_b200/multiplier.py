@@ -132,7 +132,7 @@ def _run_pipeline(req: MulRequest, plan_override: dict | None = None, device: in
     with ctx.lock:
         rc = lib.tc_multiply_host(ctx.handle, _lib.ptr(aw), da, aw.shape[1], a.bit_width,
                                   _lib.ptr(bw), db, bw.shape[1], b.bit_width,
-                                  ctypes.byref(_lib.make_plan(plan)), _lib.ptr(buf), buf.size,
+                                  ctypes.byref(_lib.make_plan(plan, po.get("flags", 0))), _lib.ptr(buf), buf.size,
                                   ctypes.byref(info), ctypes.byref(times), ctypes.byref(err))
     if rc == _lib.TC_ERR_EMPTY:
         raise EmptyInputError("empty input: zero polynomial")

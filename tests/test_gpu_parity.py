@@ -325,3 +325,38 @@ def test_distributed_multiplier_two_processes(name):
     mp.spawn(_dist_worker, args=(2, port, name, result), nprocs=2, join=True)
     cfg = json.load(open(os.path.join(GOLDEN, "configs.json")))[name]
     assert result["sha"] == cfg["out_sha256"] and result["sha2"] == cfg["out_sha256"]
+
+
+def test_corruption_is_detected():
+    # tc/multiplier.py:59-63: a residue that fails the CRT bound check raises
+    # CorruptedConvolutionError naming the slot; injected through plan.flags
+    from paper_1612_05778_b200.multiplier import _run_pipeline
+    rng = random.Random(77)
+    a = _random_poly(rng, 40, 300)
+    b = _random_poly(rng, 40, 300)
+    for row in (0, 5, 78):
+        with pytest.raises(tc.CorruptedConvolutionError, match=rf"\({row}, 1\)"):
+            _run_pipeline(tc.MulRequest(a, b), plan_override={"flags": 1 | (row << 16)})
+    assert tc.multiply(tc.MulRequest(a, b)) == tc.multiply(tc.MulRequest(b, a))   # no fault: fine
+
+
+def test_extreme_plans(oracle):
+    # K = 1 (no digit split), one prime, and the widest prime sets the planner
+    # reaches with single-word digits; every plan gives the same product
+    rng = random.Random(99)
+    cases = [(5, 12, dict(K=1)), (4, 8, {}), (64, 60, dict(K=1)), (300, 63, dict(K=1)),
+             (2048, 63, dict(K=1)), (2048, 126, dict(K=4)), (33, 1000, dict(K=16))]
+    for d, nbits, kw in cases:
+        a = _random_poly(rng, d, nbits)
+        b = _random_poly(rng, d, nbits)
+        out, _, plan = tc.multiply_with_plan(tc.MulRequest(a, b), **kw)
+        exp, bits = oracle.multiply_words(a.words, a.bit_width, b.words, b.bit_width)
+        assert out.bit_width == bits and np.array_equal(out.words, exp), plan.describe()
+    p1 = plan_gpu(4, 4, 8)
+    assert p1.P == 1
+    wide = plan_gpu(2048, 2048, 63, K=1)
+    assert wide.P >= 5
+    # an explicit split too narrow for the operands is the reference's EncodingError
+    a = _random_poly(rng, 8, 126, extremes=True)
+    with pytest.raises(tc.EncodingError):
+        tc.multiply_with_plan(tc.MulRequest(a, a), K=2, M=63)
