@@ -11,6 +11,7 @@
 #include <stdarg.h>
 #include <string.h>
 #include <climits>
+#include <cstdlib>
 #include <string>
 #include <vector>
 #include <chrono>
@@ -99,6 +100,10 @@ struct Ctx {
 };
 
 int ilog2(int64_t x) { int l = 0; while ((1ll << l) < x) ++l; return l; }
+int env_int(const char* name, int dflt) {           // tuning knobs for experiments
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
 bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 
 uint64_t powmod(uint64_t b, uint64_t e, uint64_t p) {
@@ -250,6 +255,9 @@ struct Geometry {
     int lgL, lgK, lgS, P;
     int yl;                                    // y levels inside k_low / k_final tiles
     std::vector<std::pair<int, int>> high;     // (u0, U) of the k_high passes, ascending
+    int hcb = 4;                               // contiguous column bits of a k_high tile
+    int hthreads = 512;                        // threads per k_high CTA
+    int htile = 14;
     int64_t inject = -1;                       // fault injection slot (plan.flags & 1)
 };
 
@@ -279,10 +287,14 @@ int make_geometry(const tc_plan_t* pl, Geometry& G, int world = 1) {
         return set_err(TC_ERR_BAD_ARG, "P*L = %d*%lld words exceed the final tile's shared memory",
                        G.P, (long long)G.L);
     G.high.clear();
+    G.htile = env_int("TC_HIGH_TILE_BITS", 14);       // k_high tile = 2^htile slots
+    G.hcb = env_int("TC_HIGH_CB", 4);
+    if (G.hcb > G.lgL + yl) G.hcb = G.lgL + yl;
+    G.hthreads = env_int("TC_HIGH_THREADS", 0);       // 0: by tile size (measured on B200)
     const int nlev = G.lgS - yl;
     if (nlev > 0) {
-        const int cb = G.lgL + yl < 4 ? G.lgL + yl : 4;
-        const int UH = 14 - cb;
+        const int cb = G.hcb;
+        const int UH = G.htile - cb;
         const int np = (nlev + UH - 1) / UH;
         const int base = nlev / np, extra = nlev % np;
         int u = yl;
@@ -330,24 +342,39 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
     A.sh = sh;
     A.g = grids; A.other = other; A.S = G.S;
     A.lgL = G.lgL; A.lgS = G.lgS; A.u0 = u0; A.U = U;
-    A.cb = G.lgL + u0 < 4 ? G.lgL + u0 : 4;
+    A.cb = G.hcb;
     A.twf = c->twy_f.as<uint2>(); A.twi = c->twy_i.as<uint2>();
     A.tw_stride = G.s_y;
     A.pcs = c->pcs.as<PrimeC>();
     const uint32_t n = 1u << (U + A.cb);
     const size_t smem = (size_t)padded_words(n) * 4;
-    int threads = (int)(n / 16 > 512 ? 512 : n / 16);
-    if (threads < 32) threads = 32;
+    // 32 slots per thread: 512 threads for 2^14-slot tiles, 256 below (C3: 93 -> 81 ms)
+    const int nth = G.hthreads ? (G.hthreads <= 256 ? 256 : 512) : (n >= 16384 ? 512 : 256);
     dim3 grid((unsigned)(G.S / n / sh.world), (unsigned)G.P);
     if (mode == MODE_FWD) {
-        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_high<MODE_FWD><<<grid, threads, smem, c->st>>>(A);
+        if (nth <= 256) {
+            if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_FWD, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_high<MODE_FWD, 256><<<grid, 256, smem, c->st>>>(A);
+        } else {
+            if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_FWD, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_high<MODE_FWD, 512><<<grid, 512, smem, c->st>>>(A);
+        }
     } else if (mode == MODE_INV) {
-        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_high<MODE_INV><<<grid, threads, smem, c->st>>>(A);
+        if (nth <= 256) {
+            if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_INV, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_high<MODE_INV, 256><<<grid, 256, smem, c->st>>>(A);
+        } else {
+            if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_INV, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_high<MODE_INV, 512><<<grid, 512, smem, c->st>>>(A);
+        }
     } else {
-        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_MID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_high<MODE_MID><<<grid, threads, smem, c->st>>>(A);
+        if (nth <= 256) {
+            if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_MID, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_high<MODE_MID, 256><<<grid, 256, smem, c->st>>>(A);
+        } else {
+            if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_MID, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_high<MODE_MID, 512><<<grid, 512, smem, c->st>>>(A);
+        }
     }
     c->launches++;
     CKL();
@@ -396,16 +423,16 @@ int make_shard(const Geometry& G, int rank, int world, ShardArgs& sh) {
     if (world & (world - 1)) return set_err(TC_ERR_BAD_ARG, "world=%d must be a power of two", world);
     if (rank < 0 || rank >= world) return set_err(TC_ERR_BAD_ARG, "rank %d outside [0, %d)", rank, world);
     const int TB = G.lgL + G.yl;
-    if (TB < 4) return set_err(TC_ERR_BAD_ARG, "grid tile of 2^%d slots too small to shard", TB);
+    if (TB < 4 || G.hcb < 2) return set_err(TC_ERR_BAD_ARG, "grid tile of 2^%d slots too small to shard", TB);
     const int64_t T = 1ll << (G.lgL + G.lgS - TB);
-    const int64_t Mtot = 1ll << (TB - 4);
+    const int64_t Mtot = 1ll << (TB - G.hcb);
     if (T % world || Mtot % world)
         return set_err(TC_ERR_BAD_ARG, "grid (%lld tiles, %lld column groups) does not split over %d ranks",
                        (long long)T, (long long)Mtot, world);
     sh.world = world; sh.rank = rank; sh.TB = TB;
     sh.Tl = T / world; sh.h0 = (int64_t)rank * sh.Tl;
     const int64_t Mloc = Mtot / world;
-    sh.m0 = (uint32_t)(rank * Mloc); sh.lmloc = ilog2(Mloc); sh.lchunk = sh.lmloc + 4;
+    sh.m0 = (uint32_t)(rank * Mloc); sh.lmloc = ilog2(Mloc); sh.lchunk = sh.lmloc + G.hcb;
     return TC_OK;
 }
 

@@ -539,8 +539,8 @@ struct HighArgs {
     const PrimeC* pcs;
 };
 
-template <int MODE>
-__global__ void __launch_bounds__(512, 2) k_high(HighArgs A) {
+template <int MODE, int NT>
+__global__ void __launch_bounds__(NT, NT <= 256 ? 4 : 2) k_high(HighArgs A) {
     extern __shared__ __align__(16) uint32_t s[];
     const int q = blockIdx.y;
     const bool sharded = A.sh.world > 1;
