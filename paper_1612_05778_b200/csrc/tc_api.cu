@@ -349,10 +349,13 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
     const uint32_t n = 1u << (U + A.cb);
     const size_t smem = (size_t)padded_words(n) * 4;
     // 32 slots per thread: 512 threads for 2^14-slot tiles, 256 below (C3: 93 -> 81 ms)
-    const int nth = G.hthreads ? (G.hthreads <= 256 ? 256 : 512) : (n >= 16384 ? 512 : 256);
+    const int nth = G.hthreads ? (G.hthreads <= 256 ? 256 : 512)
+                               : (n >= 16384 ? 512 : (n >= 4096 ? 256 : 64));
     dim3 grid((unsigned)(G.S / n / sh.world), (unsigned)G.P);
     if (mode == MODE_FWD) {
-        if (nth <= 256) {
+        if (nth <= 64) {
+            k_high<MODE_FWD, 64><<<grid, 64, smem, c->st>>>(A);
+        } else if (nth <= 256) {
             if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_FWD, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             k_high<MODE_FWD, 256><<<grid, 256, smem, c->st>>>(A);
         } else {
@@ -360,7 +363,9 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
             k_high<MODE_FWD, 512><<<grid, 512, smem, c->st>>>(A);
         }
     } else if (mode == MODE_INV) {
-        if (nth <= 256) {
+        if (nth <= 64) {
+            k_high<MODE_INV, 64><<<grid, 64, smem, c->st>>>(A);
+        } else if (nth <= 256) {
             if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_INV, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             k_high<MODE_INV, 256><<<grid, 256, smem, c->st>>>(A);
         } else {
@@ -368,7 +373,9 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
             k_high<MODE_INV, 512><<<grid, 512, smem, c->st>>>(A);
         }
     } else {
-        if (nth <= 256) {
+        if (nth <= 64) {
+            k_high<MODE_MID, 64><<<grid, 64, smem, c->st>>>(A);
+        } else if (nth <= 256) {
             if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_MID, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             k_high<MODE_MID, 256><<<grid, 256, smem, c->st>>>(A);
         } else {
