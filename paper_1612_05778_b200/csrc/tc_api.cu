@@ -324,9 +324,13 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     const size_t smem = (size_t)Rc * G.K * 8 + (size_t)Rc * 8 + (size_t)padded_words(n) * 4;
     const int64_t ctas = sh.world > 1 ? sh.Tl : G.S / n;
     // a tile too large for two CTAs per SM gets 32 warps in one CTA
-    if (smem > 112 * 1024) {
+    const int lt = env_int("TC_LOW_THREADS", 0);
+    if (smem > 112 * 1024 || lt >= 1024) {
         CK(cudaFuncSetAttribute(k_low<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_low<1024><<<(unsigned)ctas, 1024, smem, c->st>>>(a);
+    } else if (lt == 256 || lt == 0) {            // 256 threads: measured faster (C2 0.268 -> 0.228 ms)
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_low<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_low<256><<<(unsigned)ctas, 256, smem, c->st>>>(a);
     } else {
         if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_low<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_low<512><<<(unsigned)ctas, 512, smem, c->st>>>(a);

@@ -440,7 +440,7 @@ struct LowArgs {
 };
 
 template <int NT>
-__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_low(LowArgs A) {
+__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_low(LowArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int R = 1 << A.yl;                 // row positions in the tile
     // Odd positions hold coefficients >= s_y/2 >= d: zero rows.  With yl >= 1
@@ -719,7 +719,7 @@ struct FinalArgs {
 };
 
 template <int P, bool DUMP, int NT>
-__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2) k_final(FinalArgs A, const __grid_constant__ CrtConst cc) {
+__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_final(FinalArgs A, const __grid_constant__ CrtConst cc) {
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ uint32_t wtf[32], warp_tf1[32], wcin1[32], wcin2[32];
     __shared__ int64_t whi[32];
