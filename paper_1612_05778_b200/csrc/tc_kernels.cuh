@@ -33,6 +33,9 @@
 namespace tc {
 
 constexpr int kMaxPrimes = 16;
+#ifndef TC_HIGH_MINB
+#define TC_HIGH_MINB 3      // 256-thread k_high CTAs per SM the register budget is sized for
+#endif
 
 // ---------------------------------------------------------------------------
 // Width scan: max two's-complement width and non-zero flag of a polynomial
@@ -540,7 +543,7 @@ struct HighArgs {
 };
 
 template <int MODE, int NT>
-__global__ void __launch_bounds__(NT, NT <= 256 ? 4 : 2) k_high(HighArgs A) {
+__global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (NT <= 256 ? TC_HIGH_MINB : 2)) k_high(HighArgs A) {
     extern __shared__ __align__(16) uint32_t s[];
     const int q = blockIdx.y;
     const bool sharded = A.sh.world > 1;
@@ -923,11 +926,12 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
             if (lane == 0) s_hi = whi[nw - 1];
         }
         __syncthreads();
-        const uint32_t cv = wcin1[warp];
-        uint32_t bin = (uint32_t)(((A2[cv] + B2[cv] + wcin2[warp]) ^ A2[cv] ^ B2[cv]) >> lane) & 1u;
+        const bool cv = wcin1[warp] != 0;            // selects, not indexing: keeps arrays in registers
+        const uint64_t A2c = cv ? A2[1] : A2[0], B2c = cv ? B2[1] : B2[0];
+        uint32_t bin = (uint32_t)(((A2c + B2c + wcin2[warp]) ^ A2c ^ B2c) >> lane) & 1u;
 #pragma unroll
         for (int k = 0; k < kW; ++k) {
-            const uint32_t x = w1v[cv][k];
+            const uint32_t x = cv ? w1v[1][k] : w1v[0][k];
             if (valid[k]) {
                 const uint32_t prow = bitrev(pos0 + rw[k], A.lgS);
                 if (sharded)   // compact rows in position order; unshard() permutes
