@@ -340,6 +340,23 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     return TC_OK;
 }
 
+template <int NT, int U, int MODE>
+cudaError_t launch_high_ct_mode(const HighArgs& A, dim3 grid, uint32_t n, cudaStream_t st) {
+    const size_t smem = (size_t)ct_tw_offset_words(n) * 4 + (MODE == MODE_MID ? 2 : 1) * ((size_t)8 << U);
+    cudaError_t e = cudaSuccess;
+    if (smem > 48 * 1024) e = cudaFuncSetAttribute(k_high_ct<MODE, NT, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_high_ct<MODE, NT, U><<<grid, NT, smem, st>>>(A);
+    return cudaGetLastError();
+}
+
+template <int NT, int U>
+cudaError_t launch_high_ct(int mode, const HighArgs& A, dim3 grid, uint32_t n, cudaStream_t st) {
+    if (mode == MODE_FWD) return launch_high_ct_mode<NT, U, MODE_FWD>(A, grid, n, st);
+    if (mode == MODE_INV) return launch_high_ct_mode<NT, U, MODE_INV>(A, grid, n, st);
+    return launch_high_ct_mode<NT, U, MODE_MID>(A, grid, n, st);
+}
+
 int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint32_t* other, int u0, int U,
                 const ShardArgs& sh) {
     HighArgs A{};
@@ -356,6 +373,19 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
     const int nth = G.hthreads ? (G.hthreads <= 256 ? 256 : 512)
                                : (n >= 16384 ? 512 : (n >= 4096 ? 256 : 64));
     dim3 grid((unsigned)(G.S / n / sh.world), (unsigned)G.P);
+    // compile-time pass shapes (k_high_ct): cb = 4, rows below u0 fixed per CTA
+    if (A.cb == 4 && G.lgL >= 4 && env_int("TC_HIGH_CT", 1)) {
+        cudaError_t e = cudaErrorNotSupported;
+        if (U == 10 && nth == 512) e = launch_high_ct<512, 10>(mode, A, grid, n, c->st);
+        else if (U == 9 && nth == 256) e = launch_high_ct<256, 9>(mode, A, grid, n, c->st);
+        else if (U == 4 && nth == 64) e = launch_high_ct<64, 4>(mode, A, grid, n, c->st);
+        if (e != cudaErrorNotSupported) {
+            c->launches++;
+            if (e != cudaSuccess) return set_err(TC_ERR_CUDA, "k_high_ct launch failed: %s", cudaGetErrorString(e));
+            CKL();
+            return TC_OK;
+        }
+    }
     if (mode == MODE_FWD) {
         if (nth <= 64) {
             k_high<MODE_FWD, 64><<<grid, 64, smem, c->st>>>(A);

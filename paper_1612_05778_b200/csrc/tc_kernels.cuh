@@ -36,6 +36,9 @@ constexpr int kMaxPrimes = 16;
 #ifndef TC_HIGH_MINB
 #define TC_HIGH_MINB 3      // 256-thread k_high CTAs per SM the register budget is sized for
 #endif
+#ifndef TC_ROUND_G2
+#define TC_ROUND_G2 1       // interleave two register groups per round when each thread owns >= 2
+#endif
 
 // ---------------------------------------------------------------------------
 // Width scan: max two's-complement width and non-zero flag of a polynomial
@@ -88,16 +91,22 @@ __device__ __forceinline__ uint32_t bitrev(uint32_t x, int bits) {
     return bits ? __brev(x) >> (32 - bits) : 0u;
 }
 
-// Padded shared-memory index: one spare word per 16 keeps the stride-16
-// accesses of radix-16 rounds on low bits conflict-free, and is linear inside
-// any round that does not straddle bit 4 (run_bits never lets one).
-__device__ __forceinline__ uint32_t padi(uint32_t e) { return e + (e >> 4); }
-__host__ __device__ constexpr uint32_t padded_words(uint32_t n) { return n + (n >> 4) + 1; }
+// Padded shared-memory index: one spare word per 32.  Any 32 aligned
+// consecutive slots stay in 32 distinct banks (rounds on bits >= 5, tile
+// copies), and the transposed accesses of rounds on bits [0, NB) land on
+// distinct banks through the pad (32 rows of 2^NB slots shift by one bank per
+// 32 slots).  Rounds at bit_lo in [1, 4] permute their group index
+// (round_lane_perm) so the half-warps of a round differ by 512 slots (pad
+// offset 16).  The mapping is affine in a round's element index except for a
+// round at bit 4 that crosses bit 5, whose offsets are compile-time constants
+// (round_exec<..., ST4>).
+__device__ __forceinline__ uint32_t padi(uint32_t e) { return e + (e >> 5); }
+__host__ __device__ constexpr uint32_t padded_words(uint32_t n) { return n + (n >> 5) + 1; }
 
 // Tile copies between global and (padded) shared memory.  Slots come in
 // aligned runs of 4 that are contiguous in both layouts (tile index e..e+3 ->
 // grid index gidx(e)..gidx(e)+3, and padi is linear inside an aligned run of
-// 16), so each thread moves 16 bytes per LDG.128 / STG.128; kBatch vector
+// 32), so each thread moves 16 bytes per LDG.128 / STG.128; kBatch vector
 // loads stay in flight per thread.  Requires n % 4 == 0 and gidx(e) % 4 == 0
 // for e % 4 == 0 (callers fall back to tile_*_scalar otherwise).
 constexpr int kBatch = 4;
@@ -289,57 +298,115 @@ static __global__ void __launch_bounds__(256) k_digits(DigitSrc a, int R, int64_
 // bits below the stage bit, so a level with 2^lv distinct twiddles loads each
 // once.  tw(e, bit) returns {w, w_shoup} for the lower element e at tile bit.
 // ---------------------------------------------------------------------------
-template <int NB, bool DIF, class TW>
-__device__ __forceinline__ void round_exec(uint32_t* s, int tile_bits, int bit_lo, const TW& tw,
-                                           uint32_t p, uint32_t two_p) {
+// G groups per iteration (G = 2 when every thread owns >= 2 groups): two
+// independent butterfly chains interleave, hiding shared/twiddle latency.
+// Group-index permutation of a round at bit_lo in [1, 4]: swaps g's lane
+// bits [bit_lo, 5) with bits [bit_lo + 5 - NB, 10 - NB), which sit at slot
+// bits [5 + bit_lo, 10): the half-warps then differ by pad offsets 2^bit_lo..16
+// (a bijection when bit_lo >= NB and the tile has >= 10 bits).
+struct LanePerm {
+    uint32_t m, a, b;          // field mask, positions; m == 0: identity
+    __device__ __forceinline__ uint32_t operator()(uint32_t g) const {
+        const uint32_t t = ((g >> a) ^ (g >> b)) & m;
+        return g ^ (t << a) ^ (t << b);
+    }
+};
+__device__ __forceinline__ LanePerm round_lane_perm(int tile_bits, int bit_lo, int NB) {
+    if (bit_lo >= 1 && bit_lo <= 4 && bit_lo >= NB && tile_bits >= 10)
+        return LanePerm{(1u << (5 - bit_lo)) - 1, (uint32_t)bit_lo, (uint32_t)(bit_lo + 5 - NB)};
+    return LanePerm{0u, 0u, 0u};
+}
+
+// Slot offset of element k of a group: k * astep, or for a round at bit 4
+// crossing bit 5 (ST4), 16 k + k / 2.
+template <bool ST4>
+__device__ __forceinline__ uint32_t elem_off(int k, uint32_t astep) {
+    return ST4 ? (uint32_t)(16 * k + (k >> 1)) : k * astep;
+}
+
+template <int NB, int G, bool DIF, bool ST4, class TW>
+__device__ __forceinline__ void round_groups(uint32_t* s, uint32_t g0, uint32_t gstride, uint32_t lowmask,
+                                             uint32_t astep, int bit_lo, const uint2* tp, uint32_t tstep,
+                                             const TW& tw, uint32_t p, uint32_t two_p, LanePerm pm) {
     constexpr int R = 1 << NB;
-    const uint32_t ngroups = 1u << (tile_bits - NB);
-    const uint32_t lowmask = (1u << bit_lo) - 1;
-    const uint32_t astep = bit_lo >= 4 ? (1u << bit_lo) + (1u << (bit_lo - 4)) : (1u << bit_lo);
-    const uint2* tp = tw.table(bit_lo);
-    const uint32_t tstep = 1u << tw.shift(bit_lo);
-    for (uint32_t g = threadIdx.x; g < ngroups; g += blockDim.x) {
-        const uint32_t lo = g & lowmask;
-        const uint32_t a0 = padi(((g & ~lowmask) << NB) | lo);
-        uint32_t x[R];
+    uint32_t lo[G], a0[G];
+    uint32_t x[G][R];
 #pragma unroll
-        for (int k = 0; k < R; ++k) x[k] = s[a0 + k * astep];
+    for (int q = 0; q < G; ++q) {
+        const uint32_t g = pm(g0 + q * gstride);
+        lo[q] = g & lowmask;
+        a0[q] = padi(((g & ~lowmask) << NB) | lo[q]);
 #pragma unroll
-        for (int it = 0; it < NB; ++it) {
-            const int lv = DIF ? NB - 1 - it : it;
-            const uint2* tq = tp + tw.base(lo, bit_lo + lv);   // one 64-bit address per level
+        for (int k = 0; k < R; ++k) x[q][k] = s[a0[q] + elem_off<ST4>(k, astep)];
+    }
 #pragma unroll
-            for (int m = 0; m < (1 << lv); ++m) {
-                const uint2 w = __ldg(tq + m * tstep);
+    for (int it = 0; it < NB; ++it) {
+        const int lv = DIF ? NB - 1 - it : it;
+        const uint2* tq[G];
+#pragma unroll
+        for (int q = 0; q < G; ++q) tq[q] = tp + tw.base(lo[q], bit_lo + lv);   // one 64-bit address per level
+#pragma unroll
+        for (int m = 0; m < (1 << lv); ++m) {
+#pragma unroll
+            for (int q = 0; q < G; ++q) {
+                const uint2 w = __ldg(tq[q] + m * tstep);
 #pragma unroll
                 for (int jj = 0; jj < R / (2 << lv); ++jj) {
                     const int k = m + jj * (2 << lv);
-                    if (DIF) bfly_dif(x[k], x[k + (1 << lv)], w.x, w.y, p, two_p);
-                    else bfly_dit(x[k], x[k + (1 << lv)], w.x, w.y, p, two_p);
+                    if (DIF) bfly_dif(x[q][k], x[q][k + (1 << lv)], w.x, w.y, p, two_p);
+                    else bfly_dit(x[q][k], x[q][k + (1 << lv)], w.x, w.y, p, two_p);
                 }
             }
         }
+    }
 #pragma unroll
-        for (int k = 0; k < R; ++k) s[a0 + k * astep] = x[k];
+    for (int q = 0; q < G; ++q)
+#pragma unroll
+        for (int k = 0; k < R; ++k) s[a0[q] + elem_off<ST4>(k, astep)] = x[q][k];
+}
+
+template <int NB, bool DIF, int ILP, class TW>
+__device__ __forceinline__ void round_exec(uint32_t* s, int tile_bits, int bit_lo, const TW& tw,
+                                           uint32_t p, uint32_t two_p) {
+    const uint32_t ngroups = 1u << (tile_bits - NB);
+    const uint32_t lowmask = (1u << bit_lo) - 1;
+    const uint32_t astep = bit_lo >= 5 ? (1u << bit_lo) + (1u << (bit_lo - 5)) : (1u << bit_lo);
+    const uint2* tp = tw.table(bit_lo);
+    const uint32_t tstep = 1u << tw.shift(bit_lo);
+    const uint32_t nt = blockDim.x;
+    const LanePerm pm = round_lane_perm(tile_bits, bit_lo, NB);
+    if (NB >= 2 && bit_lo == 4) {               // crosses bit 5: constant offsets
+        for (uint32_t g = threadIdx.x; g < ngroups; g += nt)
+            round_groups<NB, 1, DIF, true>(s, g, nt, lowmask, astep, bit_lo, tp, tstep, tw, p, two_p, pm);
+    } else
+#if TC_ROUND_G2
+    if (ILP == 2 && NB == 3 && ngroups >= 2 * nt) {
+        for (uint32_t g = threadIdx.x; g < ngroups; g += 2 * nt)
+            round_groups<NB, 2, DIF, false>(s, g, nt, lowmask, astep, bit_lo, tp, tstep, tw, p, two_p, pm);
+    } else
+#endif
+    {
+        for (uint32_t g = threadIdx.x; g < ngroups; g += nt)
+            round_groups<NB, 1, DIF, false>(s, g, nt, lowmask, astep, bit_lo, tp, tstep, tw, p, two_p, pm);
     }
     __syncthreads();
 }
 
-template <bool DIF, class TW>
+template <bool DIF, int ILP, class TW>
 __device__ __forceinline__ void round_dispatch(int nb, uint32_t* s, int tile_bits, int bit_lo, const TW& tw,
                                                uint32_t p, uint32_t two_p) {
     switch (nb) {
-        case 4: round_exec<4, DIF>(s, tile_bits, bit_lo, tw, p, two_p); break;
-        case 3: round_exec<3, DIF>(s, tile_bits, bit_lo, tw, p, two_p); break;
-        case 2: round_exec<2, DIF>(s, tile_bits, bit_lo, tw, p, two_p); break;
-        case 1: round_exec<1, DIF>(s, tile_bits, bit_lo, tw, p, two_p); break;
+        case 4: round_exec<4, DIF, ILP>(s, tile_bits, bit_lo, tw, p, two_p); break;
+        case 3: round_exec<3, DIF, ILP>(s, tile_bits, bit_lo, tw, p, two_p); break;
+        case 2: round_exec<2, DIF, ILP>(s, tile_bits, bit_lo, tw, p, two_p); break;
+        case 1: round_exec<1, DIF, ILP>(s, tile_bits, bit_lo, tw, p, two_p); break;
         default: break;
     }
 }
 
 // Stages on tile bits [lo, hi): DIT ascending in rounds of <= 4 bits, DIF
 // descending; rounds never straddle bit 4 (linear padded addressing).
-template <bool DIF, class TW>
+template <bool DIF, int ILP = 1, class TW>
 __device__ __forceinline__ void run_segment(uint32_t* s, int tile_bits, int lo, int hi, const TW& tw,
                                             uint32_t p, uint32_t two_p) {
     const int nbits = hi - lo;
@@ -350,7 +417,7 @@ __device__ __forceinline__ void run_segment(uint32_t* s, int tile_bits, int lo, 
         int b = lo;
         for (int r = 0; r < nr; ++r) {
             const int nb = base + (r < extra ? 1 : 0);
-            round_dispatch<false>(nb, s, tile_bits, b, tw, p, two_p);
+            round_dispatch<false, ILP>(nb, s, tile_bits, b, tw, p, two_p);
             b += nb;
         }
     } else {
@@ -358,22 +425,22 @@ __device__ __forceinline__ void run_segment(uint32_t* s, int tile_bits, int lo, 
         for (int r = 0; r < nr; ++r) {
             const int nb = base + (r < extra ? 1 : 0);
             b -= nb;
-            round_dispatch<true>(nb, s, tile_bits, b, tw, p, two_p);
+            round_dispatch<true, ILP>(nb, s, tile_bits, b, tw, p, two_p);
         }
     }
 }
 
-template <bool DIF, class TW>
+template <bool DIF, int ILP = 1, class TW>
 __device__ __forceinline__ void run_bits(uint32_t* s, int tile_bits, int lo, int hi, const TW& tw,
                                          uint32_t p, uint32_t two_p) {
     const int mid = lo < 4 && hi > 4 ? 4 : lo;
-    if (mid == lo) { run_segment<DIF>(s, tile_bits, lo, hi, tw, p, two_p); return; }
+    if (mid == lo) { run_segment<DIF, ILP>(s, tile_bits, lo, hi, tw, p, two_p); return; }
     if (!DIF) {
-        run_segment<false>(s, tile_bits, lo, mid, tw, p, two_p);
-        run_segment<false>(s, tile_bits, mid, hi, tw, p, two_p);
+        run_segment<false, ILP>(s, tile_bits, lo, mid, tw, p, two_p);
+        run_segment<false, ILP>(s, tile_bits, mid, hi, tw, p, two_p);
     } else {
-        run_segment<true>(s, tile_bits, mid, hi, tw, p, two_p);
-        run_segment<true>(s, tile_bits, lo, mid, tw, p, two_p);
+        run_segment<true, ILP>(s, tile_bits, mid, hi, tw, p, two_p);
+        run_segment<true, ILP>(s, tile_bits, lo, mid, tw, p, two_p);
     }
 }
 
@@ -576,7 +643,7 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (NT <= 256 ? TC_HIGH_MINB :
     __syncthreads();
     const TwHigh tf{A.twf + (int64_t)q * A.tw_stride, A.lgL, A.u0, A.cb, mid << A.cb};
     if (MODE == MODE_FWD || MODE == MODE_MID)
-        run_bits<false>(s, tile_bits, A.cb, tile_bits, tf, pc.p, pc.two_p);
+        run_bits<false, (NT == 256 ? 2 : 1)>(s, tile_bits, A.cb, tile_bits, tf, pc.p, pc.two_p);
     if (MODE == MODE_MID) {
         const uint32_t* ga = A.other + (int64_t)q * qstride;
         auto pw = [&](uint32_t e, uint32_t y) {
@@ -609,10 +676,172 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (NT <= 256 ? TC_HIGH_MINB :
     if (MODE == MODE_INV || MODE == MODE_MID) {
         TwHigh ti = tf;
         ti.twy = A.twi + (int64_t)q * A.tw_stride;
-        run_bits<true>(s, tile_bits, A.cb, tile_bits, ti, pc.p, pc.two_p);
+        run_bits<true, (NT == 256 ? 2 : 1)>(s, tile_bits, A.cb, tile_bits, ti, pc.p, pc.two_p);
     }
     if (A.cb >= 2) tile_store(g, s, n, hidx);
     else tile_store_scalar(g, s, n, hidx);
+}
+
+// ---------------------------------------------------------------------------
+// k_high_ct: k_high with the pass shape fixed at compile time (cb = 4, U y
+// levels, NT threads) for the shapes the planner produces most (U = 10, 9, 4).
+// Every round's bit position, stride, lane permutation and twiddle offset is
+// a constant, so shared accesses use [R + imm] addressing, and the 2^U - 1
+// twiddles of the CTA (its row offset below u0 is fixed when lgL >= cb) are
+// gathered once into shared memory: level v' entry a' at index 2^v' + a',
+// = twy[2^(u0+v') + rb + (a' << u0)] (TwHigh's index).
+// ---------------------------------------------------------------------------
+template <int TB, int BL, int NB, bool DIF, int NT>
+__device__ __forceinline__ void ct_round(uint32_t* s, const uint2* stw, uint32_t p, uint32_t two_p) {
+    constexpr int R = 1 << NB, CB = 4;
+    constexpr uint32_t ngroups = 1u << (TB - NB);
+    constexpr uint32_t lowmask = (1u << BL) - 1;
+    constexpr bool PERM = BL >= 1 && BL <= 4 && BL >= NB && TB >= 10;
+    constexpr uint32_t pm = PERM ? (1u << (5 - BL)) - 1 : 0u, pa = BL, pb = BL + 5 - NB;
+    static_assert(BL >= CB, "k_high rounds start at the column bits");
+#pragma unroll 1
+    for (uint32_t g0 = threadIdx.x; g0 < ngroups; g0 += NT) {
+        uint32_t g = g0;
+        if (PERM) {
+            const uint32_t t = ((g >> pa) ^ (g >> pb)) & pm;
+            g ^= (t << pa) ^ (t << pb);
+        }
+        const uint32_t lo = g & lowmask;
+        uint32_t* sp = s + padi(((g & ~lowmask) << NB) | lo);
+        const uint2* tq = stw + (lo >> CB);
+        uint32_t x[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) x[k] = sp[(k << BL) + ((k << BL) >> 5)];
+#pragma unroll
+        for (int it = 0; it < NB; ++it) {
+            const int lv = DIF ? NB - 1 - it : it;
+            const int vp = BL + lv - CB;                       // level inside the pass
+#pragma unroll
+            for (int m = 0; m < (1 << lv); ++m) {
+                const uint2 w = tq[(1 << vp) + (m << (BL - CB))];
+#pragma unroll
+                for (int jj = 0; jj < R / (2 << lv); ++jj) {
+                    const int k = m + jj * (2 << lv);
+                    if (DIF) bfly_dif(x[k], x[k + (1 << lv)], w.x, w.y, p, two_p);
+                    else bfly_dit(x[k], x[k + (1 << lv)], w.x, w.y, p, two_p);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) sp[(k << BL) + ((k << BL) >> 5)] = x[k];
+    }
+    __syncthreads();
+}
+
+// Round schedule of a pass of U levels on tile bits [4, 4 + U).
+template <int U, bool DIF, int NT>
+__device__ __forceinline__ void ct_pass(uint32_t* s, const uint2* stw, uint32_t p, uint32_t two_p) {
+    constexpr int TB = U + 4;
+    if constexpr (U == 10) {
+        if (!DIF) {
+            ct_round<TB, 4, 4, false, NT>(s, stw, p, two_p);
+            ct_round<TB, 8, 3, false, NT>(s, stw, p, two_p);
+            ct_round<TB, 11, 3, false, NT>(s, stw, p, two_p);
+        } else {
+            ct_round<TB, 11, 3, true, NT>(s, stw, p, two_p);
+            ct_round<TB, 8, 3, true, NT>(s, stw, p, two_p);
+            ct_round<TB, 4, 4, true, NT>(s, stw, p, two_p);
+        }
+    } else if constexpr (U == 9) {
+        if (!DIF) {
+            ct_round<TB, 4, 3, false, NT>(s, stw, p, two_p);
+            ct_round<TB, 7, 3, false, NT>(s, stw, p, two_p);
+            ct_round<TB, 10, 3, false, NT>(s, stw, p, two_p);
+        } else {
+            ct_round<TB, 10, 3, true, NT>(s, stw, p, two_p);
+            ct_round<TB, 7, 3, true, NT>(s, stw, p, two_p);
+            ct_round<TB, 4, 3, true, NT>(s, stw, p, two_p);
+        }
+    } else {
+        static_assert(U == 4, "unsupported compile-time pass");
+        ct_round<TB, 4, 4, DIF, NT>(s, stw, p, two_p);
+    }
+}
+
+__host__ __device__ constexpr uint32_t ct_tw_offset_words(uint32_t n) { return (padded_words(n) + 1) & ~1u; }
+
+template <int MODE, int NT, int U>
+__global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (NT <= 256 ? TC_HIGH_MINB : 2)) k_high_ct(HighArgs A) {
+    constexpr int CB = 4, TB = U + CB;
+    constexpr uint32_t n = 1u << TB, ntw = 1u << U;
+    extern __shared__ __align__(16) uint32_t s[];
+    uint2* stw_f = reinterpret_cast<uint2*>(s + ct_tw_offset_words(n));
+    uint2* stw_i = MODE == MODE_MID ? stw_f + ntw : stw_f;
+    const int q = blockIdx.y;
+    const bool sharded = A.sh.world > 1;
+    const int64_t qstride = sharded ? (A.sh.Tl << A.sh.TB) : A.S;
+    uint32_t* g = A.g + (int64_t)q * qstride;
+    const PrimeC pc = A.pcs[q];
+    const int b0 = A.lgL + A.u0;
+    const int nmid = b0 - CB;
+    const uint32_t cta = blockIdx.x;
+    uint32_t mid, hi, pml = 0;
+    if (!sharded) {
+        mid = cta & ((1u << nmid) - 1);
+        hi = cta >> nmid;
+    } else {
+        pml = cta & ((1u << A.sh.lmloc) - 1);
+        const uint32_t y = cta >> A.sh.lmloc;
+        const int rbits = b0 - A.sh.TB;
+        mid = ((y & ((1u << rbits) - 1)) << (A.sh.TB - CB)) | (A.sh.m0 + pml);
+        hi = y >> rbits;
+    }
+    // CTA twiddles (requires lgL >= CB: the row bits below u0 come from mid only)
+    {
+        const uint32_t rb = mid >> (A.lgL - CB);
+        const uint2* twf = A.twf + (int64_t)q * A.tw_stride;
+        const uint2* twi = A.twi + (int64_t)q * A.tw_stride;
+        for (uint32_t i = threadIdx.x; i < ntw; i += NT) {
+            if (i == 0) continue;
+            const int v = 31 - __clz(i);
+            const uint32_t gi = (1u << (A.u0 + v)) + rb + ((i - (1u << v)) << A.u0);
+            if (MODE != MODE_INV) stw_f[i] = __ldg(twf + gi);
+            if (MODE != MODE_FWD) stw_i[i] = __ldg(twi + gi);
+        }
+    }
+    const uint32_t base = (hi << (b0 + U)) | (mid << CB);
+    constexpr uint32_t cmask = (1u << CB) - 1;
+    const HighIdx hidx = sharded
+        ? HighIdx{((base >> A.sh.TB) << A.sh.lchunk) | (pml << CB), CB, b0 - A.sh.TB + A.sh.lchunk, cmask}
+        : HighIdx{base, CB, b0, cmask};
+    tile_load(s, g, n, hidx);
+    __syncthreads();
+    if (MODE == MODE_FWD || MODE == MODE_MID) ct_pass<U, false, NT>(s, stw_f, pc.p, pc.two_p);
+    if (MODE == MODE_MID) {
+        const uint32_t* ga = A.other + (int64_t)q * qstride;
+        constexpr uint32_t nv = n >> 2;
+#pragma unroll 1
+        for (uint32_t v0 = threadIdx.x; v0 < nv; v0 += 4 * NT) {
+            uint4 y[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t vi = v0 + k * NT;
+                y[k] = vi < nv ? *reinterpret_cast<const uint4*>(ga + hidx(vi << 2)) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t vi = v0 + k * NT;
+                if (vi < nv) {
+                    uint32_t* d = s + padi(vi << 2);
+                    const uint32_t yy[4] = {y[k].x, y[k].y, y[k].z, y[k].w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t x = reduce_2p(d[j], pc.two_p);
+                        d[j] = shoup_mul(mont_mul(x, reduce_2p(yy[j], pc.two_p), pc.p, pc.pinv_neg),
+                                         pc.scale, pc.scale_sh, pc.p);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (MODE == MODE_INV || MODE == MODE_MID) ct_pass<U, true, NT>(s, stw_i, pc.p, pc.two_p);
+    tile_store(g, s, n, hidx);
 }
 
 // ---------------------------------------------------------------------------
