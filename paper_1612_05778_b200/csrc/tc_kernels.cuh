@@ -450,6 +450,106 @@ __device__ __forceinline__ void run_bits(uint32_t* s, int tile_bits, int lo, int
 // at base + (m << shift).
 // Whole-row tiles (k_low / k_final): tile index e = local_row * L + col; a
 // round lies entirely in the x bits [0, lgL) or the y bits.
+// ---------------------------------------------------------------------------
+// x-direction transform with a compile-time round schedule (lgL is one of 13
+// values; the same rounds as run_bits on [0, lgL)): constant strides, lane
+// permutation and twiddle offsets (level-major x table: lower element with
+// bits lo below stage bit b uses entry 2^b + lo).  The tile size stays a
+// runtime value (only the group count depends on it).
+// ---------------------------------------------------------------------------
+template <int BL, int NB, bool DIF>
+__device__ __forceinline__ void xct_round(uint32_t* s, int tile_bits, const uint2* twx, uint32_t p, uint32_t two_p) {
+    constexpr int R = 1 << NB;
+    constexpr uint32_t lowmask = (1u << BL) - 1;
+    constexpr bool PERMC = BL >= 1 && BL <= 4 && BL >= NB;
+    constexpr uint32_t pa = BL, pb = BL + 5 - NB;
+    const uint32_t pm = (PERMC && tile_bits >= 10) ? (1u << (5 - BL)) - 1 : 0u;
+    const uint32_t ngroups = 1u << (tile_bits - NB);
+    for (uint32_t g0 = threadIdx.x; g0 < ngroups; g0 += blockDim.x) {
+        uint32_t g = g0;
+        if (PERMC) {
+            const uint32_t t = ((g >> pa) ^ (g >> pb)) & pm;
+            g ^= (t << pa) ^ (t << pb);
+        }
+        const uint32_t lo = g & lowmask;
+        uint32_t* sp = s + padi(((g & ~lowmask) << NB) | lo);
+        const uint2* tq = twx + lo;
+        uint32_t x[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) x[k] = sp[(k << BL) + ((k << BL) >> 5)];
+#pragma unroll
+        for (int it = 0; it < NB; ++it) {
+            const int lv = DIF ? NB - 1 - it : it;
+#pragma unroll
+            for (int m = 0; m < (1 << lv); ++m) {
+                const uint2 w = __ldg(tq + (1 << (BL + lv)) + (m << BL));
+#pragma unroll
+                for (int jj = 0; jj < R / (2 << lv); ++jj) {
+                    const int k = m + jj * (2 << lv);
+                    if (DIF) bfly_dif(x[k], x[k + (1 << lv)], w.x, w.y, p, two_p);
+                    else bfly_dit(x[k], x[k + (1 << lv)], w.x, w.y, p, two_p);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) sp[(k << BL) + ((k << BL) >> 5)] = x[k];
+    }
+    __syncthreads();
+}
+
+// bits [LO, HI) in rounds of <= 4 bits (run_segment's partition)
+template <int LO, int HI, bool DIF>
+__device__ __forceinline__ void xct_seg(uint32_t* s, int tile_bits, const uint2* twx, uint32_t p, uint32_t two_p) {
+    constexpr int nbits = HI - LO;
+    if constexpr (nbits > 0) {
+        constexpr int nr = (nbits + 3) / 4;
+        constexpr int nb = nbits / nr + (nbits % nr ? 1 : 0);
+        if constexpr (!DIF) {
+            xct_round<LO, nb, false>(s, tile_bits, twx, p, two_p);
+            xct_seg<LO + nb, HI, false>(s, tile_bits, twx, p, two_p);
+        } else {
+            xct_round<HI - nb, nb, true>(s, tile_bits, twx, p, two_p);
+            xct_seg<LO, HI - nb, true>(s, tile_bits, twx, p, two_p);
+        }
+    }
+}
+
+template <int LGL, bool DIF>
+__device__ __forceinline__ void xct(uint32_t* s, int tile_bits, const uint2* twx, uint32_t p, uint32_t two_p) {
+    constexpr int mid = LGL > 4 ? 4 : LGL;
+    if (!DIF) {
+        xct_seg<0, mid, false>(s, tile_bits, twx, p, two_p);
+        xct_seg<mid, LGL, false>(s, tile_bits, twx, p, two_p);
+    } else {
+        xct_seg<mid, LGL, true>(s, tile_bits, twx, p, two_p);
+        xct_seg<0, mid, true>(s, tile_bits, twx, p, two_p);
+    }
+}
+
+// The x transform of a tile: one out-of-line copy per direction, dispatched on lgL.
+template <bool DIF>
+__device__ __noinline__ void x_transform(uint32_t* s, int lgL, int tile_bits, const uint2* twx,
+                                         uint32_t p, uint32_t two_p) {
+    switch (lgL) {
+        case 1: xct<1, DIF>(s, tile_bits, twx, p, two_p); break;
+        case 2: xct<2, DIF>(s, tile_bits, twx, p, two_p); break;
+        case 3: xct<3, DIF>(s, tile_bits, twx, p, two_p); break;
+        case 4: xct<4, DIF>(s, tile_bits, twx, p, two_p); break;
+        case 5: xct<5, DIF>(s, tile_bits, twx, p, two_p); break;
+        case 6: xct<6, DIF>(s, tile_bits, twx, p, two_p); break;
+        case 7: xct<7, DIF>(s, tile_bits, twx, p, two_p); break;
+        case 8: xct<8, DIF>(s, tile_bits, twx, p, two_p); break;
+        case 9: xct<9, DIF>(s, tile_bits, twx, p, two_p); break;
+        case 10: xct<10, DIF>(s, tile_bits, twx, p, two_p); break;
+        case 11: xct<11, DIF>(s, tile_bits, twx, p, two_p); break;
+        case 12: xct<12, DIF>(s, tile_bits, twx, p, two_p); break;
+        case 13: xct<13, DIF>(s, tile_bits, twx, p, two_p); break;
+        case 14: xct<14, DIF>(s, tile_bits, twx, p, two_p); break;
+        case 15: xct<15, DIF>(s, tile_bits, twx, p, two_p); break;
+        default: __trap();
+    }
+}
+
 struct TwRows {
     const uint2* twx; const uint2* twy; int lgL;
     __device__ __forceinline__ const uint2* table(int bit_lo) const { return bit_lo < lgL ? twx : twy; }
@@ -558,7 +658,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
         }
         __syncthreads();
         const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
-        run_bits<true>(tile, cbits, 0, A.lgL, tw, pc.p, pc.two_p);               // x: DIF, computed rows
+        x_transform<true>(tile, A.lgL, cbits, tw.twx, pc.p, pc.two_p);           // x: DIF, computed rows
         if (prune) {
             // expand in place, highest chunk first: compact e -> rows 2r', 2r'+1
             const uint32_t chunk = 8u * blockDim.x;
@@ -986,7 +1086,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
         __syncthreads();
         const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
         run_bits<true>(t, tile_bits, A.lgL, tile_bits, tw, pc.p, pc.two_p);   // y low: DIF
-        run_bits<false>(t, tile_bits, 0, A.lgL, tw, pc.p, pc.two_p);          // x: DIT
+        x_transform<false>(t, A.lgL, tile_bits, tw.twx, pc.p, pc.two_p);      // x: DIT
     }
     // CRT in place
     for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {

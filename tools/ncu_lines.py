@@ -42,3 +42,21 @@ tot_s = sum(num(d.get(ks)) for d in data)
 print(f"total warp instructions {tot_i:.3e}, stall samples {tot_s:.0f}")
 for d in sorted(data, key=lambda x: -num(x.get(ki)))[:top]:
     print(f"{d['file']}:{d['line']:>5s} inst {num(d.get(ki))/max(tot_i,1):6.1%} stall {num(d.get(ks))/max(tot_s,1):6.1%}  {d['src'].strip()[:80]}")
+
+# optional: aggregate by line ranges, e.g. RANGES="xf:280-470,crt:690-800,out:840-1010"
+import os
+rng = os.environ.get("RANGES")
+if rng:
+    agg = {}
+    for part in rng.split(","):
+        name, span = part.split(":")
+        a, b = (int(v) for v in span.split("-"))
+        for d in data:
+            if d["file"] == "tc_kernels.cuh" and a <= int(d["line"]) <= b:
+                agg.setdefault(name, [0.0, 0.0])
+                agg[name][0] += num(d.get(ki)); agg[name][1] += num(d.get(ks))
+    other_i = tot_i - sum(v[0] for v in agg.values())
+    for k, (i, s) in agg.items():
+        print(f"range {k:8s} inst {i/tot_i:6.1%} stall {s/max(tot_s,1):6.1%}")
+    fld = [d for d in data if d["file"] == "tc_field.cuh"]
+    print(f"tc_field.cuh   inst {sum(num(d.get(ki)) for d in fld)/tot_i:6.1%}")
