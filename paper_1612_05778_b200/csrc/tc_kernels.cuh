@@ -550,6 +550,86 @@ __device__ __noinline__ void x_transform(uint32_t* s, int lgL, int tile_bits, co
     }
 }
 
+// ---------------------------------------------------------------------------
+// Low y levels of a k_low / k_final tile (tile bits [lgL + RB0, lgL + RB0 +
+// NY)) with the round schedule fixed relative to lgL: twiddle offsets are
+// constants (y table: lower element at stage bit b with row bits lo >> lgL
+// uses entry 2^(b - lgL) + (lo >> lgL)); strides are one runtime step.
+// Requires lgL >= 5 (every round above bit 5: linear padded addressing, no
+// lane permutation).
+// ---------------------------------------------------------------------------
+template <int RB, int NB, bool DIF>
+__device__ __forceinline__ void yct_round(uint32_t* s, int tile_bits, int lgL, const uint2* twy,
+                                          uint32_t p, uint32_t two_p) {
+    constexpr int R = 1 << NB;
+    const int bl = lgL + RB;
+    const uint32_t lowmask = (1u << bl) - 1;
+    const uint32_t astep = (1u << bl) + (1u << (bl - 5));
+    const uint32_t ngroups = 1u << (tile_bits - NB);
+    for (uint32_t g = threadIdx.x; g < ngroups; g += blockDim.x) {
+        const uint32_t lo = g & lowmask;
+        uint32_t* sp = s + padi(((g & ~lowmask) << NB) | lo);
+        const uint2* tq = twy + (lo >> lgL);
+        uint32_t x[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) x[k] = sp[k * astep];
+#pragma unroll
+        for (int it = 0; it < NB; ++it) {
+            const int lv = DIF ? NB - 1 - it : it;
+#pragma unroll
+            for (int m = 0; m < (1 << lv); ++m) {
+                const uint2 w = __ldg(tq + (1 << (RB + lv)) + (m << RB));
+#pragma unroll
+                for (int jj = 0; jj < R / (2 << lv); ++jj) {
+                    const int k = m + jj * (2 << lv);
+                    if (DIF) bfly_dif(x[k], x[k + (1 << lv)], w.x, w.y, p, two_p);
+                    else bfly_dit(x[k], x[k + (1 << lv)], w.x, w.y, p, two_p);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) sp[k * astep] = x[k];
+    }
+    __syncthreads();
+}
+
+template <int LO, int HI, bool DIF>
+__device__ __forceinline__ void yct_seg(uint32_t* s, int tile_bits, int lgL, const uint2* twy, uint32_t p,
+                                        uint32_t two_p) {
+    constexpr int nbits = HI - LO;
+    if constexpr (nbits > 0) {
+        constexpr int nr = (nbits + 3) / 4;
+        constexpr int nb = nbits / nr + (nbits % nr ? 1 : 0);
+        if constexpr (!DIF) {
+            yct_round<LO, nb, false>(s, tile_bits, lgL, twy, p, two_p);
+            yct_seg<LO + nb, HI, false>(s, tile_bits, lgL, twy, p, two_p);
+        } else {
+            yct_round<HI - nb, nb, true>(s, tile_bits, lgL, twy, p, two_p);
+            yct_seg<LO, HI - nb, true>(s, tile_bits, lgL, twy, p, two_p);
+        }
+    }
+}
+
+// y levels [lgL + rb0, tile_bits) of a tile; false if the shape has no
+// compile-time schedule (caller runs the generic rounds).
+template <bool DIF>
+__device__ __noinline__ bool y_transform(uint32_t* s, int lgL, int rb0, int tile_bits, const uint2* twy,
+                                         uint32_t p, uint32_t two_p) {
+    const int ny = tile_bits - lgL - rb0;
+    if (lgL < 5 || ny < 0 || ny > 12 || rb0 > 1) return false;
+#define TC_YCASE(R0, N) case (R0) * 16 + (N): yct_seg<R0, R0 + N, DIF>(s, tile_bits, lgL, twy, p, two_p); break;
+    switch (rb0 * 16 + ny) {
+        case 0: case 16: break;
+        TC_YCASE(0, 1) TC_YCASE(0, 2) TC_YCASE(0, 3) TC_YCASE(0, 4) TC_YCASE(0, 5) TC_YCASE(0, 6)
+        TC_YCASE(0, 7) TC_YCASE(0, 8) TC_YCASE(0, 9) TC_YCASE(0, 10) TC_YCASE(0, 11) TC_YCASE(0, 12)
+        TC_YCASE(1, 1) TC_YCASE(1, 2) TC_YCASE(1, 3) TC_YCASE(1, 4) TC_YCASE(1, 5) TC_YCASE(1, 6)
+        TC_YCASE(1, 7) TC_YCASE(1, 8) TC_YCASE(1, 9) TC_YCASE(1, 10) TC_YCASE(1, 11) TC_YCASE(1, 12)
+        default: return false;
+    }
+#undef TC_YCASE
+    return true;
+}
+
 struct TwRows {
     const uint2* twx; const uint2* twy; int lgL;
     __device__ __forceinline__ const uint2* table(int bit_lo) const { return bit_lo < lgL ? twx : twy; }
@@ -682,7 +762,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
                 __syncthreads();
             }
         }
-        run_bits<false>(tile, tile_bits, A.lgL + (prune ? 1 : 0), tile_bits, tw, pc.p, pc.two_p);  // y: DIT
+        if (!y_transform<false>(tile, A.lgL, prune ? 1 : 0, tile_bits, tw.twy, pc.p, pc.two_p))   // y: DIT
+            run_bits<false>(tile, tile_bits, A.lgL + (prune ? 1 : 0), tile_bits, tw, pc.p, pc.two_p);
         uint32_t* g = dst(q);
         if (sharded) tile_store(g, tile, n, XchgIdx{A.sh, blockIdx.x});
         else if (n >= 4) tile_store(g, tile, n, Contig{});
@@ -1085,7 +1166,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
         }
         __syncthreads();
         const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
-        run_bits<true>(t, tile_bits, A.lgL, tile_bits, tw, pc.p, pc.two_p);   // y low: DIF
+        if (!y_transform<true>(t, A.lgL, 0, tile_bits, tw.twy, pc.p, pc.two_p))   // y low: DIF
+            run_bits<true>(t, tile_bits, A.lgL, tile_bits, tw, pc.p, pc.two_p);
         x_transform<false>(t, A.lgL, tile_bits, tw.twx, pc.p, pc.two_p);      // x: DIT
     }
     // CRT in place
