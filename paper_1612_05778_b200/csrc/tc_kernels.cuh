@@ -1204,7 +1204,9 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
     // The last word of a row never generates or propagates, so chains never
     // cross rows; carries out of a row's top word are the mod 2^(32 W32) wrap.
     const int M = A.M, W32 = A.W32;
-    const int64_t total = (int64_t)R * W32;
+    constexpr int kW = 4;                     // consecutive words per thread per round
+    const int Wp = (W32 + kW - 1) / kW * kW;  // row stride of the word loop: a thread never straddles rows
+    const int64_t total = (int64_t)R * Wp;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (threadIdx.x == 0) { s_c1 = 0; s_c2 = 0; s_hi = 0; }
     __syncthreads();
@@ -1232,33 +1234,41 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
         }
         return sum;
     };
-    // M >= 32: word w takes at most one piece from each piece index k = 0..P,
-    // from term j_k = ceil(32(w-k)/M) when M j_k < 32(w-k+1) -- a fixed,
-    // unrolled, divergence-free loop.
-    auto word_sum_wide = [&](int r, int w) -> int64_t {
+    // M >= 32: every word holds at most one term start.  The thread walks the
+    // term starts in words w0-P .. w0+kW-1 (j tracked incrementally from one
+    // division) and adds piece k of the term starting in word u to word u+k;
+    // only limbs reaching the thread's words are loaded.
+    auto word_sums_wide = [&](int r, int w0, int64_t (&acc)[kW]) {
         const uint32_t rowbase = (uint32_t)r << A.lgL;
-        int64_t sum = 0;
+        const int u0 = w0 - P;
+        int j = u0 <= 0 ? 0 : div_m(32 * u0 + M - 1, M, A.minv);     // ceil(32 u0 / M)
 #pragma unroll
-        for (int k = 0; k <= P; ++k) {
-            const int base = 32 * (w - k);
-            if (base < 0) break;
-            const int j = div_m(base + M - 1, M, A.minv);
-            const int bit = M * j;
-            if (bit < base + 32 && j <= L - 2) {
-                const uint32_t e = padi(rowbase + j);
-                const int rr = bit & 31;
-                const uint32_t prv = k > 0 ? sm[(k - 1) * stride + e] : 0u;
-                if (k < P) {
-                    sum += __funnelshift_l(prv, sm[k * stride + e], rr);
-                } else {
-                    sum += (int64_t)(int32_t)__funnelshift_l(prv, (uint32_t)((int32_t)prv >> 31), rr);
-                }
+        for (int t = 0; t < kW; ++t) acc[t] = 0;
+#pragma unroll
+        for (int iu = 0; iu < kW + P; ++iu) {
+            const int u = u0 + iu;
+            const int st = M * j - 32 * u;                            // term j's start inside word u
+            const bool has = u >= 0 && st < 32 && j <= L - 2 && w0 + iu - P < W32;
+            const uint32_t e = padi(rowbase + (uint32_t)j);
+            const int kmin = iu < P ? P - iu : 0;                     // pieces landing in [w0, w0+kW)
+            const int kmax = (kW - 1 + P - iu) < P ? (kW - 1 + P - iu) : P;
+            uint32_t x[P];
+#pragma unroll
+            for (int l = 0; l < P; ++l)
+                x[l] = (has && l >= kmin - 1 && l <= kmax) ? sm[l * stride + e] : 0u;
+            const int rr = st & 31;
+#pragma unroll
+            for (int k = 0; k <= P; ++k) {
+                if (k < kmin || k > kmax) continue;
+                const int t = iu - P + k;
+                if (k == 0) acc[t] += (uint32_t)(x[0] << rr);
+                else if (k < P) acc[t] += __funnelshift_l(x[k - 1], x[k], rr);
+                else acc[t] += (int64_t)(int32_t)__funnelshift_l(x[P - 1], (uint32_t)((int32_t)x[P - 1] >> 31), rr);
             }
+            j += has ? 1 : 0;
         }
-        return sum;
     };
     const bool wide = M >= 32;
-    constexpr int kW = 4;                     // consecutive words per thread per round
     for (int64_t gb = 0; gb < total; gb += (int64_t)blockDim.x * kW) {
         const int64_t g0 = gb + (int64_t)threadIdx.x * kW;
         int rw[kW], ww[kW];
@@ -1266,14 +1276,16 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
         int64_t sum[kW];
         {
             const uint32_t gc = (uint32_t)min(g0, total);
-            int r = (int)(gc / (uint32_t)W32), w = (int)(gc - (uint32_t)r * (uint32_t)W32);
+            const int r = (int)(gc / (uint32_t)Wp), w0 = (int)(gc - (uint32_t)r * (uint32_t)Wp);
+            if (wide && g0 < total) word_sums_wide(r, w0, sum);
 #pragma unroll
             for (int k = 0; k < kW; ++k) {
-                valid[k] = g0 + k < total;
+                const int w = w0 + k;
+                valid[k] = g0 < total && w < W32;
                 rw[k] = r; ww[k] = w;
                 live[k] = valid[k] && w != W32 - 1;     // a row's top word never carries on
-                sum[k] = valid[k] ? (wide ? word_sum_wide(r, w) : word_sum(r, w)) : 0;
-                if (++w == W32) { w = 0; ++r; }
+                if (!wide) sum[k] = valid[k] ? word_sum(r, w) : 0;
+                else if (!valid[k]) sum[k] = 0;
             }
         }
         // hi of the word before each word
