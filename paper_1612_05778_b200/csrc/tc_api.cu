@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <string>
 #include <vector>
+#include <algorithm>
 #include <chrono>
 
 #include "../../include/tc_api.h"
@@ -81,7 +82,8 @@ enum Stage { ST_CONVERT = 0, ST_FWD, ST_MID, ST_INV, ST_OUT, ST_D2H, ST_COUNT };
 struct Ctx {
     int device = 0;
     cudaStream_t st = nullptr;
-    DevBuf in_a, in_b, grids, twx_f, twx_i, twy_f, twy_i, pcs, flags, outbuf, dbg;
+    DevBuf in_a, in_b, grids, twx_f, twx_i, twy_f, twy_i, pcs, flags, outbuf, dbg, nbias;
+    int64_t nb_key[4] = {-1, -1, -1, -1};  // (M, P, L, W32) of nbias
     const uint64_t* a_dev = nullptr; const uint64_t* b_dev = nullptr;
     int64_t da = 0, db = 0; int a_cw = 0, b_cw = 0;
     bool staged = false;
@@ -422,6 +424,27 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
     return TC_OK;
 }
 
+// ConvertOut's bias words: the CRT terms c_ij are stored as c_ij + 2^(32P-1)
+// (unsigned), so k_final adds (-sum_{j <= L-2} 2^(32P-1+Mj)) mod 2^(32 W32)
+// to every row.
+int ensure_nbias(Ctx* c, int M, int P, int64_t L, int W32) {
+    const int64_t key[4] = {M, P, L, W32};
+    if (std::equal(key, key + 4, c->nb_key) && c->nbias.p) return TC_OK;
+    std::vector<uint32_t> b((size_t)W32, 0u);
+    for (int64_t j = 0; j <= L - 2; ++j) {
+        const int64_t bit = 32ll * P - 1 + (int64_t)M * j;
+        if (bit >= 32ll * W32) break;
+        b[(size_t)(bit >> 5)] |= 1u << (bit & 31);
+    }
+    uint64_t carry = 1;                              // two's complement negation
+    for (auto& w : b) { const uint64_t t = (uint64_t)(uint32_t)~w + carry; w = (uint32_t)t; carry = t >> 32; }
+    int rc;
+    if ((rc = c->nbias.ensure(sizeof(uint32_t) * (size_t)W32))) return rc;
+    CK(cudaMemcpyAsync(c->nbias.p, b.data(), sizeof(uint32_t) * (size_t)W32, cudaMemcpyHostToDevice, c->st));
+    std::copy(key, key + 4, c->nb_key);
+    return TC_OK;
+}
+
 int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows, int M, int W32,
                  uint32_t* out, const CrtConst& cc, bool dump, const ShardArgs& sh,
                  int64_t x0 = 0, int64_t nx = -1) {
@@ -435,6 +458,11 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
     A.pcs = c->pcs.as<PrimeC>();
     A.rows_out = rows; A.M = M; A.minv = (uint32_t)(0xffffffffu / (uint32_t)M); A.W32 = W32;
     A.out = out; A.err = c->flags.as<int>();
+    if (!dump && W32 > 0) {
+        int rc = ensure_nbias(c, M, G.P, G.L, W32);
+        if (rc) return rc;
+        A.nbias = c->nbias.as<uint32_t>();
+    }
     const uint32_t n = 1u << (G.lgL + G.yl);
     const size_t smem = (size_t)G.P * padded_words(n) * 4;
     const unsigned grid = (unsigned)(sh.world > 1 ? sh.Tl : (nx >= 0 ? nx : G.S / n));
@@ -580,7 +608,7 @@ int tc_ctx_destroy(void* ctx) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->st);
     for (DevBuf* b : {&c->in_a, &c->in_b, &c->grids, &c->twx_f, &c->twx_i, &c->twy_f, &c->twy_i,
-                      &c->pcs, &c->flags, &c->outbuf, &c->dbg}) b->release();
+                      &c->pcs, &c->flags, &c->outbuf, &c->dbg, &c->nbias}) b->release();
     for (auto& ev : c->ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : c->user_ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : c->xev) if (ev) cudaEventDestroy(ev);

@@ -1123,6 +1123,7 @@ struct FinalArgs {
     const PrimeC* pcs;
     int64_t rows_out; int M; uint32_t minv; int W32;
     uint32_t* out;                 // rows_out x W32 (or rows_out x L x P for DUMP)
+    const uint32_t* nbias;         // W32 words of (-sum_j 2^(32P-1+Mj)) mod 2^(32 W32), see ConvertOut
     int* err;                      // err[2]: first bad flat index i*L + j
     // unsharded: CTA x0 + blockIdx.x handles tile bitrev(x) over lgT bits, so
     // a range of CTAs finishes a 2-D block of natural-order product rows
@@ -1134,9 +1135,9 @@ struct FinalArgs {
 template <int P, bool DUMP, int NT>
 __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_final(FinalArgs A, const __grid_constant__ CrtConst cc) {
     extern __shared__ __align__(16) uint32_t sm[];
-    __shared__ uint32_t wtf[32], warp_tf1[32], wcin1[32], wcin2[32];
+    __shared__ uint32_t wtf[32], wcin1[32];
     __shared__ int64_t whi[32];
-    __shared__ uint32_t s_c1, s_c2;
+    __shared__ uint32_t s_c1;
     __shared__ int64_t s_hi;
     __shared__ int s_any;
     const int R = 1 << A.yl;
@@ -1188,49 +1189,45 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
             }
         }
 #pragma unroll
-        for (int l = 0; l < P; ++l) sm[l * stride + padi(e)] = x[l];
+        for (int l = 0; l < P - 1; ++l) sm[l * stride + padi(e)] = x[l];
+        sm[(P - 1) * stride + padi(e)] = x[P - 1] ^ 0x80000000u;     // biased: c_ij + 2^(32P-1) >= 0
     }
     if (DUMP) return;
     __syncthreads();
 
-    // ConvertOut over the tile's rows, words flattened as gi = r * W32 + w.
-    // value(row) = sum_w lo_w 2^(32w) + sum_w hi_{w-1} 2^(32w), hi small signed
-    //            = A + B+ - B-  (B+ / B- the positive / negative hi parts):
-    // chain 1 adds B+ (carries), chain 2 subtracts B- (borrows); each is a
-    // binary generate/propagate chain resolved per warp by one 64-bit add of
-    // ballot masks and across warps by warp 0's ballot scan of per-warp
-    // transfer bits (chain 2's per-warp masks are kept for both chain-1
-    // carry-ins, so one pass of warp 0 resolves both chains).
-    // The last word of a row never generates or propagates, so chains never
-    // cross rows; carries out of a row's top word are the mod 2^(32 W32) wrap.
+    // ConvertOut over the tile's rows, kW words per thread (rows padded to a
+    // multiple of kW words).  Terms are stored biased (c_ij + 2^(32P-1), an
+    // unsigned P-limb number) so every shifted piece is unsigned; the bias
+    // sum_j 2^(32P-1+Mj) is removed by adding the per-word constants nbias =
+    // its negation mod 2^(32 W32).  S_w = sum of w's pieces + nbias_w >= 0, so
+    // value(row) = sum_w S_w 2^(32w) (mod 2^(32 W32)) is resolved by ONE binary
+    // carry chain over t_w = lo(S_w) + hi(S_{w-1}): generate t_w >= 2^32,
+    // propagate t_w == 2^32 - 1, per thread over its kW words, per warp by a
+    // 64-bit add of ballot masks, across warps by warp 0's ballot scan.  A
+    // row's top word never generates or propagates (the mod 2^(32 W32) wrap),
+    // so chains never cross rows.
     const int M = A.M, W32 = A.W32;
-    constexpr int kW = 4;                     // consecutive words per thread per round
-    const int Wp = (W32 + kW - 1) / kW * kW;  // row stride of the word loop: a thread never straddles rows
+    constexpr int kW = 4;
+    const int Wp = (W32 + kW - 1) / kW * kW;
     const int64_t total = (int64_t)R * Wp;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    if (threadIdx.x == 0) { s_c1 = 0; s_c2 = 0; s_hi = 0; }
+    if (threadIdx.x == 0) { s_c1 = 0; s_hi = 0; }
     __syncthreads();
-    // S_w of output word w of tile row r: the 32-bit pieces of every shifted
-    // term c_rj 2^(Mj) overlapping w (unsigned pieces, signed top piece).
-    auto word_sum = [&](int r, int w) -> int64_t {
+    // M < 32: S_w gathers every piece of every term overlapping word w.
+    auto word_sum = [&](int r, int w) -> uint64_t {
         const int lo_n = 32 * (w - P);
         const int jf = lo_n <= 0 ? 0 : div_m(lo_n + M - 1, M, A.minv);
         const int jl = min(L - 2, div_m(32 * w + 31, M, A.minv));
         const uint32_t rowbase = (uint32_t)r << A.lgL;
-        int64_t sum = 0;
+        uint64_t sum = 0;
         int bit = M * jf;
         for (int j = jf; j <= jl; ++j, bit += M) {
             const int k = w - (bit >> 5);              // piece index 0..P of term j
             const int rr = bit & 31;
             const uint32_t e = padi(rowbase + j);
             const uint32_t prv = k > 0 ? sm[(k - 1) * stride + e] : 0u;
-            if (k < P) {
-                const uint32_t cur = sm[k * stride + e];
-                sum += __funnelshift_l(prv, cur, rr);             // (cur:prv) << rr, high word
-            } else {                                               // signed top piece
-                const uint32_t sgn = (uint32_t)((int32_t)prv >> 31);
-                sum += (int64_t)(int32_t)__funnelshift_l(prv, sgn, rr);
-            }
+            const uint32_t cur = k < P ? sm[k * stride + e] : 0u;
+            sum += __funnelshift_l(prv, cur, rr);       // (cur:prv) << rr, high word
         }
         return sum;
     };
@@ -1238,7 +1235,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
     // term starts in words w0-P .. w0+kW-1 (j tracked incrementally from one
     // division) and adds piece k of the term starting in word u to word u+k;
     // only limbs reaching the thread's words are loaded.
-    auto word_sums_wide = [&](int r, int w0, int64_t (&acc)[kW]) {
+    auto word_sums_wide = [&](int r, int w0, uint64_t (&acc)[kW]) {
         const uint32_t rowbase = (uint32_t)r << A.lgL;
         const int u0 = w0 - P;
         int j = u0 <= 0 ? 0 : div_m(32 * u0 + M - 1, M, A.minv);     // ceil(32 u0 / M)
@@ -1248,7 +1245,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
         for (int iu = 0; iu < kW + P; ++iu) {
             const int u = u0 + iu;
             const int st = M * j - 32 * u;                            // term j's start inside word u
-            const bool has = u >= 0 && st < 32 && j <= L - 2 && w0 + iu - P < W32;
+            const bool has = u >= 0 && st < 32 && j <= L - 2 && u < W32;
             const uint32_t e = padi(rowbase + (uint32_t)j);
             const int kmin = iu < P ? P - iu : 0;                     // pieces landing in [w0, w0+kW)
             const int kmax = (kW - 1 + P - iu) < P ? (kW - 1 + P - iu) : P;
@@ -1261,9 +1258,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
             for (int k = 0; k <= P; ++k) {
                 if (k < kmin || k > kmax) continue;
                 const int t = iu - P + k;
-                if (k == 0) acc[t] += (uint32_t)(x[0] << rr);
-                else if (k < P) acc[t] += __funnelshift_l(x[k - 1], x[k], rr);
-                else acc[t] += (int64_t)(int32_t)__funnelshift_l(x[P - 1], (uint32_t)((int32_t)x[P - 1] >> 31), rr);
+                const uint32_t lo = k > 0 ? x[k - 1] : 0u, hi = k < P ? x[k] : 0u;
+                acc[t] += __funnelshift_l(lo, hi, rr);
             }
             j += has ? 1 : 0;
         }
@@ -1271,99 +1267,58 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
     const bool wide = M >= 32;
     for (int64_t gb = 0; gb < total; gb += (int64_t)blockDim.x * kW) {
         const int64_t g0 = gb + (int64_t)threadIdx.x * kW;
-        int rw[kW], ww[kW];
+        const uint32_t gc = (uint32_t)min(g0, total);
+        const int r = (int)(gc / (uint32_t)Wp), w0 = (int)(gc - (uint32_t)r * (uint32_t)Wp);
+        uint64_t sum[kW];
         bool valid[kW], live[kW];
-        int64_t sum[kW];
-        {
-            const uint32_t gc = (uint32_t)min(g0, total);
-            const int r = (int)(gc / (uint32_t)Wp), w0 = (int)(gc - (uint32_t)r * (uint32_t)Wp);
-            if (wide && g0 < total) word_sums_wide(r, w0, sum);
-#pragma unroll
-            for (int k = 0; k < kW; ++k) {
-                const int w = w0 + k;
-                valid[k] = g0 < total && w < W32;
-                rw[k] = r; ww[k] = w;
-                live[k] = valid[k] && w != W32 - 1;     // a row's top word never carries on
-                if (!wide) sum[k] = valid[k] ? word_sum(r, w) : 0;
-                else if (!valid[k]) sum[k] = 0;
-            }
-        }
-        // hi of the word before each word
-        const int64_t hlast = sum[kW - 1] >> 32;
-        int64_t hprev0 = __shfl_up_sync(0xffffffffu, hlast, 1);
-        if (lane == 31) whi[warp] = hlast;
-        __syncthreads();
-        if (lane == 0) hprev0 = warp > 0 ? whi[warp - 1] : s_hi;
-        uint32_t w1[kW], bm[kW];
-        bool g1[kW], p1[kW];
+        if (wide && g0 < total) word_sums_wide(r, w0, sum);
 #pragma unroll
         for (int k = 0; k < kW; ++k) {
-            const int64_t bb = ww[k] == 0 ? 0 : (k == 0 ? hprev0 : (sum[k - 1] >> 32));
-            const uint32_t bp = bb > 0 ? (uint32_t)bb : 0u;
-            bm[k] = bb < 0 ? (uint32_t)(-bb) : 0u;
-            const uint64_t t1 = (uint64_t)(uint32_t)sum[k] + bp;
-            w1[k] = (uint32_t)t1;
-            g1[k] = live[k] && (t1 >> 32);
-            p1[k] = live[k] && w1[k] == 0xffffffffu;
+            const int w = w0 + k;
+            valid[k] = g0 < total && w < W32;
+            live[k] = valid[k] && w != W32 - 1;     // a row's top word never carries on
+            if (!wide) sum[k] = valid[k] ? word_sum(r, w) : 0;
+            if (valid[k]) sum[k] += __ldg(A.nbias + w);
+            else sum[k] = 0;
         }
-        // chain 1 (carries of lo + B+): thread block transfer, then warp ballot add
+        // hi of the word before each word
+        const uint64_t hlast = sum[kW - 1] >> 32;
+        uint64_t hprev0 = __shfl_up_sync(0xffffffffu, hlast, 1);
+        if (lane == 31) whi[warp] = (int64_t)hlast;
+        __syncthreads();
+        if (lane == 0) hprev0 = warp > 0 ? (uint64_t)whi[warp - 1] : (uint64_t)s_hi;
+        uint32_t tw[kW];
+        bool gg[kW], pp[kW];
+#pragma unroll
+        for (int k = 0; k < kW; ++k) {
+            const uint64_t hb = w0 + k == 0 ? 0 : (k == 0 ? hprev0 : (sum[k - 1] >> 32));
+            const uint64_t t = (sum[k] & 0xffffffffull) + hb;
+            tw[k] = (uint32_t)t;
+            gg[k] = live[k] && (t >> 32) != 0;
+            pp[k] = live[k] && tw[k] == 0xffffffffu;
+        }
         uint32_t c0 = 0, c1 = 1;
 #pragma unroll
-        for (int k = 0; k < kW; ++k) { c0 = g1[k] | (p1[k] & c0); c1 = g1[k] | (p1[k] & c1); }
+        for (int k = 0; k < kW; ++k) { c0 = gg[k] | (pp[k] & c0); c1 = gg[k] | (pp[k] & c1); }
         const unsigned G1 = __ballot_sync(0xffffffffu, c0);
         const unsigned P1 = __ballot_sync(0xffffffffu, c1 & !c0);
         const uint64_t A1 = (uint64_t)(G1 | P1), B1 = (uint64_t)G1;
-        uint32_t tf = (uint32_t)((A1 + B1) >> 32) | ((uint32_t)((A1 + B1 + 1) >> 32) << 1);
-        // chain 2 (borrows of - B-), for both warp carry-ins of chain 1
-        uint32_t w1v[2][kW];
-        uint64_t A2[2], B2[2];
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-            uint32_t c = (uint32_t)(((A1 + B1 + v) ^ A1 ^ B1) >> lane) & 1u;   // carry into this thread
-            uint32_t b0 = 0, b1 = 1;
-#pragma unroll
-            for (int k = 0; k < kW; ++k) {
-                w1v[v][k] = w1[k] + c;
-                c = g1[k] | (p1[k] & c);
-                const uint32_t g2 = live[k] && w1v[v][k] < bm[k];
-                const uint32_t p2 = live[k] && w1v[v][k] == bm[k];
-                b0 = g2 | (p2 & b0); b1 = g2 | (p2 & b1);
-            }
-            const unsigned G2 = __ballot_sync(0xffffffffu, b0);
-            const unsigned P2 = __ballot_sync(0xffffffffu, b1 & !b0);
-            A2[v] = (uint64_t)(G2 | P2); B2[v] = (uint64_t)G2;
-            tf |= ((uint32_t)((A2[v] + B2[v]) >> 32) | ((uint32_t)((A2[v] + B2[v] + 1) >> 32) << 1)) << (2 + 2 * v);
-        }
-        if (lane == 0) wtf[warp] = tf;
+        if (lane == 0) wtf[warp] = (uint32_t)((A1 + B1) >> 32) | ((uint32_t)((A1 + B1 + 1) >> 32) << 1);
         __syncthreads();
         if (warp == 0) {
-            const uint32_t t = lane < nw ? wtf[lane] : 0u;
-            warp_tf1[lane] = t & 3u;
-            __syncwarp();
-            warp_carry_scan(warp_tf1, wcin1, &s_c1, nw, lane);
-            __syncwarp();
-            const uint32_t cc = lane < nw ? wcin1[lane] : 0u;
-            warp_tf1[lane] = (t >> (2 + 2 * cc)) & 3u;
-            __syncwarp();
-            warp_carry_scan(warp_tf1, wcin2, &s_c2, nw, lane);
+            warp_carry_scan(wtf, wcin1, &s_c1, nw, lane);
             if (lane == 0) s_hi = whi[nw - 1];
         }
         __syncthreads();
-        const bool cv = wcin1[warp] != 0;            // selects, not indexing: keeps arrays in registers
-        const uint64_t A2c = cv ? A2[1] : A2[0], B2c = cv ? B2[1] : B2[0];
-        uint32_t bin = (uint32_t)(((A2c + B2c + wcin2[warp]) ^ A2c ^ B2c) >> lane) & 1u;
+        uint32_t c = (uint32_t)(((A1 + B1 + wcin1[warp]) ^ A1 ^ B1) >> lane) & 1u;
+        const uint32_t prow = bitrev(pos0 + (uint32_t)r, A.lgS);
+        uint32_t* orow = sharded ? A.out + ((int64_t)blockIdx.x * R + r) * W32
+                                 : A.out + (int64_t)prow * W32;
+        const bool store = sharded || prow < A.rows_out;
 #pragma unroll
         for (int k = 0; k < kW; ++k) {
-            const uint32_t x = cv ? w1v[1][k] : w1v[0][k];
-            if (valid[k]) {
-                const uint32_t prow = bitrev(pos0 + rw[k], A.lgS);
-                if (sharded)   // compact rows in position order; unshard() permutes
-                    A.out[((int64_t)blockIdx.x * R + rw[k]) * W32 + ww[k]] = x - bm[k] - bin;
-                else if (prow < A.rows_out) A.out[(int64_t)prow * W32 + ww[k]] = x - bm[k] - bin;
-            }
-            const uint32_t g2 = live[k] && x < bm[k];
-            const uint32_t p2 = live[k] && x == bm[k];
-            bin = g2 | (p2 & bin);
+            if (valid[k] && store) orow[w0 + k] = tw[k] + c;    // sharded: compact rows in position order
+            c = gg[k] | (pp[k] & c);
         }
     }
 }
