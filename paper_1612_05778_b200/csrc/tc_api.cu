@@ -216,6 +216,11 @@ int make_crt_const(const tc_plan_t* pl, int64_t dmin, CrtConst* cc) {
     const int P = pl->P;
     for (int k = 0; k < P; ++k) {
         cc->p[k] = pl->p[k];
+        cc->halfp[k] = (pl->p[k] - 1) / 2;
+        for (int m = 0; m < k; ++m) {
+            const uint32_t need = (pl->p[m] - 1) / 2;
+            cc->cadd[m][k] = (uint32_t)((need + pl->p[k] - 1) / pl->p[k] * (uint64_t)pl->p[k]);
+        }
         for (int m = 0; m < k; ++m) {
             uint32_t v = inv_mod(pl->p[m] % pl->p[k], pl->p[k]);
             cc->inv[m][k] = v;

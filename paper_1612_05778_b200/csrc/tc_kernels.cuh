@@ -1035,54 +1035,56 @@ struct CrtConst {
     uint32_t inv_sh[kMaxPrimes][kMaxPrimes];
     uint32_t prod[kMaxPrimes];                // prod p_k, P limbs
     uint32_t half[kMaxPrimes];                // (prod - 1) / 2
+    uint32_t halfp[kMaxPrimes];               // (p_k - 1) / 2
+    uint32_t cadd[kMaxPrimes][kMaxPrimes];    // least multiple of p_k >= (p_m - 1) / 2, m < k
     uint32_t bound[kMaxPrimes];               // max |c_ij| admitted
 };
 
+// Garner with balanced digits: v_k in (-p_k/2, p_k/2] from
+//   t = r_k;  t = (t + c_mk - v_m) * (p_m^{-1} mod p_k)  for m < k  (Shoup, lazy [0, 2p))
+// with c_mk the least multiple of p_k >= (p_m - 1)/2: 0 <= t + c_mk - v_m <
+// 3 p_k + p_m < 2^32 for primes < 2^30, so no fix-ups between steps;
+// then x = v_0 + p_0 (v_1 + p_1 (v_2 + ...)) by signed Horner lies in the
+// symmetric range |x| <= (prod - 1)/2 directly: the symmetric lift of
+// tc/_kernels.py:258-313 without a comparison with prod/2.  r[0] must be
+// canonical, r[k > 0] in [0, 2p_k).  Returns |x| > bound.
 template <int P>
 __device__ __forceinline__ bool crt_term(const uint32_t (&r)[P], const CrtConst& cc, uint32_t (&x)[P]) {
-    uint32_t v[P];
+    int32_t v[P];
 #pragma unroll
     for (int k = 0; k < P; ++k) {
         const uint32_t p = cc.p[k];
         uint32_t t = r[k];
 #pragma unroll
-        for (int m = 0; m < k; ++m) {
-            uint32_t vm = v[m];
-            vm = vm >= p ? vm - p : vm;
-            uint32_t diff = t >= vm ? t - vm : t + p - vm;
-            t = shoup_mul(diff, cc.inv[m][k], cc.inv_sh[m][k], p);
-            t = t >= p ? t - p : t;
-        }
-        v[k] = t;
+        for (int m = 0; m < k; ++m) t = shoup_mul(t + cc.cadd[m][k] - (uint32_t)v[m], cc.inv[m][k], cc.inv_sh[m][k], p);
+        if (k > 0) t = t >= p ? t - p : t;
+        v[k] = t > cc.halfp[k] ? (int32_t)(t - p) : (int32_t)t;
     }
-#pragma unroll
-    for (int l = 0; l < P; ++l) x[l] = 0;
-    x[0] = v[P - 1];
+    // Horner, top digit first; after step k the value has P-k limbs, top limb signed
+    x[0] = (uint32_t)v[P - 1];
 #pragma unroll
     for (int k = P - 2; k >= 0; --k) {
-        uint64_t carry = v[k];
+        const int n = P - 1 - k;                  // limbs so far
+        const uint32_t p = cc.p[k];
+        int64_t carry = v[k];
 #pragma unroll
-        for (int l = 0; l < P - 1 - k; ++l) {
-            uint64_t t = (uint64_t)x[l] * cc.p[k] + carry;
+        for (int l = 0; l < n; ++l) {
+            const int64_t prod = l == n - 1 ? (int64_t)(int32_t)x[l] * (int64_t)p
+                                            : (int64_t)((uint64_t)x[l] * p);
+            const int64_t t = prod + carry;
             x[l] = (uint32_t)t;
             carry = t >> 32;
         }
-        x[P - 1 - k] = (uint32_t)carry;
+        x[n] = (uint32_t)carry;
     }
-    int gt = 0;
-#pragma unroll
-    for (int l = P - 1; l >= 0; --l)
-        if (gt == 0 && x[l] != cc.half[l]) gt = x[l] > cc.half[l] ? 1 : -1;
+    // |x| <= bound: decided by the top limb unless it reaches the bound's top limb
+    const int32_t top = (int32_t)x[P - 1], bt = (int32_t)cc.bound[P - 1];
+    if (top >= -bt && top < bt) return false;
     uint32_t mag[P];
-    if (gt > 0) {
-        uint64_t br = 0, br2 = 0;
+    if (top < 0) {
+        uint64_t c = 1;
 #pragma unroll
-        for (int l = 0; l < P; ++l) {
-            uint64_t d1 = (uint64_t)cc.prod[l] - x[l] - br;
-            mag[l] = (uint32_t)d1; br = (d1 >> 63) & 1;
-            uint64_t d2 = (uint64_t)x[l] - cc.prod[l] - br2;
-            x[l] = (uint32_t)d2; br2 = (d2 >> 63) & 1;
-        }
+        for (int l = 0; l < P; ++l) { const uint64_t t = (uint64_t)(uint32_t)~x[l] + c; mag[l] = (uint32_t)t; c = t >> 32; }
     } else {
 #pragma unroll
         for (int l = 0; l < P; ++l) mag[l] = x[l];
@@ -1174,8 +1176,9 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
     // CRT in place
     for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
         uint32_t r[P], x[P];
+        r[0] = canon(sm[padi(e)], cc.p[0]);
 #pragma unroll
-        for (int q = 0; q < P; ++q) r[q] = canon(sm[q * stride + padi(e)], cc.p[q]);
+        for (int q = 1; q < P; ++q) r[q] = reduce_2p(sm[q * stride + padi(e)], 2 * cc.p[q]);
         if (A.inject >= 0 && (int64_t)bitrev(pos0 + (e >> A.lgL), A.lgS) * L + (e & (L - 1)) == A.inject)
             r[0] = r[0] ? r[0] - 1 : cc.p[0] - 1;     // fault injection (tests of the bound check)
         const bool bad = crt_term<P>(r, cc, x);
