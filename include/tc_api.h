@@ -89,7 +89,9 @@ int tc_ctx_destroy(void* ctx);
 /* Copy (or, with on_device != 0, adopt) both operands and reduce their widths
  * on the device.  Replaces the Python-int scans of tc/params.py:290-293 and
  * tc/zpoly.py:103-114.  Device pointers must stay valid until tc_execute
- * returns. */
+ * returns.  info != NULL reads the widths back (a blocking round trip, for
+ * planning); info == NULL leaves them on the device (a caller re-running a
+ * plan it already made for these shapes). */
 int tc_stage_inputs(void* ctx,
                     const uint64_t* a, int64_t da, int32_t a_cw,
                     const uint64_t* b, int64_t db, int32_t b_cw,

@@ -84,6 +84,9 @@ struct Ctx {
     cudaStream_t st = nullptr;
     DevBuf in_a, in_b, grids, twx_f, twx_i, twy_f, twy_i, pcs, flags, outbuf, dbg, nbias;
     int64_t nb_key[4] = {-1, -1, -1, -1};  // (M, P, L, W32) of nbias
+    std::vector<uint32_t> pcs_key; int64_t pcs_S = -1;   // primes and S of pcs
+    cudaGraphExec_t gexec = nullptr;                     // captured product pipeline (run_pipeline)
+    std::vector<int64_t> gkey; int64_t glaunches = 0;
     const uint64_t* a_dev = nullptr; const uint64_t* b_dev = nullptr;
     int64_t da = 0, db = 0; int a_cw = 0, b_cw = 0;
     bool staged = false;
@@ -333,13 +336,13 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     // a tile too large for two CTAs per SM gets 32 warps in one CTA
     const int lt = env_int("TC_LOW_THREADS", 0);
     if (smem > 112 * 1024 || lt >= 1024) {
-        CK(cudaFuncSetAttribute(k_low<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(ensure_smem((const void*)k_low<1024>, smem));
         k_low<1024><<<(unsigned)ctas, 1024, smem, c->st>>>(a);
     } else if (lt == 256 || lt == 0) {            // 256 threads: measured faster (C2 0.268 -> 0.228 ms)
-        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_low<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(ensure_smem((const void*)k_low<256>, smem));
         k_low<256><<<(unsigned)ctas, 256, smem, c->st>>>(a);
     } else {
-        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_low<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(ensure_smem((const void*)k_low<512>, smem));
         k_low<512><<<(unsigned)ctas, 512, smem, c->st>>>(a);
     }
     c->launches++;
@@ -351,7 +354,7 @@ template <int NT, int U, int MODE>
 cudaError_t launch_high_ct_mode(const HighArgs& A, dim3 grid, uint32_t n, cudaStream_t st) {
     const size_t smem = (size_t)ct_tw_offset_words(n) * 4 + (MODE == MODE_MID ? 2 : 1) * ((size_t)8 << U);
     cudaError_t e = cudaSuccess;
-    if (smem > 48 * 1024) e = cudaFuncSetAttribute(k_high_ct<MODE, NT, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = ensure_smem((const void*)k_high_ct<MODE, NT, U>, smem);
     if (e != cudaSuccess) return e;
     k_high_ct<MODE, NT, U><<<grid, NT, smem, st>>>(A);
     return cudaGetLastError();
@@ -397,30 +400,30 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
         if (nth <= 64) {
             k_high<MODE_FWD, 64><<<grid, 64, smem, c->st>>>(A);
         } else if (nth <= 256) {
-            if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_FWD, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CK(ensure_smem((const void*)k_high<MODE_FWD, 256>, smem));
             k_high<MODE_FWD, 256><<<grid, 256, smem, c->st>>>(A);
         } else {
-            if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_FWD, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CK(ensure_smem((const void*)k_high<MODE_FWD, 512>, smem));
             k_high<MODE_FWD, 512><<<grid, 512, smem, c->st>>>(A);
         }
     } else if (mode == MODE_INV) {
         if (nth <= 64) {
             k_high<MODE_INV, 64><<<grid, 64, smem, c->st>>>(A);
         } else if (nth <= 256) {
-            if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_INV, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CK(ensure_smem((const void*)k_high<MODE_INV, 256>, smem));
             k_high<MODE_INV, 256><<<grid, 256, smem, c->st>>>(A);
         } else {
-            if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_INV, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CK(ensure_smem((const void*)k_high<MODE_INV, 512>, smem));
             k_high<MODE_INV, 512><<<grid, 512, smem, c->st>>>(A);
         }
     } else {
         if (nth <= 64) {
             k_high<MODE_MID, 64><<<grid, 64, smem, c->st>>>(A);
         } else if (nth <= 256) {
-            if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_MID, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CK(ensure_smem((const void*)k_high<MODE_MID, 256>, smem));
             k_high<MODE_MID, 256><<<grid, 256, smem, c->st>>>(A);
         } else {
-            if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_high<MODE_MID, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CK(ensure_smem((const void*)k_high<MODE_MID, 512>, smem));
             k_high<MODE_MID, 512><<<grid, 512, smem, c->st>>>(A);
         }
     }
@@ -511,32 +514,35 @@ int make_shard(const Geometry& G, int rank, int world, ShardArgs& sh) {
 }
 
 // Per-plan device state shared by every phase: twiddles, prime constants.
+// Per-prime constants on the device, uploaded when the primes or S change.
+int ensure_pcs(Ctx* c, const tc_plan_t* pl, int64_t S) {
+    std::vector<uint32_t> key(pl->p, pl->p + pl->P);
+    if (key == c->pcs_key && c->pcs_S == S) return TC_OK;
+    std::vector<PrimeC> pcs(pl->P);
+    for (int q = 0; q < pl->P; ++q) pcs[q] = make_prime_const(pl->p[q], S);
+    int rc;
+    if ((rc = c->pcs.ensure(sizeof(PrimeC) * pl->P))) return rc;
+    CK(cudaMemcpyAsync(c->pcs.p, pcs.data(), sizeof(PrimeC) * pl->P, cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));      // pageable source: complete before it goes out of scope
+    c->pcs_key = key; c->pcs_S = S;
+    return TC_OK;
+}
+
 int prepare(Ctx* c, const tc_plan_t* pl, Geometry& G, bool reset_flags, int world = 1) {
     int rc;
     if ((rc = make_geometry(pl, G, world))) return rc;
     if ((rc = ensure_twiddles(c, pl))) return rc;
-    std::vector<PrimeC> pcs(G.P);
-    for (int q = 0; q < G.P; ++q) pcs[q] = make_prime_const(pl->p[q], G.S);
-    if ((rc = c->pcs.ensure(sizeof(PrimeC) * G.P))) return rc;
-    CK(cudaMemcpyAsync(c->pcs.p, pcs.data(), sizeof(PrimeC) * G.P, cudaMemcpyHostToDevice, c->st));
+    if ((rc = ensure_pcs(c, pl, G.S))) return rc;
     if ((rc = c->flags.ensure(64))) return rc;
     if (reset_flags) CK(cudaMemsetAsync(c->flags.p, 0x7f, 64, c->st));
     return TC_OK;
 }
 
-int run_pipeline(Ctx* c, const tc_plan_t* pl, int a_bits, int b_bits, int64_t rows, int W32,
-                 uint32_t* out, bool dump, const CrtConst& cc) {
+// The stream work of one product (flags reset, stage events, all kernels).
+int enqueue_pipeline(Ctx* c, const tc_plan_t* pl, const Geometry& G, int a_bits, int b_bits, int64_t rows,
+                     int W32, uint32_t* out, bool dump, const CrtConst& cc, bool ev) {
     int rc;
-    Geometry G;
     const ShardArgs one = single_gpu();
-    if ((rc = make_geometry(pl, G))) return rc;
-    if ((rc = ensure_twiddles(c, pl))) return rc;
-    if ((rc = c->grids.ensure((size_t)2 * G.P * G.S * 4))) return rc;
-    std::vector<PrimeC> pcs(G.P);
-    for (int q = 0; q < G.P; ++q) pcs[q] = make_prime_const(pl->p[q], G.S);
-    if ((rc = c->pcs.ensure(sizeof(PrimeC) * G.P))) return rc;
-    CK(cudaMemcpyAsync(c->pcs.p, pcs.data(), sizeof(PrimeC) * G.P, cudaMemcpyHostToDevice, c->st));
-    if ((rc = c->flags.ensure(64))) return rc;
     CK(cudaMemsetAsync(c->flags.p, 0x7f, 64, c->st));
 
     uint32_t* GA = c->grids.as<uint32_t>();
@@ -544,29 +550,79 @@ int run_pipeline(Ctx* c, const tc_plan_t* pl, int a_bits, int b_bits, int64_t ro
     const int nh = (int)G.high.size();
     int64_t l0 = c->launches;
 
-    CK(cudaEventRecord(c->ev[0], c->st));
+    if (ev) CK(cudaEventRecord(c->ev[0], c->st));
     if ((rc = launch_low(c, G, pl, c->a_dev, c->da, c->a_cw, a_bits > pl->N, GA, one))) return rc;
     if ((rc = launch_low(c, G, pl, c->b_dev, c->db, c->b_cw, b_bits > pl->N, GB, one))) return rc;
     c->stage_launches[0] = c->launches - l0; l0 = c->launches;
-    CK(cudaEventRecord(c->ev[1], c->st));
+    if (ev) CK(cudaEventRecord(c->ev[1], c->st));
     for (int i = 0; i < nh; ++i)
         if ((rc = launch_high(c, MODE_FWD, G, GA, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
     for (int i = 0; i + 1 < nh; ++i)
         if ((rc = launch_high(c, MODE_FWD, G, GB, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
     c->stage_launches[1] = c->launches - l0; l0 = c->launches;
-    CK(cudaEventRecord(c->ev[2], c->st));
+    if (ev) CK(cudaEventRecord(c->ev[2], c->st));
     if (nh > 0) rc = launch_high(c, MODE_MID, G, GB, GA, G.high[nh - 1].first, G.high[nh - 1].second, one);
     else rc = launch_high(c, MODE_MID, G, GB, GA, G.lgS, 0, one);
     if (rc) return rc;
     c->stage_launches[2] = c->launches - l0; l0 = c->launches;
-    CK(cudaEventRecord(c->ev[3], c->st));
+    if (ev) CK(cudaEventRecord(c->ev[3], c->st));
     for (int i = nh - 2; i >= 0; --i)
         if ((rc = launch_high(c, MODE_INV, G, GB, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
     c->stage_launches[3] = c->launches - l0; l0 = c->launches;
-    CK(cudaEventRecord(c->ev[4], c->st));
+    if (ev) CK(cudaEventRecord(c->ev[4], c->st));
     if ((rc = launch_final(c, G, GB, rows, (int)pl->M, W32, out, cc, dump, one))) return rc;
     c->stage_launches[4] = c->launches - l0;
-    CK(cudaEventRecord(c->ev[5], c->st));
+    if (ev) CK(cudaEventRecord(c->ev[5], c->st));
+    return TC_OK;
+}
+
+// Host preparation (uploads happen here, outside any capture), then the
+// stream work -- captured once per (plan, buffers, shapes) into a CUDA graph
+// and replayed: one cudaGraphLaunch instead of the per-kernel launch path.
+// TC_GRAPH=0 enqueues directly.
+int run_pipeline(Ctx* c, const tc_plan_t* pl, int a_bits, int b_bits, int64_t rows, int W32,
+                 uint32_t* out, bool dump, const CrtConst& cc, bool stage_events) {
+    int rc;
+    Geometry G;
+    if ((rc = make_geometry(pl, G))) return rc;
+    if ((rc = ensure_twiddles(c, pl))) return rc;
+    if ((rc = c->grids.ensure((size_t)2 * G.P * G.S * 4))) return rc;
+    if ((rc = ensure_pcs(c, pl, G.S))) return rc;
+    if ((rc = c->flags.ensure(64))) return rc;
+    if (!dump && W32 > 0 && (rc = ensure_nbias(c, (int)pl->M, G.P, G.L, W32))) return rc;
+    static const int use_graph = env_int("TC_GRAPH", 1);
+    // stage events (per-stage times, profiling) go on the direct path: event
+    // nodes inside the graph cost as much as the launches it saves
+    if (!use_graph || stage_events)
+        return enqueue_pipeline(c, pl, G, a_bits, b_bits, rows, W32, out, dump, cc, stage_events);
+    std::vector<int64_t> key = {pl->d, pl->N, pl->K, pl->M, pl->s_y, pl->P, pl->flags,
+                                a_bits > pl->N, b_bits > pl->N, rows, W32, dump,
+                                (int64_t)(intptr_t)out, (int64_t)(intptr_t)c->a_dev, (int64_t)(intptr_t)c->b_dev,
+                                c->da, c->db, c->a_cw, c->b_cw,
+                                (int64_t)(intptr_t)c->grids.p, (int64_t)(intptr_t)c->pcs.p,
+                                (int64_t)(intptr_t)c->flags.p, (int64_t)(intptr_t)c->nbias.p,
+                                (int64_t)(intptr_t)c->twx_f.p, (int64_t)(intptr_t)c->twx_i.p,
+                                (int64_t)(intptr_t)c->twy_f.p, (int64_t)(intptr_t)c->twy_i.p};
+    for (int q = 0; q < pl->P; ++q) key.push_back(pl->p[q]);
+    if (c->gexec && key == c->gkey) {
+        CK(cudaGraphLaunch(c->gexec, c->st));
+        c->launches += c->glaunches;
+        return TC_OK;
+    }
+    if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; c->gkey.clear(); }
+    CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeRelaxed));
+    const int64_t l0 = c->launches;
+    rc = enqueue_pipeline(c, pl, G, a_bits, b_bits, rows, W32, out, dump, cc, false);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(c->st, &graph);
+    if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
+    if (ec != cudaSuccess) return set_err(TC_ERR_CUDA, "stream capture failed: %s", cudaGetErrorString(ec));
+    const cudaError_t ei = cudaGraphInstantiate(&c->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) { c->gexec = nullptr; return set_err(TC_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(ei)); }
+    c->gkey = key;
+    c->glaunches = c->launches - l0;
+    CK(cudaGraphLaunch(c->gexec, c->st));
     return TC_OK;
 }
 
@@ -614,6 +670,7 @@ int tc_ctx_destroy(void* ctx) {
     cudaStreamSynchronize(c->st);
     for (DevBuf* b : {&c->in_a, &c->in_b, &c->grids, &c->twx_f, &c->twx_i, &c->twy_f, &c->twy_i,
                       &c->pcs, &c->flags, &c->outbuf, &c->dbg, &c->nbias}) b->release();
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (auto& ev : c->ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : c->user_ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : c->xev) if (ev) cudaEventDestroy(ev);
@@ -650,10 +707,12 @@ int tc_stage_inputs(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw,
     k_width<<<(unsigned)((db + 255) / 256), 256, 0, c->st>>>(c->b_dev, db, b_cw, wf + 2);
     c->launches += 2;
     CKL();
-    int h[4];
-    CK(cudaMemcpyAsync(h, wf, sizeof h, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    if (info) { info->n_in_a = h[0]; info->nonzero_a = h[1]; info->n_in_b = h[2]; info->nonzero_b = h[3]; }
+    if (info) {              // read the widths back (blocks); NULL: caller reuses a plan, no host round trip
+        int h[4];
+        CK(cudaMemcpyAsync(h, wf, sizeof h, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        info->n_in_a = h[0]; info->nonzero_a = h[1]; info->n_in_b = h[2]; info->nonzero_b = h[3];
+    }
     return TC_OK;
 }
 
@@ -679,15 +738,19 @@ int tc_execute(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32_t b_bits,
         if ((rc = c->outbuf.ensure((size_t)rows * out_cw * 8))) return rc;
         dout = c->outbuf.as<uint32_t>();
     }
-    if ((rc = run_pipeline(c, plan, a_bits, b_bits, rows, 2 * out_cw, dout, false, cc))) return rc;
+    const bool stage_events = times != nullptr || c->profiling;
+    if ((rc = run_pipeline(c, plan, a_bits, b_bits, rows, 2 * out_cw, dout, false, cc, stage_events))) return rc;
     if (!out_on_device)
         CK(cudaMemcpyAsync(out, dout, (size_t)rows * out_cw * 8, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaEventRecord(c->ev[6], c->st));
+    if (stage_events) CK(cudaEventRecord(c->ev[6], c->st));
     int f[4];
     if ((rc = read_flags(c, f))) return rc;
     float ms[6] = {0};
-    for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&ms[i], c->ev[i], c->ev[i + 1]);
-    for (int i = 0; i < 6; ++i) c->stage_ms[i] = ms[i];
+    if (stage_events) {
+        for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&ms[i], c->ev[i], c->ev[i + 1]);
+        (void)cudaGetLastError();
+        for (int i = 0; i < 6; ++i) c->stage_ms[i] = ms[i];
+    }
     if (times) {
         times->convert = ms[0] * 1e-3;
         times->ntt_forward = ms[1] * 1e-3;
@@ -828,6 +891,7 @@ int tc_multiply_host(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int
     CK(cudaStreamSynchronize(c->aux));
     float ms[6] = {0};
     for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&ms[i], c->ev[i], c->ev[i + 1]);
+    (void)cudaGetLastError();         // an unrecorded stage event is not an error of the product
     for (int i = 0; i < 6; ++i) c->stage_ms[i] = ms[i];
     if (times) {
         times->convert = ms[0] * 1e-3;
@@ -866,7 +930,7 @@ int tc_digits(void* ctx, int32_t which, int64_t K, int64_t M, int64_t N, int32_t
     int R = (int)(K >= 2048 ? 1 : 2048 / K);
     if (R > d) R = (int)d;
     const size_t smem = (size_t)R * K * 8 + (size_t)R * 8;
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_digits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(ensure_smem((const void*)k_digits, smem));
     k_digits<<<(unsigned)((d + R - 1) / R), 256, smem, c->st>>>(src, R, dd);
     c->launches++;
     CKL();
@@ -892,7 +956,7 @@ int tc_bivariate_product(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32
     if ((rc = make_crt_const(plan, dmin, &cc))) return rc;
     const size_t bytes = (size_t)rows * 2 * plan->K * plan->P * 4;
     if ((rc = c->outbuf.ensure(bytes))) return rc;
-    if ((rc = run_pipeline(c, plan, a_bits, b_bits, rows, 0, c->outbuf.as<uint32_t>(), true, cc))) return rc;
+    if ((rc = run_pipeline(c, plan, a_bits, b_bits, rows, 0, c->outbuf.as<uint32_t>(), true, cc, true))) return rc;
     CK(cudaMemcpyAsync(coeffs_out, c->outbuf.p, bytes, cudaMemcpyDeviceToHost, c->st));
     int f[4];
     if ((rc = read_flags(c, f))) return rc;

@@ -17,8 +17,7 @@ cudaError_t launch_final_t(bool dump, const FinalArgs& A, const CrtConst& cc, un
     cudaError_t e = cudaSuccess;
 #define TC_LAUNCH(DUMP, NT)                                                                       \
     do {                                                                                          \
-        if (smem > 48 * 1024)                                                                     \
-            e = cudaFuncSetAttribute(k_final<P, DUMP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        e = ensure_smem((const void*)k_final<P, DUMP, NT>, smem);                                \
         if (e != cudaSuccess) return e;                                                           \
         k_final<P, DUMP, NT><<<grid, NT, smem, st>>>(A, cc);                                     \
     } while (0)

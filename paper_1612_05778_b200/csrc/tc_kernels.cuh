@@ -28,9 +28,25 @@
 //              (tc/_kernels.py:78-423, tc/multiplier.py:66-160)
 #pragma once
 #include <stdint.h>
+#include <mutex>
+#include <unordered_map>
 #include "tc_field.cuh"
 
 namespace tc {
+
+// Raise a kernel's dynamic shared-memory limit once per (kernel, size): the
+// attribute call costs host time on every launch otherwise.
+static inline cudaError_t ensure_smem(const void* fn, size_t smem) {
+    if (smem <= 48 * 1024) return cudaSuccess;
+    static std::mutex mu;
+    static std::unordered_map<const void*, size_t> done;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = done.find(fn);
+    if (it != done.end() && it->second >= smem) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) done[fn] = smem;
+    return e;
+}
 
 constexpr int kMaxPrimes = 16;
 #ifndef TC_HIGH_MINB
