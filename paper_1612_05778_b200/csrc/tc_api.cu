@@ -807,23 +807,42 @@ int tc_multiply_host(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int
     uint32_t* GB = GA + (size_t)G.P * G.S;
     const ShardArgs one = single_gpu();
     int* wf = c->dbg.as<int>();
-    // main: A in, its width, its first pass (planned from the declared widths)
+    // main: A in, its width, its first pass and its forward high passes (A's
+    // whole forward transform: nothing of it waits for B)
+    const int nh = (int)G.high.size();
     CK(cudaEventRecord(c->ev[0], c->st));
     CK(cudaMemsetAsync(wf, 0, 16, c->st));
     CK(cudaMemcpyAsync(c->in_a.p, a, (size_t)da * a_cw * 8, cudaMemcpyHostToDevice, c->st));
+    CK(cudaEventRecord(c->xev[0], c->st));            // A uploaded (and the width flags cleared)
     k_width<<<(unsigned)((da + 255) / 256), 256, 0, c->st>>>(c->a_dev, da, a_cw, wf);
     c->launches++;
     CKL();
-    CK(cudaEventRecord(c->xev[0], c->st));
     if ((rc = launch_low(c, G, plan, c->a_dev, da, a_cw, a_bits > plan->N, GA, one))) return rc;
-    // aux, concurrently: B in, its width, both widths back to the host
-    CK(cudaMemcpyAsync(c->in_b.p, b, (size_t)db * b_cw * 8, cudaMemcpyHostToDevice, c->aux));
+    for (int i = 0; i < nh; ++i)
+        if ((rc = launch_high(c, MODE_FWD, G, GA, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
+    // aux, behind A's upload (A first over PCIe): B in, its width, both widths back to the host
     CK(cudaStreamWaitEvent(c->aux, c->xev[0], 0));
+    CK(cudaMemcpyAsync(c->in_b.p, b, (size_t)db * b_cw * 8, cudaMemcpyHostToDevice, c->aux));
+    CK(cudaEventRecord(c->xev[10], c->aux));
     k_width<<<(unsigned)((db + 255) / 256), 256, 0, c->aux>>>(c->b_dev, db, b_cw, wf + 2);
     c->launches++;
     CKL();
     CK(cudaMemcpyAsync(c->hinfo, wf, 16, cudaMemcpyDeviceToHost, c->aux));
     CK(cudaEventRecord(c->xev[1], c->aux));
+    CK(cudaStreamWaitEvent(c->st, c->xev[10], 0));      // B uploaded
+    if ((rc = launch_low(c, G, plan, c->b_dev, db, b_cw, b_bits > plan->N, GB, one))) return rc;
+    CK(cudaEventRecord(c->ev[1], c->st));
+    for (int i = 0; i + 1 < nh; ++i)
+        if ((rc = launch_high(c, MODE_FWD, G, GB, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
+    CK(cudaEventRecord(c->ev[2], c->st));
+    if (nh > 0) rc = launch_high(c, MODE_MID, G, GB, GA, G.high[nh - 1].first, G.high[nh - 1].second, one);
+    else rc = launch_high(c, MODE_MID, G, GB, GA, G.lgS, 0, one);
+    if (rc) return rc;
+    CK(cudaEventRecord(c->ev[3], c->st));
+    for (int i = nh - 2; i >= 0; --i)
+        if ((rc = launch_high(c, MODE_INV, G, GB, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
+    CK(cudaEventRecord(c->ev[4], c->st));
+    // the true widths (back long ago) fix the product's row length: only k_final needs them
     CK(cudaEventSynchronize(c->xev[1]));
     const int n_in = c->hinfo[0] > c->hinfo[2] ? c->hinfo[0] : c->hinfo[2];
     const int64_t d = da > db ? da : db;
@@ -841,22 +860,6 @@ int tc_multiply_host(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int
         return set_err(TC_ERR_BAD_ARG, "output capacity %lld words < %lld", (long long)out_capacity_words,
                        (long long)rows * out_cw);
     }
-    CK(cudaStreamWaitEvent(c->st, c->xev[1], 0));
-    if ((rc = launch_low(c, G, plan, c->b_dev, db, b_cw, b_bits > plan->N, GB, one))) return rc;
-    CK(cudaEventRecord(c->ev[1], c->st));
-    const int nh = (int)G.high.size();
-    for (int i = 0; i < nh; ++i)
-        if ((rc = launch_high(c, MODE_FWD, G, GA, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
-    for (int i = 0; i + 1 < nh; ++i)
-        if ((rc = launch_high(c, MODE_FWD, G, GB, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
-    CK(cudaEventRecord(c->ev[2], c->st));
-    if (nh > 0) rc = launch_high(c, MODE_MID, G, GB, GA, G.high[nh - 1].first, G.high[nh - 1].second, one);
-    else rc = launch_high(c, MODE_MID, G, GB, GA, G.lgS, 0, one);
-    if (rc) return rc;
-    CK(cudaEventRecord(c->ev[3], c->st));
-    for (int i = nh - 2; i >= 0; --i)
-        if ((rc = launch_high(c, MODE_INV, G, GB, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
-    CK(cudaEventRecord(c->ev[4], c->st));
     // k_final in chunks; chunk j's rows (k*T + x, x in the chunk) go to the host while later chunks run
     const int W32 = 2 * out_cw;
     if ((rc = c->outbuf.ensure((size_t)rows * out_cw * 8))) return rc;
