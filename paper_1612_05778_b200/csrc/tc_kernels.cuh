@@ -291,6 +291,102 @@ static __device__ void compute_digits(const DigitSrc& a, int R, const int64_t* c
     }
 }
 
+// The same digits from coefficient words staged in shared memory (sw, R x cw
+// words, all loads in flight at once), D = ceil(R K / threads) consecutive
+// digits per thread: thread-local generate/propagate transfer, one warp
+// ballot add and one cross-warp scan for the whole tile (one barrier pair,
+// instead of two per blockDim digits).  Ends with a barrier (sw is reusable).
+static __device__ void compute_digits_staged(const DigitSrc& a, int R, const int64_t* coeff, int64_t* dig,
+                                             DigitScratch& ds, uint64_t* sw) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int M = a.M, cw = a.cw;
+    const uint64_t half = 1ull << (M - 1), beta = 1ull << M, mask = beta - 1;
+    const int64_t sq = (a.N - 1) >> 6;
+    const int sr = (int)((a.N - 1) & 63);
+    if (tid == 0) ds.round_carry = 0;
+    const int64_t nw = (int64_t)R * cw;
+    for (int64_t t = tid; t < nw; t += blockDim.x) {
+        const int r = (int)(t / cw);
+        const int64_t ci = coeff[r];
+        sw[t] = ci >= 0 ? __ldg(a.words + ci * cw + (t - (int64_t)r * cw)) : 0ull;
+    }
+    __syncthreads();
+    auto word = [&](const uint64_t* row, int64_t k) -> uint64_t {
+        return k < cw ? row[k] : ((row[cw - 1] >> 63) ? ~0ull : 0ull);
+    };
+    for (int r = tid; a.check_range && r < R; r += blockDim.x) {      // N-bit range (tc/codec.py:78-83)
+        const int64_t i = coeff[r];
+        if (i < 0) continue;
+        const uint64_t* row = sw + (int64_t)r * cw;
+        const uint64_t sgn = ((word(row, sq) >> sr) & 1) ? ~0ull : 0ull;
+        bool bad = false;
+        for (int64_t k = sq; k < cw; ++k) {
+            uint64_t lim = row[k], expect = sgn;
+            if (k == sq) { lim >>= sr; expect >>= sr; }
+            if (lim != expect) { bad = true; break; }
+        }
+        if (bad) atomicMin(&a.err[1], (int)min(i, (int64_t)0x7fffffff));
+    }
+    const int64_t ndig = (int64_t)R * a.K;
+    const int D = (int)((ndig + blockDim.x - 1) / blockDim.x);
+    const int64_t t0 = (int64_t)tid * D;
+    auto chunk_of = [&](int r, int64_t j) -> uint64_t {
+        if (coeff[r] < 0) return 0ull;
+        const uint64_t* row = sw + (int64_t)r * cw;
+        const int64_t off = j * M, wq = off >> 6;
+        const int wr = (int)(off & 63);
+        uint64_t c = word(row, wq) >> wr;
+        if (wr + M > 64) c |= word(row, wq + 1) << (64 - wr);
+        return c & mask;
+    };
+    uint32_t c0 = 0, c1 = 1;                  // carry out of this thread's digits for carry in 0 / 1
+    for (int i = 0; i < D; ++i) {
+        const int64_t t = t0 + i;
+        if (t >= ndig) break;
+        const int r = (int)(t >> a.lgK);
+        const int64_t j = t & (a.K - 1);
+        const bool top = j == a.K - 1;
+        const uint64_t ch = chunk_of(r, j);
+        const uint32_t g = !top && ch >= half, p = !top && ch == half - 1;
+        c0 = g | (p & c0);
+        c1 = g | (p & c1);
+    }
+    const unsigned G = __ballot_sync(0xffffffffu, c0);
+    const unsigned Pm = __ballot_sync(0xffffffffu, c1 & !c0);
+    const uint64_t A = (uint64_t)(G | Pm), B = (uint64_t)G;
+    if (lane == 0) ds.warp_tf[warp] = (uint32_t)((A + B) >> 32) | ((uint32_t)((A + B + 1) >> 32) << 1);
+    __syncthreads();
+    if (warp == 0) warp_carry_scan(ds.warp_tf, ds.warp_cin, &ds.round_carry, nwarps, lane);
+    __syncthreads();
+    uint32_t c = (uint32_t)(((A + B + ds.warp_cin[warp]) ^ A ^ B) >> lane) & 1u;
+    for (int i = 0; i < D; ++i) {
+        const int64_t t = t0 + i;
+        if (t >= ndig) break;
+        const int r = (int)(t >> a.lgK);
+        const int64_t j = t & (a.K - 1);
+        const int64_t ci = coeff[r];
+        const bool top = j == a.K - 1;
+        const uint64_t ch = chunk_of(r, j);
+        if (ci >= 0) {
+            const uint64_t cu = ch + c;
+            int64_t dg;
+            if (!top) {
+                dg = cu >= half ? -(int64_t)(beta - cu) : (int64_t)cu;
+            } else if ((word(sw + (int64_t)r * cw, sq) >> sr) & 1) {
+                if (cu < half) atomicMin(&a.err[0], (int)min(ci, (int64_t)0x7fffffff));
+                dg = -(int64_t)(beta - cu);
+            } else {
+                if (cu >= half) atomicMin(&a.err[0], (int)min(ci, (int64_t)0x7fffffff));
+                dg = (int64_t)cu;
+            }
+            dig[t] = dg;
+        }
+        const uint32_t g = !top && ch >= half, p = !top && ch == half - 1;
+        c = g | (p & c);
+    }
+    __syncthreads();
+}
+
 // Parity seam: digits of coefficients [r0, r0+R) in natural order.
 static __global__ void __launch_bounds__(256) k_digits(DigitSrc a, int R, int64_t* out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -547,6 +643,7 @@ template <bool DIF>
 __device__ __noinline__ void x_transform(uint32_t* s, int lgL, int tile_bits, const uint2* twx,
                                          uint32_t p, uint32_t two_p) {
     switch (lgL) {
+        case 0: break;
         case 1: xct<1, DIF>(s, tile_bits, twx, p, two_p); break;
         case 2: xct<2, DIF>(s, tile_bits, twx, p, two_p); break;
         case 3: xct<3, DIF>(s, tile_bits, twx, p, two_p); break;
@@ -745,16 +842,34 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
         }
         return;
     }
-    compute_digits(A.src, Rc, coeff, dig, ds);
+    // coefficient words staged in the (not yet used) tile buffer when they fit
+    if ((int64_t)Rc * A.src.cw * 8 <= (int64_t)padded_words(n) * 4)
+        compute_digits_staged(A.src, Rc, coeff, dig, ds, reinterpret_cast<uint64_t*>(tile));
+    else
+        compute_digits(A.src, Rc, coeff, dig, ds);
     for (int q = 0; q < A.P; ++q) {
         const PrimeC pc = A.pcs[q];
-        for (uint32_t e = threadIdx.x; e < nc; e += blockDim.x) {
-            const uint32_t r = e >> A.lgL, j = e & (L - 1);
-            tile[padi(e)] = (j < A.src.K && coeff[r] >= 0) ? digit_residue(dig[(int64_t)r * A.src.K + j], pc) : 0u;
+        const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
+        // residues of the K digit columns; the top x level (DIF on (x_j, 0) pairs,
+        // the theta-twist) is fused here: columns j and j + K get x_j and x_j w_j
+        {
+            const uint2* wtop = tw.twx + (L >> 1);             // level lgL-1, entry 2^(lgL-1) + j
+            const uint32_t kk = (uint32_t)A.src.K, nk = (uint32_t)Rc * kk;
+            for (uint32_t t = threadIdx.x; t < nk; t += blockDim.x) {
+                const uint32_t r = t >> A.src.lgK, j = t & (kk - 1);
+                const uint32_t e = (r << A.lgL) | j;
+                uint32_t x = 0, y = 0;
+                if (coeff[r] >= 0) {
+                    x = digit_residue(dig[t], pc);
+                    const uint2 w = __ldg(wtop + j);
+                    y = shoup_mul(x, w.x, w.y, pc.p);
+                }
+                tile[padi(e)] = x;
+                tile[padi(e + kk)] = y;
+            }
         }
         __syncthreads();
-        const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
-        x_transform<true>(tile, A.lgL, cbits, tw.twx, pc.p, pc.two_p);           // x: DIF, computed rows
+        x_transform<true>(tile, A.lgL - 1, cbits, tw.twx, pc.p, pc.two_p);       // x: DIF, levels below the twist
         if (prune) {
             // expand in place, highest chunk first: compact e -> rows 2r', 2r'+1
             const uint32_t chunk = 8u * blockDim.x;
