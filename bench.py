@@ -358,6 +358,8 @@ def run_sharded(args, rank, world, local):
     clocks.start()
 
     def timed(fn):
+        _lib.check(dm.ctx.lib.tc_flush_l2(dm.ctx.handle), "flush")     # every rank, before every timed step
+        dm._sync()
         torch.cuda.synchronize()
         _barrier(world)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -391,8 +393,8 @@ def run_sharded(args, rank, world, local):
         "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded PCG64, BASELINE.md section 4 recipe)",
         "config": {"workload": f"{args.config}: {workloads.CONFIGS[args.config].text}",
                    "plan": plan.describe(), "parallelism": f"sharded x{world} (row tiles / column groups, "
-                   f"NCCL all-to-all per prime, gather to rank 0)",
-                   "l2": "working set per product > L2 only for C3; not flushed between steps",
+                   f"{torch.distributed.get_backend()} all-to-all per prime, gather to rank 0)",
+                   "l2": "flushed (256 MiB memset) on every rank before every timed step",
                    "verified_vs_reference_sha256": verified},
         "e2e": {"value": round(args.steps * out_gbit / (e2e_ms / 1e3), 3), "unit": "Gbit/s",
                 "ms_per_step": round(e2e_ms / args.steps, 4),

@@ -308,6 +308,7 @@ class DistributedMultiplier:
         t.cuda.synchronize(self.device)
         g = t.cat(self.gathered, dim=0)
         dout = t.empty((rows, 2 * out_cw), dtype=t.int32, device=self.device)
+        t.cuda.synchronize(self.device)          # torch's stream produced g; the library reads it on its own
         _lib.check(lib.tc_unshard(h, tp, g.data_ptr(), rows, out_cw, dout.data_ptr()), "unshard")
         self._sync()
         if not to_host:
