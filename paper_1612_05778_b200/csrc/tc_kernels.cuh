@@ -52,6 +52,9 @@ constexpr int kMaxPrimes = 16;
 #ifndef TC_HIGH_MINB
 #define TC_HIGH_MINB 3      // 256-thread k_high CTAs per SM the register budget is sized for
 #endif
+#ifndef TC_CT_R32
+#define TC_CT_R32 1         // k_high_ct passes in radix-32 rounds
+#endif
 #ifndef TC_ROUND_G2
 #define TC_ROUND_G2 1       // interleave two register groups per round when each thread owns >= 2
 #endif
@@ -1049,6 +1052,25 @@ __device__ __forceinline__ void ct_round(uint32_t* s, const uint2* stw, uint32_t
 template <int U, bool DIF, int NT>
 __device__ __forceinline__ void ct_pass(uint32_t* s, const uint2* stw, uint32_t p, uint32_t two_p) {
     constexpr int TB = U + 4;
+#if TC_CT_R32
+    if constexpr (U == 10) {            // two radix-32 rounds (bit 4's half-warps 512 slots apart: no permutation)
+        if (!DIF) {
+            ct_round<TB, 4, 5, false, NT>(s, stw, p, two_p);
+            ct_round<TB, 9, 5, false, NT>(s, stw, p, two_p);
+        } else {
+            ct_round<TB, 9, 5, true, NT>(s, stw, p, two_p);
+            ct_round<TB, 4, 5, true, NT>(s, stw, p, two_p);
+        }
+    } else if constexpr (U == 9) {
+        if (!DIF) {
+            ct_round<TB, 4, 5, false, NT>(s, stw, p, two_p);
+            ct_round<TB, 9, 4, false, NT>(s, stw, p, two_p);
+        } else {
+            ct_round<TB, 9, 4, true, NT>(s, stw, p, two_p);
+            ct_round<TB, 4, 5, true, NT>(s, stw, p, two_p);
+        }
+    } else {
+#else
     if constexpr (U == 10) {
         if (!DIF) {
             ct_round<TB, 4, 4, false, NT>(s, stw, p, two_p);
@@ -1070,6 +1092,7 @@ __device__ __forceinline__ void ct_pass(uint32_t* s, const uint2* stw, uint32_t 
             ct_round<TB, 4, 3, true, NT>(s, stw, p, two_p);
         }
     } else {
+#endif
         static_assert(U == 4, "unsupported compile-time pass");
         ct_round<TB, 4, 4, DIF, NT>(s, stw, p, two_p);
     }
