@@ -800,33 +800,40 @@ int tc_multiply_host(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int
     if ((rc = c->dbg.ensure(64))) return rc;
     c->a_dev = c->in_a.as<uint64_t>(); c->b_dev = c->in_b.as<uint64_t>();
     c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true;
-    Geometry G;
-    if ((rc = prepare(c, plan, G, true))) return rc;
-    if ((rc = c->grids.ensure((size_t)2 * G.P * G.S * 4))) return rc;
-    uint32_t* GA = c->grids.as<uint32_t>();
-    uint32_t* GB = GA + (size_t)G.P * G.S;
-    const ShardArgs one = single_gpu();
     int* wf = c->dbg.as<int>();
-    // main: A in, its width, its first pass and its forward high passes (A's
-    // whole forward transform: nothing of it waits for B)
-    const int nh = (int)G.high.size();
+    // both uploads first (A, then B behind it on the aux stream: A first over
+    // PCIe); the host preparation below runs while they are on the wire
     CK(cudaEventRecord(c->ev[0], c->st));
     CK(cudaMemsetAsync(wf, 0, 16, c->st));
     CK(cudaMemcpyAsync(c->in_a.p, a, (size_t)da * a_cw * 8, cudaMemcpyHostToDevice, c->st));
     CK(cudaEventRecord(c->xev[0], c->st));            // A uploaded (and the width flags cleared)
-    k_width<<<(unsigned)((da + 255) / 256), 256, 0, c->st>>>(c->a_dev, da, a_cw, wf);
-    c->launches++;
-    CKL();
-    if ((rc = launch_low(c, G, plan, c->a_dev, da, a_cw, a_bits > plan->N, GA, one))) return rc;
-    for (int i = 0; i < nh; ++i)
-        if ((rc = launch_high(c, MODE_FWD, G, GA, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
-    // aux, behind A's upload (A first over PCIe): B in, its width, both widths back to the host
     CK(cudaStreamWaitEvent(c->aux, c->xev[0], 0));
     CK(cudaMemcpyAsync(c->in_b.p, b, (size_t)db * b_cw * 8, cudaMemcpyHostToDevice, c->aux));
     CK(cudaEventRecord(c->xev[10], c->aux));
+    Geometry G;
+    if ((rc = prepare(c, plan, G, true)) || (rc = c->grids.ensure((size_t)2 * G.P * G.S * 4))) {
+        cudaStreamSynchronize(c->st);        // the uploads read the caller's buffers: finish them first
+        cudaStreamSynchronize(c->aux);
+        return rc;
+    }
+    uint32_t* GA = c->grids.as<uint32_t>();
+    uint32_t* GB = GA + (size_t)G.P * G.S;
+    const ShardArgs one = single_gpu();
+    // main: A's width, its first pass and its forward high passes (A's whole
+    // forward transform: nothing of it waits for B)
+    const int nh = (int)G.high.size();
+    k_width<<<(unsigned)((da + 255) / 256), 256, 0, c->st>>>(c->a_dev, da, a_cw, wf);
+    c->launches++;
+    CKL();
+    CK(cudaEventRecord(c->xev[11], c->st));           // A's width reduced
+    if ((rc = launch_low(c, G, plan, c->a_dev, da, a_cw, a_bits > plan->N, GA, one))) return rc;
+    for (int i = 0; i < nh; ++i)
+        if ((rc = launch_high(c, MODE_FWD, G, GA, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
+    // aux: B's width, both widths back to the host
     k_width<<<(unsigned)((db + 255) / 256), 256, 0, c->aux>>>(c->b_dev, db, b_cw, wf + 2);
     c->launches++;
     CKL();
+    CK(cudaStreamWaitEvent(c->aux, c->xev[11], 0));
     CK(cudaMemcpyAsync(c->hinfo, wf, 16, cudaMemcpyDeviceToHost, c->aux));
     CK(cudaEventRecord(c->xev[1], c->aux));
     CK(cudaStreamWaitEvent(c->st, c->xev[10], 0));      // B uploaded
