@@ -746,6 +746,61 @@ __device__ __noinline__ bool y_transform(uint32_t* s, int lgL, int rb0, int tile
     return true;
 }
 
+// k_low with pruned rows: the compact tile holds the even rows (row r' at
+// compact row r'), and the first y level is the duplication r' -> rows 2r',
+// 2r'+1.  When the remaining y levels form one round (ny <= 4: the tile has
+// exactly 2^ny compact rows), a thread owns whole columns: it reads the
+// column's compact rows once, runs the round for both parities (twiddle
+// offset = parity, as y_transform's round at row bit 1) and writes the 2^(ny+1)
+// expanded rows of the same column -- duplication and y levels in one pass,
+// and no other thread touches the column, so no barrier between read and write.
+template <int NB>
+__device__ __forceinline__ void yct_expand_columns(uint32_t* s, int lgL, const uint2* twy, uint32_t p,
+                                                   uint32_t two_p) {
+    constexpr int R = 1 << NB;
+    const uint32_t L = 1u << lgL;
+    for (uint32_t col = threadIdx.x; col < L; col += blockDim.x) {
+        uint32_t xa[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) xa[k] = s[padi(((uint32_t)k << lgL) | col)];
+#pragma unroll 1
+        for (int b = 0; b < 2; ++b) {
+            uint32_t x[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) x[k] = xa[k];
+            const uint2* tq = twy + b;
+#pragma unroll
+            for (int lv = 0; lv < NB; ++lv) {
+#pragma unroll
+                for (int m = 0; m < (1 << lv); ++m) {
+                    const uint2 w = __ldg(tq + (1 << (1 + lv)) + (m << 1));
+#pragma unroll
+                    for (int jj = 0; jj < R / (2 << lv); ++jj) {
+                        const int k = m + jj * (2 << lv);
+                        bfly_dit(x[k], x[k + (1 << lv)], w.x, w.y, p, two_p);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < R; ++k) s[padi(((uint32_t)(2 * k + b) << lgL) | col)] = x[k];
+        }
+    }
+    __syncthreads();
+}
+
+// false: shape not covered (caller expands and runs y_transform / run_bits).
+static __device__ __noinline__ bool y_transform_expand(uint32_t* s, int lgL, int tile_bits, const uint2* twy,
+                                                       uint32_t p, uint32_t two_p) {
+    const int ny = tile_bits - lgL - 1;          // y levels after the duplication
+    switch (lgL >= 5 ? ny : 0) {
+        case 1: yct_expand_columns<1>(s, lgL, twy, p, two_p); return true;
+        case 2: yct_expand_columns<2>(s, lgL, twy, p, two_p); return true;
+        case 3: yct_expand_columns<3>(s, lgL, twy, p, two_p); return true;
+        case 4: yct_expand_columns<4>(s, lgL, twy, p, two_p); return true;
+        default: return false;
+    }
+}
+
 struct TwRows {
     const uint2* twx; const uint2* twy; int lgL;
     __device__ __forceinline__ const uint2* table(int bit_lo) const { return bit_lo < lgL ? twx : twy; }
@@ -873,7 +928,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
         }
         __syncthreads();
         x_transform<true>(tile, A.lgL - 1, cbits, tw.twx, pc.p, pc.two_p);       // x: DIF, levels below the twist
-        if (prune) {
+        const bool fused = prune && y_transform_expand(tile, A.lgL, tile_bits, tw.twy, pc.p, pc.two_p);
+        if (prune && !fused) {
             // expand in place, highest chunk first: compact e -> rows 2r', 2r'+1
             const uint32_t chunk = 8u * blockDim.x;
             for (int64_t c0 = (int64_t)((nc - 1) / chunk) * chunk; c0 >= 0; c0 -= chunk) {
@@ -896,7 +952,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
                 __syncthreads();
             }
         }
-        if (!y_transform<false>(tile, A.lgL, prune ? 1 : 0, tile_bits, tw.twy, pc.p, pc.two_p))   // y: DIT
+        if (!fused && !y_transform<false>(tile, A.lgL, prune ? 1 : 0, tile_bits, tw.twy, pc.p, pc.two_p))   // y: DIT
             run_bits<false>(tile, tile_bits, A.lgL + (prune ? 1 : 0), tile_bits, tw, pc.p, pc.two_p);
         uint32_t* g = dst(q);
         if (sharded) tile_store(g, tile, n, XchgIdx{A.sh, blockIdx.x});
