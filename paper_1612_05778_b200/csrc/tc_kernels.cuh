@@ -55,6 +55,9 @@ constexpr int kMaxPrimes = 16;
 #ifndef TC_CT_R32
 #define TC_CT_R32 1         // k_high_ct passes in radix-32 rounds
 #endif
+#ifndef TC_CO_KW
+#define TC_CO_KW 4          // ConvertOut words per thread (8: C2 +16 %; 2: C2 +2 %, C4 -12 %)
+#endif
 #ifndef TC_ROUND_G2
 #define TC_ROUND_G2 1       // interleave two register groups per round when each thread owns >= 2
 #endif
@@ -1420,7 +1423,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
     // row's top word never generates or propagates (the mod 2^(32 W32) wrap),
     // so chains never cross rows.
     const int M = A.M, W32 = A.W32;
-    constexpr int kW = 4;
+    constexpr int kW = TC_CO_KW;
     const int Wp = (W32 + kW - 1) / kW * kW;
     const int64_t total = (int64_t)R * Wp;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
