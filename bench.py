@@ -54,23 +54,40 @@ def _dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled during the measured loops: NVML
+    polled every 2 ms from a background thread (nvidia-smi -lms 50 when NVML
+    is unavailable)."""
 
     def __init__(self, device: int):
-        self.device = device
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [x for x in vis.split(",") if x.strip()]
+        self.index = int(ids[device]) if device < len(ids) and ids[device].strip().isdigit() else device
+        self.samples, self.reason_bits, self.max_mhz = [], 0, None
+        self.stop_evt = threading.Event()
         self.proc = None
         self.lines = []
+        self.nvml = None
 
     def start(self, wait_s: float = 5.0):
-        """Start sampling every 50 ms and wait for the first sample, so the
-        measurement that follows is covered from its first step."""
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = (pynvml, h)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < wait_s:
+                time.sleep(0.001)
+            return
+        except Exception:  # noqa: BLE001 -- fall back to nvidia-smi
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                  "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
@@ -78,39 +95,62 @@ class ClockSampler:
             t0 = time.time()
             while not self.lines and time.time() - t0 < wait_s:
                 time.sleep(0.01)
-            self.skip = len(self.lines)
         except (OSError, FileNotFoundError):
             self.proc = None
+
+    def _poll(self):
+        pynvml, h = self.nvml
+        get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop_evt.is_set():
+            try:
+                self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                self.reason_bits |= int(get_reasons(h))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-        sm, mx, reasons = [], None, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines[getattr(self, "skip", 0):]:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
+        reasons = set()
+        if self.nvml:
+            self.stop_evt.set()
+            self.thread.join(timeout=2)
+            pynvml = self.nvml[0]
+            bits = (pynvml.nvmlClocksThrottleReasonHwSlowdown, pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksThrottleReasonSwThermalSlowdown, pynvml.nvmlClocksThrottleReasonSwPowerCap)
+            for n, b in zip(names, bits):
+                if self.reason_bits & b:
                     reasons.add(n)
+            sm, mx, src = self.samples, self.max_mhz, "nvml, 2 ms"
+        else:
+            if self.proc:
+                self.proc.terminate()
+                try:
+                    self.proc.wait(timeout=5)
+                except subprocess.TimeoutExpired:
+                    self.proc.kill()
+            sm, mx, src = [], None, "nvidia-smi, 50 ms"
+            for ln in self.lines:
+                parts = [x.strip() for x in ln.split(",")]
+                if len(parts) < 6:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    mx = float(parts[1])
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[2:6]):
+                    if v.lower() == "active":
+                        reasons.add(n)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": float(np.min(sm)), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm), "sampler": src}
 
 
 def _peaks():
@@ -258,7 +298,7 @@ def run_ours(args, rank, world, local):
         e2e.append(time.perf_counter() - t0)
         del prod
     clock_info = clocks.stop()
-    clock_info["window"] = "sampled every 50 ms over the warm-up, timed and e2e loops"
+    clock_info["window"] = "the warm-up, timed and e2e loops"
     e2e_s = _max_over_ranks(float(np.sum(e2e)), world)
 
     out_gbit = rows * out_bits / 1e9
