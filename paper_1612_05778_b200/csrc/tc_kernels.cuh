@@ -759,7 +759,7 @@ __device__ __noinline__ bool y_transform(uint32_t* s, int lgL, int rb0, int tile
 // and no other thread touches the column, so no barrier between read and write.
 template <int NB>
 __device__ __forceinline__ void yct_expand_columns(uint32_t* s, int lgL, const uint2* twy, uint32_t p,
-                                                   uint32_t two_p) {
+                                                   uint32_t two_p, uint32_t* gout) {
     constexpr int R = 1 << NB;
     const uint32_t L = 1u << lgL;
     for (uint32_t col = threadIdx.x; col < L; col += blockDim.x) {
@@ -784,22 +784,28 @@ __device__ __forceinline__ void yct_expand_columns(uint32_t* s, int lgL, const u
                     }
                 }
             }
+            if (gout) {      // straight to the grid (coalesced across the warp's columns)
 #pragma unroll
-            for (int k = 0; k < R; ++k) s[padi(((uint32_t)(2 * k + b) << lgL) | col)] = x[k];
+                for (int k = 0; k < R; ++k) gout[((uint32_t)(2 * k + b) << lgL) | col] = x[k];
+            } else {
+#pragma unroll
+                for (int k = 0; k < R; ++k) s[padi(((uint32_t)(2 * k + b) << lgL) | col)] = x[k];
+            }
         }
     }
     __syncthreads();
 }
 
 // false: shape not covered (caller expands and runs y_transform / run_bits).
+// gout != NULL: the finished tile goes straight to the grid (contiguous tile).
 static __device__ __noinline__ bool y_transform_expand(uint32_t* s, int lgL, int tile_bits, const uint2* twy,
-                                                       uint32_t p, uint32_t two_p) {
+                                                       uint32_t p, uint32_t two_p, uint32_t* gout) {
     const int ny = tile_bits - lgL - 1;          // y levels after the duplication
     switch (lgL >= 5 ? ny : 0) {
-        case 1: yct_expand_columns<1>(s, lgL, twy, p, two_p); return true;
-        case 2: yct_expand_columns<2>(s, lgL, twy, p, two_p); return true;
-        case 3: yct_expand_columns<3>(s, lgL, twy, p, two_p); return true;
-        case 4: yct_expand_columns<4>(s, lgL, twy, p, two_p); return true;
+        case 1: yct_expand_columns<1>(s, lgL, twy, p, two_p, gout); return true;
+        case 2: yct_expand_columns<2>(s, lgL, twy, p, two_p, gout); return true;
+        case 3: yct_expand_columns<3>(s, lgL, twy, p, two_p, gout); return true;
+        case 4: yct_expand_columns<4>(s, lgL, twy, p, two_p, gout); return true;
         default: return false;
     }
 }
@@ -931,7 +937,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
         }
         __syncthreads();
         x_transform<true>(tile, A.lgL - 1, cbits, tw.twx, pc.p, pc.two_p);       // x: DIF, levels below the twist
-        const bool fused = prune && y_transform_expand(tile, A.lgL, tile_bits, tw.twy, pc.p, pc.two_p);
+        const bool fused = prune && y_transform_expand(tile, A.lgL, tile_bits, tw.twy, pc.p, pc.two_p,
+                                                       sharded ? nullptr : dst(q));
         if (prune && !fused) {
             // expand in place, highest chunk first: compact e -> rows 2r', 2r'+1
             const uint32_t chunk = 8u * blockDim.x;
@@ -959,6 +966,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
             run_bits<false>(tile, tile_bits, A.lgL + (prune ? 1 : 0), tile_bits, tw, pc.p, pc.two_p);
         uint32_t* g = dst(q);
         if (sharded) tile_store(g, tile, n, XchgIdx{A.sh, blockIdx.x});
+        else if (fused) {}                                   // written by the fused round
         else if (n >= 4) tile_store(g, tile, n, Contig{});
         else tile_store_scalar(g, tile, n, Contig{});
         __syncthreads();
