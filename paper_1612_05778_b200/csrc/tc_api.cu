@@ -100,7 +100,7 @@ struct Ctx {
     cudaEvent_t user_ev[16] = {};
     DevBuf flush;
     cudaStream_t aux = nullptr;          // H2D of operand B and the chunked D2H of the product
-    cudaEvent_t xev[16] = {};            // cross-stream events of tc_multiply_host
+    cudaEvent_t xev[24] = {};            // cross-stream events of tc_multiply_host: 0 A up, 1 widths back, 2.. chunks, 20 B up, 21 A width
     int* hinfo = nullptr;                // pinned: widths read back early
 };
 
@@ -809,7 +809,7 @@ int tc_multiply_host(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int
     CK(cudaEventRecord(c->xev[0], c->st));            // A uploaded (and the width flags cleared)
     CK(cudaStreamWaitEvent(c->aux, c->xev[0], 0));
     CK(cudaMemcpyAsync(c->in_b.p, b, (size_t)db * b_cw * 8, cudaMemcpyHostToDevice, c->aux));
-    CK(cudaEventRecord(c->xev[10], c->aux));
+    CK(cudaEventRecord(c->xev[20], c->aux));
     Geometry G;
     if ((rc = prepare(c, plan, G, true)) || (rc = c->grids.ensure((size_t)2 * G.P * G.S * 4))) {
         cudaStreamSynchronize(c->st);        // the uploads read the caller's buffers: finish them first
@@ -825,7 +825,7 @@ int tc_multiply_host(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int
     k_width<<<(unsigned)((da + 255) / 256), 256, 0, c->st>>>(c->a_dev, da, a_cw, wf);
     c->launches++;
     CKL();
-    CK(cudaEventRecord(c->xev[11], c->st));           // A's width reduced
+    CK(cudaEventRecord(c->xev[21], c->st));           // A's width reduced
     if ((rc = launch_low(c, G, plan, c->a_dev, da, a_cw, a_bits > plan->N, GA, one))) return rc;
     for (int i = 0; i < nh; ++i)
         if ((rc = launch_high(c, MODE_FWD, G, GA, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
@@ -833,10 +833,10 @@ int tc_multiply_host(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int
     k_width<<<(unsigned)((db + 255) / 256), 256, 0, c->aux>>>(c->b_dev, db, b_cw, wf + 2);
     c->launches++;
     CKL();
-    CK(cudaStreamWaitEvent(c->aux, c->xev[11], 0));
+    CK(cudaStreamWaitEvent(c->aux, c->xev[21], 0));
     CK(cudaMemcpyAsync(c->hinfo, wf, 16, cudaMemcpyDeviceToHost, c->aux));
     CK(cudaEventRecord(c->xev[1], c->aux));
-    CK(cudaStreamWaitEvent(c->st, c->xev[10], 0));      // B uploaded
+    CK(cudaStreamWaitEvent(c->st, c->xev[20], 0));      // B uploaded
     if ((rc = launch_low(c, G, plan, c->b_dev, db, b_cw, b_bits > plan->N, GB, one))) return rc;
     CK(cudaEventRecord(c->ev[1], c->st));
     for (int i = 0; i + 1 < nh; ++i)
@@ -874,6 +874,7 @@ int tc_multiply_host(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int
     const int64_t T = G.S >> (G.lgL + G.yl), R = 1ll << G.yl;
     int nchunk = 1;                                   // >= one wave of CTAs per chunk
     while (nchunk < 8 && T / (2 * nchunk) >= 148) nchunk *= 2;
+    if (const int ce = env_int("TC_FINAL_CHUNKS", 0)) { nchunk = 1; while (nchunk < ce && nchunk < 16 && T / (2 * nchunk) >= 1) nchunk *= 2; }
     const int64_t nx = T / nchunk;
     const size_t rb = (size_t)out_cw * 8;
     for (int ch = 0; ch < nchunk; ++ch) {
