@@ -133,6 +133,26 @@ __host__ __device__ constexpr uint32_t padded_words(uint32_t n) { return n + (n 
 // for e % 4 == 0 (callers fall back to tile_*_scalar otherwise).
 constexpr int kBatch = 4;
 
+// Asynchronous 4-byte global -> shared copies (any padded slot); one commit
+// group per call site, waited with cp_async_wait<N> (N = groups left pending).
+__device__ __forceinline__ void cp_async4(uint32_t* smem, const uint32_t* gmem) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" :: "r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" :: "n"(N) : "memory"); }
+__device__ __forceinline__ void cp_async_wait_dyn(int n) {      // n = pending groups allowed, 0..15
+    switch (n) {
+        case 0: cp_async_wait<0>(); break;  case 1: cp_async_wait<1>(); break;  case 2: cp_async_wait<2>(); break;
+        case 3: cp_async_wait<3>(); break;  case 4: cp_async_wait<4>(); break;  case 5: cp_async_wait<5>(); break;
+        case 6: cp_async_wait<6>(); break;  case 7: cp_async_wait<7>(); break;  case 8: cp_async_wait<8>(); break;
+        case 9: cp_async_wait<9>(); break;  case 10: cp_async_wait<10>(); break; case 11: cp_async_wait<11>(); break;
+        case 12: cp_async_wait<12>(); break; case 13: cp_async_wait<13>(); break; case 14: cp_async_wait<14>(); break;
+        default: cp_async_wait<15>(); break;
+    }
+}
+
 template <class F>
 __device__ __forceinline__ void tile_load(uint32_t* s, const uint32_t* g, uint32_t n, F gidx) {
     const uint32_t nv = n >> 2, st = blockDim.x;
@@ -1378,16 +1398,24 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
     __syncthreads();
     if (!s_any) return;      // every row of this tile is zero padding
 
+    // all P tiles stream in at once (one cp.async group per prime); prime q's
+    // transform waits only for its own tile, later primes' loads overlap it
+    for (int q = 0; q < P; ++q) {
+        uint32_t* t = sm + q * stride;
+        if (sharded) {
+            const uint32_t* g = A.g + (int64_t)q * (A.sh.Tl << A.sh.TB);
+            const XchgIdx xi{A.sh, blockIdx.x};
+            for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) cp_async4(t + padi(e), g + xi(e));
+        } else {
+            const uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)tile * n;
+            for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) cp_async4(t + padi(e), g + e);
+        }
+        cp_async_commit();
+    }
     for (int q = 0; q < P; ++q) {
         const PrimeC pc = A.pcs[q];
         uint32_t* t = sm + q * stride;
-        if (sharded) {
-            tile_load(t, A.g + (int64_t)q * (A.sh.Tl << A.sh.TB), n, XchgIdx{A.sh, blockIdx.x});
-        } else {
-            const uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)tile * n;
-            if (n >= 4) tile_load(t, g, n, Contig{});
-            else tile_load_scalar(t, g, n, Contig{});
-        }
+        cp_async_wait_dyn(P - 1 - q);
         __syncthreads();
         const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
         if (!y_transform<true>(t, A.lgL, 0, tile_bits, tw.twy, pc.p, pc.two_p))   // y low: DIF
