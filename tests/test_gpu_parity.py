@@ -137,12 +137,14 @@ def test_c_plus_minus_match_reference_golden():
     assert ran >= len(meta) // 3
 
 
-def test_bivariate_product_vs_naive(oracle):
-    rng = random.Random(31)
+@pytest.mark.parametrize("mlo,mhi,seed", [(2, 40, 31), (41, 63, 32)])
+def test_bivariate_product_vs_naive(oracle, mlo, mhi, seed):
+    # exact c_ij (k_final's DUMP mode) for P = 1..5 primes
+    rng = random.Random(seed)
     for _ in range(20):
         d = rng.randint(1, 9)
         K = rng.choice([1, 2, 4, 8])
-        M = rng.randint(2, 40)
+        M = rng.randint(mlo, mhi)
         half = 1 << (M - 1)
         dg = lambda: np.array([[rng.randint(-half, half - 1) for _ in range(K)] for _ in range(d)],
                               dtype=np.int64)
@@ -360,3 +362,30 @@ def test_extreme_plans(oracle):
     a = _random_poly(rng, 8, 126, extremes=True)
     with pytest.raises(tc.EncodingError):
         tc.multiply_with_plan(tc.MulRequest(a, a), K=2, M=63)
+
+
+def test_plan_sweep(oracle):
+    # every transform length 2K = 2 .. 2^14 (the compile-time x schedules, the
+    # fused twist / duplication rounds, k_high_ct / generic passes), degrees
+    # that move the in-tile y levels yl across their range, unbalanced
+    # operands and explicit digit sizes: bit-exact against the oracle
+    rng = random.Random(2024)
+    cases = []
+    for lgk in range(0, 14):
+        K = 1 << lgk
+        for d, nbits, db in ((3, 20, 3), (40, 60, 17), (700, 50, 700)):
+            nb = max(2, min(K * 31, nbits * (1 + lgk)))       # widths that want about this K
+            if d * nb > 3_000_000:
+                continue
+            cases.append((d, db, nb, dict(K=K)))
+    cases += [(1, 1, 5, {}), (2, 1, 63, {}), (1, 300, 64, {}), (2047, 3, 33, {}), (5000, 5000, 31, {}),
+              (1000, 1000, 200, dict(M=25)), (64, 64, 4000, dict(M=40)), (257, 255, 129, dict(M=63))]
+    for da, db, nbits, kw in cases:
+        a = _random_poly(rng, da, nbits)
+        b = _random_poly(rng, db, nbits)
+        try:
+            out, _, plan = tc.multiply_with_plan(tc.MulRequest(a, b), **kw)
+        except tc.EncodingError:
+            continue                     # an explicit split too narrow for the operands
+        exp, bits = oracle.multiply_words(a.words, a.bit_width, b.words, b.bit_width)
+        assert out.bit_width == bits and np.array_equal(out.words, exp), (da, db, nbits, plan.describe())
