@@ -288,6 +288,27 @@ int make_geometry(const tc_plan_t* pl, Geometry& G, int world = 1) {
     int yl = tb - G.lgL;
     if (yl < 0) yl = 0;
     if (yl > G.lgS) yl = G.lgS;
+    // small grids: the row tiles (2^(lgL+yl) slots) and the high-pass tiles
+    // (2^(4+U) slots) share out the grid; when the default leaves fewer than
+    // two waves (2 x 148 CTAs) on either side, take the yl in [1, yl] that
+    // maximises the smaller CTA count (params.pass_layout mirrors this)
+    if (world == 1 && yl > 1) {
+        auto min_ctas = [&](int y) -> int64_t {
+            const int64_t lo = G.S >> (G.lgL + y);
+            const int nl = G.lgS - y;
+            if (nl <= 0) return lo;
+            const int cb = G.lgL + y < 4 ? G.lgL + y : 4;
+            const int np = (nl + 9) / 10, umax = (nl + np - 1) / np;
+            const int64_t hi = G.S >> (umax + cb);
+            return lo < hi ? lo : hi;
+        };
+        if (min_ctas(yl) < 2 * 148) {
+            int best = yl;
+            for (int y = yl - 1; y >= 1; --y)
+                if (min_ctas(y) > min_ctas(best)) best = y;
+            yl = best;
+        }
+    }
     // sharded: at least `world` row tiles
     const int lw = ilog2(world);
     if (world > 1 && yl > G.lgS - lw) yl = G.lgS - lw > 0 ? G.lgS - lw : 0;

@@ -242,6 +242,24 @@ def pass_layout(lgL: int, lgS: int, P: int):
         tb += 1
     tb = min(tb, 13)
     yl = max(0, min(tb - lgL, lgS))
+    if yl > 1:                       # small grids: balance row tiles and high-pass tiles
+
+        def min_ctas(y):
+            lo = 1 << max(lgL + lgS - (lgL + y), 0)
+            nl = lgS - y
+            if nl <= 0:
+                return lo
+            cb = min(lgL + y, 4)
+            npass = _ceil_div(nl, 10)
+            umax = _ceil_div(nl, npass)
+            return min(lo, 1 << max(lgL + lgS - (umax + cb), 0))
+
+        if min_ctas(yl) < 2 * 148:
+            best = yl
+            for y in range(yl - 1, 0, -1):
+                if min_ctas(y) > min_ctas(best):
+                    best = y
+            yl = best
     high = []
     nlev = lgS - yl
     if nlev > 0:
