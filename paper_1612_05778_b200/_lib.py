@@ -15,7 +15,8 @@ import numpy as np
 
 from .errors import DeviceError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtcgpu.so")
+LIB_PATH = os.environ.get("TC_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                          "libtcgpu.so")   # override: A/B builds (tools/)
 TC_MAX_PRIMES = 16
 
 TC_OK = 0

@@ -102,6 +102,7 @@ struct Ctx {
     cudaStream_t aux = nullptr;          // H2D of operand B and the chunked D2H of the product
     cudaEvent_t xev[24] = {};            // cross-stream events of tc_multiply_host: 0 A up, 1 widths back, 2.. chunks, 20 B up, 21 A width
     int* hinfo = nullptr;                // pinned: widths read back early
+    cudaEvent_t fev[2] = {};             // fork / join of the resident pipeline's two branches
 };
 
 int ilog2(int64_t x) { int l = 0; while ((1ll << l) < x) ++l; return l; }
@@ -339,7 +340,8 @@ int make_geometry(const tc_plan_t* pl, Geometry& G, int world = 1) {
 }
 
 int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* words, int64_t d, int cw,
-               int check_range, uint32_t* grids, const ShardArgs& sh) {
+               int check_range, uint32_t* grids, const ShardArgs& sh, cudaStream_t stream = nullptr) {
+    cudaStream_t st = stream ? stream : c->st;
     LowArgs a{};
     a.sh = sh;
     a.src.words = words; a.src.d = d; a.src.cw = cw;
@@ -358,13 +360,13 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     const int lt = env_int("TC_LOW_THREADS", 0);
     if (smem > 112 * 1024 || lt >= 1024) {
         CK(ensure_smem((const void*)k_low<1024>, smem));
-        k_low<1024><<<(unsigned)ctas, 1024, smem, c->st>>>(a);
+        k_low<1024><<<(unsigned)ctas, 1024, smem, st>>>(a);
     } else if (lt == 256 || lt == 0) {            // 256 threads: measured faster (C2 0.268 -> 0.228 ms)
         CK(ensure_smem((const void*)k_low<256>, smem));
-        k_low<256><<<(unsigned)ctas, 256, smem, c->st>>>(a);
+        k_low<256><<<(unsigned)ctas, 256, smem, st>>>(a);
     } else {
         CK(ensure_smem((const void*)k_low<512>, smem));
-        k_low<512><<<(unsigned)ctas, 512, smem, c->st>>>(a);
+        k_low<512><<<(unsigned)ctas, 512, smem, st>>>(a);
     }
     c->launches++;
     CKL();
@@ -571,7 +573,26 @@ int enqueue_pipeline(Ctx* c, const tc_plan_t* pl, const Geometry& G, int a_bits,
     const int nh = (int)G.high.size();
     int64_t l0 = c->launches;
 
+    // graph path: two branches, k_low(A) -> A's forward passes on the main
+    // stream and k_low(B) on the aux stream, joined before B's passes -- the
+    // kernels fill each other's last partial wave of CTAs.  Stage-timed runs
+    // (ev) keep one stream so the stage events bracket whole stages.
+    static const int fork_env = env_int("TC_FORK", 1);
+    const bool fork = !ev && fork_env;
     if (ev) CK(cudaEventRecord(c->ev[0], c->st));
+    if (fork) {
+        CK(cudaEventRecord(c->fev[0], c->st));
+        CK(cudaStreamWaitEvent(c->aux, c->fev[0], 0));
+        if ((rc = launch_low(c, G, pl, c->b_dev, c->db, c->b_cw, b_bits > pl->N, GB, one, c->aux))) return rc;
+        CK(cudaEventRecord(c->fev[1], c->aux));
+        if ((rc = launch_low(c, G, pl, c->a_dev, c->da, c->a_cw, a_bits > pl->N, GA, one))) return rc;
+        for (int i = 0; i < nh; ++i)
+            if ((rc = launch_high(c, MODE_FWD, G, GA, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
+        CK(cudaStreamWaitEvent(c->st, c->fev[1], 0));
+        for (int i = 0; i + 1 < nh; ++i)
+            if ((rc = launch_high(c, MODE_FWD, G, GB, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
+        l0 = c->launches;
+    } else {
     if ((rc = launch_low(c, G, pl, c->a_dev, c->da, c->a_cw, a_bits > pl->N, GA, one))) return rc;
     if ((rc = launch_low(c, G, pl, c->b_dev, c->db, c->b_cw, b_bits > pl->N, GB, one))) return rc;
     c->stage_launches[0] = c->launches - l0; l0 = c->launches;
@@ -581,6 +602,7 @@ int enqueue_pipeline(Ctx* c, const tc_plan_t* pl, const Geometry& G, int a_bits,
     for (int i = 0; i + 1 < nh; ++i)
         if ((rc = launch_high(c, MODE_FWD, G, GB, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
     c->stage_launches[1] = c->launches - l0; l0 = c->launches;
+    }
     if (ev) CK(cudaEventRecord(c->ev[2], c->st));
     if (nh > 0) rc = launch_high(c, MODE_MID, G, GB, GA, G.high[nh - 1].first, G.high[nh - 1].second, one);
     else rc = launch_high(c, MODE_MID, G, GB, GA, G.lgS, 0, one);
@@ -678,6 +700,7 @@ int tc_ctx_create(int device, void** out) {
     if (e != cudaSuccess) { delete c; return set_err(TC_ERR_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e)); }
     for (auto& ev : c->ev) cudaEventCreate(&ev);
     for (auto& ev : c->xev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    for (auto& ev : c->fev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking);
     cudaHostAlloc((void**)&c->hinfo, 64, cudaHostAllocDefault);
     *out = c;
@@ -695,6 +718,7 @@ int tc_ctx_destroy(void* ctx) {
     for (auto& ev : c->ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : c->user_ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : c->xev) if (ev) cudaEventDestroy(ev);
+    for (auto& ev : c->fev) if (ev) cudaEventDestroy(ev);
     if (c->aux) { cudaStreamSynchronize(c->aux); cudaStreamDestroy(c->aux); }
     if (c->hinfo) cudaFreeHost(c->hinfo);
     c->flush.release();

@@ -58,6 +58,12 @@ constexpr int kMaxPrimes = 16;
 #ifndef TC_CO_KW
 #define TC_CO_KW 4          // ConvertOut words per thread (8: C2 +16 %; 2: C2 +2 %, C4 -12 %)
 #endif
+#ifndef TC_HIGH_ASYNC
+#define TC_HIGH_ASYNC 0     // k_high_ct: whole-tile cp.async loads (all in flight) instead of LDG batches
+#endif
+#ifndef TC_MID_BATCH
+#define TC_MID_BATCH 8      // k_high_ct MID: 16-byte loads of A in flight per thread (8: C2 MID 168 -> 157 us)
+#endif
 #ifndef TC_ROUND_G2
 #define TC_ROUND_G2 1       // interleave two register groups per round when each thread owns >= 2
 #endif
@@ -1213,6 +1219,15 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (NT <= 256 ? TC_HIGH_MINB :
         mid = ((y & ((1u << rbits) - 1)) << (A.sh.TB - CB)) | (A.sh.m0 + pml);
         hi = y >> rbits;
     }
+    const uint32_t base = (hi << (b0 + U)) | (mid << CB);
+    constexpr uint32_t cmask = (1u << CB) - 1;
+    const HighIdx hidx = sharded
+        ? HighIdx{((base >> A.sh.TB) << A.sh.lchunk) | (pml << CB), CB, b0 - A.sh.TB + A.sh.lchunk, cmask}
+        : HighIdx{base, CB, b0, cmask};
+#if TC_HIGH_ASYNC
+    for (uint32_t e = threadIdx.x; e < n; e += NT) cp_async4(s + padi(e), g + hidx(e));   // all in flight
+    cp_async_commit();
+#endif
     // CTA twiddles (requires lgL >= CB: the row bits below u0 come from mid only)
     {
         const uint32_t rb = mid >> (A.lgL - CB);
@@ -1226,27 +1241,27 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (NT <= 256 ? TC_HIGH_MINB :
             if (MODE != MODE_FWD) stw_i[i] = __ldg(twi + gi);
         }
     }
-    const uint32_t base = (hi << (b0 + U)) | (mid << CB);
-    constexpr uint32_t cmask = (1u << CB) - 1;
-    const HighIdx hidx = sharded
-        ? HighIdx{((base >> A.sh.TB) << A.sh.lchunk) | (pml << CB), CB, b0 - A.sh.TB + A.sh.lchunk, cmask}
-        : HighIdx{base, CB, b0, cmask};
+#if TC_HIGH_ASYNC
+    cp_async_wait<0>();
+#else
     tile_load(s, g, n, hidx);
+#endif
     __syncthreads();
     if (MODE == MODE_FWD || MODE == MODE_MID) ct_pass<U, false, NT>(s, stw_f, pc.p, pc.two_p);
     if (MODE == MODE_MID) {
         const uint32_t* ga = A.other + (int64_t)q * qstride;
         constexpr uint32_t nv = n >> 2;
 #pragma unroll 1
-        for (uint32_t v0 = threadIdx.x; v0 < nv; v0 += 4 * NT) {
-            uint4 y[4];
+        constexpr int MB = TC_MID_BATCH;
+        for (uint32_t v0 = threadIdx.x; v0 < nv; v0 += MB * NT) {
+            uint4 y[MB];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < MB; ++k) {
                 const uint32_t vi = v0 + k * NT;
                 y[k] = vi < nv ? *reinterpret_cast<const uint4*>(ga + hidx(vi << 2)) : make_uint4(0, 0, 0, 0);
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < MB; ++k) {
                 const uint32_t vi = v0 + k * NT;
                 if (vi < nv) {
                     uint32_t* d = s + padi(vi << 2);
