@@ -43,6 +43,7 @@ extern "C" {
 #define TC_ERR_EMPTY     8  /* EmptyInputError: a zero polynomial (tc/params.py:288-289) */
 
 #define TC_MAX_PRIMES 16
+#define TC_MAX_DIGIT_BITS 126   /* M > 63: two-word digits (the paper allows 1-3 words) */
 
 /*
  * One multiplication plan, produced by the host planner
@@ -56,7 +57,7 @@ typedef struct {
     int64_t d;        /* max(da, db)                                          */
     int64_t N;        /* padded coefficient width, N = K*M                    */
     int64_t K;        /* digits per coefficient, power of two, 1 <= K <= 2^14 */
-    int64_t M;        /* digit width in bits, 2 <= M <= 63                    */
+    int64_t M;        /* digit width in bits, 2 <= M <= TC_MAX_DIGIT_BITS      */
     int64_t s_y;      /* least power of two >= 2d-1                           */
     int32_t P;        /* number of word primes, 1..TC_MAX_PRIMES              */
     int32_t flags;    /* 0; bit 0 = fault injection for tests: the residue of product

@@ -151,7 +151,8 @@ int validate_plan(const tc_plan_t* pl, int64_t da, int64_t db) {
     int64_t d = da > db ? da : db;
     if (pl->d != d) return set_err(TC_ERR_BAD_ARG, "plan.d=%lld but max(da,db)=%lld", (long long)pl->d, (long long)d);
     if (!is_pow2(pl->K) || pl->K > (1 << 14)) return set_err(TC_ERR_BAD_ARG, "K=%lld must be a power of two <= 2^14", (long long)pl->K);
-    if (pl->M < 2 || pl->M > 63) return set_err(TC_ERR_BAD_ARG, "M=%lld outside [2, 63]", (long long)pl->M);
+    if (pl->M < 2 || pl->M > TC_MAX_DIGIT_BITS)
+        return set_err(TC_ERR_BAD_ARG, "M=%lld outside [2, %d]", (long long)pl->M, TC_MAX_DIGIT_BITS);
     if (pl->N != pl->K * pl->M) return set_err(TC_ERR_BAD_ARG, "N != K*M");
     if (!is_pow2(pl->s_y) || pl->s_y < 2 * d - 1 || (pl->s_y > 1 && pl->s_y / 2 >= 2 * d - 1))
         return set_err(TC_ERR_BAD_ARG, "s_y=%lld is not the least power of two >= 2d-1", (long long)pl->s_y);
@@ -208,6 +209,7 @@ PrimeC make_prime_const(uint32_t p, int64_t S) {
     pc.pinv_neg = (uint32_t)(0u - inv);
     const uint64_t r32 = (1ull << 32) % p;
     pc.c64 = (uint32_t)(r32 * r32 % p);
+    pc.c96 = (uint32_t)(r32 * r32 % p * r32 % p);
     pc.one_sh = (uint32_t)((1ull << 32) / p);
     const uint64_t sinv = inv_mod((uint32_t)(S % p), p);
     pc.scale = (uint32_t)(sinv * r32 % p);
@@ -293,6 +295,7 @@ int make_geometry(const tc_plan_t* pl, Geometry& G, int world = 1) {
     // (2^(4+U) slots) share out the grid; when the default leaves fewer than
     // two waves (2 x 148 CTAs) on either side, take the yl in [1, yl] that
     // maximises the smaller CTA count (params.pass_layout mirrors this)
+    static const int bal_p = env_int("TC_BAL_P", 1);
     if (world == 1 && yl > 1) {
         auto min_ctas = [&](int y) -> int64_t {
             const int64_t lo = G.S >> (G.lgL + y);
@@ -300,7 +303,7 @@ int make_geometry(const tc_plan_t* pl, Geometry& G, int world = 1) {
             if (nl <= 0) return lo;
             const int cb = G.lgL + y < 4 ? G.lgL + y : 4;
             const int np = (nl + 9) / 10, umax = (nl + np - 1) / np;
-            const int64_t hi = G.S >> (umax + cb);
+            const int64_t hi = (G.S >> (umax + cb)) * (bal_p ? G.P : 1);   // high-pass grid: tiles x primes
             return lo < hi ? lo : hi;
         };
         if (min_ctas(yl) < 2 * 148) {
@@ -354,7 +357,7 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     a.pcs = c->pcs.as<PrimeC>(); a.P = G.P;
     const int Rc = G.yl >= 1 ? 1 << (G.yl - 1) : 1;      // computed (even) rows, see k_low
     const uint32_t n = 1u << (G.lgL + G.yl);
-    const size_t smem = (size_t)Rc * G.K * 8 + (size_t)Rc * 8 + (size_t)padded_words(n) * 4;
+    const size_t smem = (size_t)Rc * G.K * (pl->M > 63 ? 16 : 8) + (size_t)Rc * 8 + (size_t)padded_words(n) * 4;
     const int64_t ctas = sh.world > 1 ? sh.Tl : G.S / n;
     // a tile too large for two CTAs per SM gets 32 warps in one CTA
     const int lt = env_int("TC_LOW_THREADS", 0);

@@ -24,7 +24,7 @@ struct PrimeC {
     uint32_t one_sh;     // floor(2^32 / p): Shoup companion of 1
     uint32_t scale;      // (s_y * L)^{-1} * 2^32 mod p, applied after the Montgomery pointwise product
     uint32_t scale_sh;   // Shoup companion of scale
-    uint32_t pad;
+    uint32_t c96;        // 2^96 mod p (residues of two-word digits, M > 63)
 };
 
 // a * w mod p for a fixed w with companion wsh = floor(w * 2^32 / p).
@@ -68,12 +68,26 @@ __device__ __forceinline__ void bfly_dit(uint32_t& x, uint32_t& y, uint32_t w, u
     y = u - v + two_p;
 }
 
-// |digit| mod p for a signed 64-bit balanced digit, canonical.
+// a mod p, canonical, for any 64-bit a.
+__device__ __forceinline__ uint32_t u64_mod(uint64_t a, const PrimeC& c) {
+    const uint32_t r = mont_mul((uint32_t)(a >> 32), c.c64, c.p, c.pinv_neg) + shoup_mul((uint32_t)a, 1u, c.one_sh, c.p);
+    return canon(r, c.p);
+}
+
+// |digit| mod p for a signed balanced digit (one word, M <= 63), canonical.
 __device__ __forceinline__ uint32_t digit_residue(int64_t dg, const PrimeC& c) {
-    uint64_t a = dg < 0 ? (uint64_t)(-(dg + 1)) + 1 : (uint64_t)dg;
-    uint32_t hi = (uint32_t)(a >> 32), lo = (uint32_t)a;
-    uint32_t r = mont_mul(hi, c.c64, c.p, c.pinv_neg) + shoup_mul(lo, 1u, c.one_sh, c.p);
-    r = canon(r, c.p);
+    const uint64_t a = dg < 0 ? (uint64_t)(-(dg + 1)) + 1 : (uint64_t)dg;
+    uint32_t r = u64_mod(a, c);
+    if (dg < 0 && r) r = c.p - r;
+    return r;
+}
+
+// The same for a two-word digit (64 <= M <= 126): lo + hi * 2^64, the high
+// part through a Montgomery product with 2^96 mod p.
+__device__ __forceinline__ uint32_t digit_residue(__int128 dg, const PrimeC& c) {
+    const unsigned __int128 a = dg < 0 ? (unsigned __int128)(-(dg + 1)) + 1 : (unsigned __int128)dg;
+    const uint32_t lo = u64_mod((uint64_t)a, c), hi = u64_mod((uint64_t)(a >> 64), c);
+    uint32_t r = canon(lo + mont_mul(hi, c.c96, c.p, c.pinv_neg), c.p);
     if (dg < 0 && r) r = c.p - r;
     return r;
 }

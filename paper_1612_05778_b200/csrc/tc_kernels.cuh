@@ -246,14 +246,33 @@ __device__ __forceinline__ uint64_t limb_at(const uint64_t* row, int cw, int64_t
 
 struct DigitScratch { uint32_t warp_tf[32]; uint32_t warp_cin[32]; uint32_t round_carry; };
 
+// Digit types: int64_t for M <= 63, __int128 (two words) for 64 <= M <= 126.
+template <class DT> struct DigitTraits;
+template <> struct DigitTraits<int64_t> { using U = uint64_t; };
+template <> struct DigitTraits<__int128> { using U = unsigned __int128; };
+
+// Bits [wr, wr + M) of the little-endian words from word wq on (wr < 64),
+// word(k) yielding the sign extension past the row.
+template <class U, class WF>
+__device__ __forceinline__ U digit_chunk(const WF& word, int64_t wq, int wr, int M, U mask) {
+    U c = (U)word(wq) >> wr;
+    if (wr + M > 64) c |= (U)word(wq + 1) << (64 - wr);
+    if constexpr (sizeof(U) > 8) {
+        if (wr + M > 128) c |= (U)word(wq + 2) << (128 - wr);
+    }
+    return c & mask;
+}
+
 // coeff[r] (r < R) is the coefficient index held by tile row r, or -1.
-static __device__ void compute_digits(const DigitSrc& a, int R, const int64_t* coeff, int64_t* dig,
+template <class DT>
+static __device__ void compute_digits(const DigitSrc& a, int R, const int64_t* coeff, DT* dig,
                                DigitScratch& ds) {
+    using U = typename DigitTraits<DT>::U;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const int M = a.M;
-    const uint64_t half = 1ull << (M - 1);
-    const uint64_t beta = 1ull << M;
-    const uint64_t mask = beta - 1;
+    const U half = (U)1 << (M - 1);
+    const U beta = (U)1 << M;
+    const U mask = beta - 1;
     const int64_t sq = (a.N - 1) >> 6;
     const int sr = (int)((a.N - 1) & 63);
     const int64_t ndig = (int64_t)R * a.K;
@@ -281,17 +300,14 @@ static __device__ void compute_digits(const DigitSrc& a, int R, const int64_t* c
         const int64_t j = idx & (a.K - 1);
         const int64_t ci = (idx < ndig) ? coeff[r] : -1;
         const bool active = ci >= 0;
-        uint64_t chunk = 0;
+        U chunk = 0;
         bool neg = false;
         if (active) {
             const uint64_t* row = a.words + ci * a.cw;
             const uint64_t signw = (row[a.cw - 1] >> 63) ? ~0ull : 0ull;
             const int64_t off = j * M;
-            const int64_t wq = off >> 6;
-            const int wr = (int)(off & 63);
-            chunk = limb_at(row, a.cw, wq, signw) >> wr;
-            if (wr + M > 64) chunk |= limb_at(row, a.cw, wq + 1, signw) << (64 - wr);
-            chunk &= mask;
+            auto word = [&](int64_t k) -> uint64_t { return limb_at(row, a.cw, k, signw); };
+            chunk = digit_chunk<U>(word, off >> 6, (int)(off & 63), M, mask);
             neg = (limb_at(row, a.cw, sq, signw) >> sr) & 1;
         }
         const bool top = (j == a.K - 1);
@@ -306,16 +322,16 @@ static __device__ void compute_digits(const DigitSrc& a, int R, const int64_t* c
         const uint64_t cin = ds.warp_cin[warp];
         const uint32_t carries = (uint32_t)((A + B + cin) ^ A ^ B);
         if (active) {
-            const uint64_t cu = chunk + ((carries >> lane) & 1u);
-            int64_t dg;
+            const U cu = chunk + ((carries >> lane) & 1u);
+            DT dg;
             if (!top) {
-                dg = cu >= half ? -(int64_t)(beta - cu) : (int64_t)cu;
+                dg = cu >= half ? -(DT)(beta - cu) : (DT)cu;
             } else if (neg) {
                 if (cu < half) atomicMin(&a.err[0], (int)min(ci, (int64_t)0x7fffffff));
-                dg = -(int64_t)(beta - cu);
+                dg = -(DT)(beta - cu);
             } else {
                 if (cu >= half) atomicMin(&a.err[0], (int)min(ci, (int64_t)0x7fffffff));
-                dg = (int64_t)cu;
+                dg = (DT)cu;
             }
             dig[idx] = dg;
         }
@@ -328,11 +344,13 @@ static __device__ void compute_digits(const DigitSrc& a, int R, const int64_t* c
 // digits per thread: thread-local generate/propagate transfer, one warp
 // ballot add and one cross-warp scan for the whole tile (one barrier pair,
 // instead of two per blockDim digits).  Ends with a barrier (sw is reusable).
-static __device__ void compute_digits_staged(const DigitSrc& a, int R, const int64_t* coeff, int64_t* dig,
+template <class DT>
+static __device__ void compute_digits_staged(const DigitSrc& a, int R, const int64_t* coeff, DT* dig,
                                              DigitScratch& ds, uint64_t* sw) {
+    using U = typename DigitTraits<DT>::U;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const int M = a.M, cw = a.cw;
-    const uint64_t half = 1ull << (M - 1), beta = 1ull << M, mask = beta - 1;
+    const U half = (U)1 << (M - 1), beta = (U)1 << M, mask = beta - 1;
     const int64_t sq = (a.N - 1) >> 6;
     const int sr = (int)((a.N - 1) & 63);
     if (tid == 0) ds.round_carry = 0;
@@ -362,14 +380,12 @@ static __device__ void compute_digits_staged(const DigitSrc& a, int R, const int
     const int64_t ndig = (int64_t)R * a.K;
     const int D = (int)((ndig + blockDim.x - 1) / blockDim.x);
     const int64_t t0 = (int64_t)tid * D;
-    auto chunk_of = [&](int r, int64_t j) -> uint64_t {
-        if (coeff[r] < 0) return 0ull;
+    auto chunk_of = [&](int r, int64_t j) -> U {
+        if (coeff[r] < 0) return (U)0;
         const uint64_t* row = sw + (int64_t)r * cw;
-        const int64_t off = j * M, wq = off >> 6;
-        const int wr = (int)(off & 63);
-        uint64_t c = word(row, wq) >> wr;
-        if (wr + M > 64) c |= word(row, wq + 1) << (64 - wr);
-        return c & mask;
+        const int64_t off = j * M;
+        auto wf = [&](int64_t k) -> uint64_t { return word(row, k); };
+        return digit_chunk<U>(wf, off >> 6, (int)(off & 63), M, mask);
     };
     uint32_t c0 = 0, c1 = 1;                  // carry out of this thread's digits for carry in 0 / 1
     for (int i = 0; i < D; ++i) {
@@ -378,7 +394,7 @@ static __device__ void compute_digits_staged(const DigitSrc& a, int R, const int
         const int r = (int)(t >> a.lgK);
         const int64_t j = t & (a.K - 1);
         const bool top = j == a.K - 1;
-        const uint64_t ch = chunk_of(r, j);
+        const U ch = chunk_of(r, j);
         const uint32_t g = !top && ch >= half, p = !top && ch == half - 1;
         c0 = g | (p & c0);
         c1 = g | (p & c1);
@@ -398,18 +414,18 @@ static __device__ void compute_digits_staged(const DigitSrc& a, int R, const int
         const int64_t j = t & (a.K - 1);
         const int64_t ci = coeff[r];
         const bool top = j == a.K - 1;
-        const uint64_t ch = chunk_of(r, j);
+        const U ch = chunk_of(r, j);
         if (ci >= 0) {
-            const uint64_t cu = ch + c;
-            int64_t dg;
+            const U cu = ch + c;
+            DT dg;
             if (!top) {
-                dg = cu >= half ? -(int64_t)(beta - cu) : (int64_t)cu;
+                dg = cu >= half ? -(DT)(beta - cu) : (DT)cu;
             } else if ((word(sw + (int64_t)r * cw, sq) >> sr) & 1) {
                 if (cu < half) atomicMin(&a.err[0], (int)min(ci, (int64_t)0x7fffffff));
-                dg = -(int64_t)(beta - cu);
+                dg = -(DT)(beta - cu);
             } else {
                 if (cu >= half) atomicMin(&a.err[0], (int)min(ci, (int64_t)0x7fffffff));
-                dg = (int64_t)cu;
+                dg = (DT)cu;
             }
             dig[t] = dg;
         }
@@ -428,7 +444,7 @@ static __global__ void __launch_bounds__(256) k_digits(DigitSrc a, int R, int64_
     const int64_t r0 = (int64_t)blockIdx.x * R;
     for (int r = threadIdx.x; r < R; r += blockDim.x) coeff[r] = r0 + r < a.d ? r0 + r : -1;
     __syncthreads();
-    compute_digits(a, R, coeff, dig, ds);
+    compute_digits<int64_t>(a, R, coeff, dig, ds);
     const int64_t nrows = min((int64_t)R, a.d - r0);
     for (int64_t idx = threadIdx.x; idx < nrows * a.K; idx += blockDim.x) out[r0 * a.K + idx] = dig[idx];
 }
@@ -908,8 +924,10 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
     const int tile_bits = A.lgL + A.yl;
     const int cbits = tile_bits - (prune ? 1 : 0);
     const uint32_t n = 1u << tile_bits, nc = 1u << cbits;
+    const bool wide = A.src.M > 63;                         // two-word digits
     int64_t* dig = reinterpret_cast<int64_t*>(smem_raw);
-    int64_t* coeff = dig + (int64_t)Rc * A.src.K;
+    __int128* dig2 = reinterpret_cast<__int128*>(smem_raw);
+    int64_t* coeff = dig + (int64_t)Rc * A.src.K * (wide ? 2 : 1);
     uint32_t* tile = reinterpret_cast<uint32_t*>(coeff + Rc);
     __shared__ DigitScratch ds;
     __shared__ int s_nvalid;
@@ -936,10 +954,14 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
         return;
     }
     // coefficient words staged in the (not yet used) tile buffer when they fit
-    if ((int64_t)Rc * A.src.cw * 8 <= (int64_t)padded_words(n) * 4)
-        compute_digits_staged(A.src, Rc, coeff, dig, ds, reinterpret_cast<uint64_t*>(tile));
-    else
-        compute_digits(A.src, Rc, coeff, dig, ds);
+    const bool staged = (int64_t)Rc * A.src.cw * 8 <= (int64_t)padded_words(n) * 4;
+    if (!wide) {
+        if (staged) compute_digits_staged<int64_t>(A.src, Rc, coeff, dig, ds, reinterpret_cast<uint64_t*>(tile));
+        else compute_digits<int64_t>(A.src, Rc, coeff, dig, ds);
+    } else {
+        if (staged) compute_digits_staged<__int128>(A.src, Rc, coeff, dig2, ds, reinterpret_cast<uint64_t*>(tile));
+        else compute_digits<__int128>(A.src, Rc, coeff, dig2, ds);
+    }
     for (int q = 0; q < A.P; ++q) {
         const PrimeC pc = A.pcs[q];
         const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
@@ -953,7 +975,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
                 const uint32_t e = (r << A.lgL) | j;
                 uint32_t x = 0, y = 0;
                 if (coeff[r] >= 0) {
-                    x = digit_residue(dig[t], pc);
+                    x = wide ? digit_residue(dig2[t], pc) : digit_residue(dig[t], pc);
                     const uint2 w = __ldg(wtop + j);
                     y = shoup_mul(x, w.x, w.y, pc.p);
                 }
@@ -1251,8 +1273,8 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (NT <= 256 ? TC_HIGH_MINB :
     if (MODE == MODE_MID) {
         const uint32_t* ga = A.other + (int64_t)q * qstride;
         constexpr uint32_t nv = n >> 2;
-#pragma unroll 1
         constexpr int MB = TC_MID_BATCH;
+#pragma unroll 1
         for (uint32_t v0 = threadIdx.x; v0 < nv; v0 += MB * NT) {
             uint4 y[MB];
 #pragma unroll

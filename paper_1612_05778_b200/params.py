@@ -29,6 +29,7 @@ from .zpoly import IntPolynomial, _int_from_words, row_widths, twos_complement_w
 
 WORD_BITS = 64
 MAX_DIGIT_BITS = 63                  # tc/params.py:20-22
+MAX_GPU_DIGIT_BITS = 126             # GPU plans: two-word digits (TC_MAX_DIGIT_BITS, include/tc_api.h)
 GRID_REBALANCE_THRESHOLD = 1 << 18   # tc/params.py:24-27
 MAX_PRIMES = 16                      # TC_MAX_PRIMES, include/tc_api.h
 MAX_K = 1 << 13                      # one x-row (L = 2K) of a CTA fits shared memory
@@ -252,7 +253,7 @@ def pass_layout(lgL: int, lgS: int, P: int):
             cb = min(lgL + y, 4)
             npass = _ceil_div(nl, 10)
             umax = _ceil_div(nl, npass)
-            return min(lo, 1 << max(lgL + lgS - (umax + cb), 0))
+            return min(lo, P << max(lgL + lgS - (umax + cb), 0))     # high-pass grid: tiles x primes
 
         if min_ctas(yl) < 2 * 148:
             best = yl
@@ -309,9 +310,14 @@ def plan_gpu(d: int, dmin: int, n_in: int, K: int | None = None, M: int | None =
     best = None
     for k in cands:
         m = M if M else min_digit_bits(k, n_in)
-        if K is None and (m > MAX_DIGIT_BITS or k > MAX_K):
+        if K is None and (m > MAX_GPU_DIGIT_BITS or k > MAX_K):
             continue
-        if m > MAX_DIGIT_BITS or m < 2 or k > MAX_K:
+        # two-word digits trade primes for per-slot CRT / ConvertIn work; they
+        # pay on grids of >= 2^20 slots per prime (B200: C2 -8 %, C3 -6 %,
+        # C4 -9 %, C5 -5 %) but not on latency-bound small ones (C1 +8 %)
+        if K is None and M is None and m > MAX_DIGIT_BITS and s_y * 2 * k < (1 << 20):
+            continue
+        if m > MAX_GPU_DIGIT_BITS or m < 2 or k > MAX_K:
             raise ValueError(f"unsupported digit split K={k} M={m}")
         primes = _primes_for_bound(2 * (dmin * k << (2 * m - 2)), max(s_y, 2 * k))
         if primes is None:

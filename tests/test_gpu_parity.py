@@ -364,6 +364,27 @@ def test_extreme_plans(oracle):
         tc.multiply_with_plan(tc.MulRequest(a, a), K=2, M=63)
 
 
+def test_two_word_digits(oracle):
+    # 64 <= M <= 126: digits of two words (planner's choice for C1/C2/C3/C5
+    # widths); random, extreme (most negative, all-ones) and mixed-width
+    # operands against the oracle, and the digit-capacity EncodingError
+    rng = random.Random(6565)
+    cases = [(40, 33, 129, dict(K=2, M=65)), (300, 300, 1025, dict(K=16, M=65)), (128, 100, 4000, dict(K=64, M=64)),
+             (64, 64, 2000, dict(K=16, M=126)), (500, 20, 700, dict(K=8, M=90)), (7, 9, 8193, dict(K=128, M=65)),
+             (256, 256, 1025, dict(K=16, M=65)), (3, 2, 126, dict(K=1, M=126)), (1000, 1000, 65, dict(K=1, M=65))]
+    for da, db, nbits, kw in cases:
+        for extremes in (False, True):
+            a = _random_poly(rng, da, nbits, extremes=extremes)
+            b = _random_poly(rng, db, max(2, nbits - rng.randrange(0, 60)), extremes=extremes)
+            out, _, plan = tc.multiply_with_plan(tc.MulRequest(a, b), **kw)
+            assert plan.M > 63, plan.describe()
+            exp, bits = oracle.multiply_words(a.words, a.bit_width, b.words, b.bit_width)
+            assert out.bit_width == bits and np.array_equal(out.words, exp), (da, db, nbits, plan.describe())
+    a = _random_poly(rng, 8, 300, extremes=True)
+    with pytest.raises(tc.EncodingError):
+        tc.multiply_with_plan(tc.MulRequest(a, a), K=2, M=100)
+
+
 def test_plan_sweep(oracle):
     # every transform length 2K = 2 .. 2^14 (the compile-time x schedules, the
     # fused twist / duplication rounds, k_high_ct / generic passes), degrees

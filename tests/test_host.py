@@ -99,7 +99,7 @@ def test_gpu_plan_invariants():
     for d, n_in in shapes:
         dmin = rng.randint(1, d)
         pl = params.plan_gpu(d, dmin, n_in)
-        assert pl.K & (pl.K - 1) == 0 and 1 <= pl.K <= params.MAX_K and 2 <= pl.M <= 63
+        assert pl.K & (pl.K - 1) == 0 and 1 <= pl.K <= params.MAX_K and 2 <= pl.M <= params.MAX_GPU_DIGIT_BITS
         lo, hi = params.balanced_capacity(pl.K, pl.M)
         assert lo <= -(1 << (n_in - 1)) and (1 << (n_in - 1)) - 1 <= hi
         prod = 1

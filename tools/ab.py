@@ -32,7 +32,9 @@ info = _lib.TcInputInfo()
 lib.tc_stage_inputs(h, d_a, da, aw.shape[1], d_b, db, bw.shape[1], 1, ctypes.byref(info))
 n_in = max(info.n_in_a, info.n_in_b); out_bits = output_bit_width(max(da, db), n_in); out_cw = -(-out_bits // 64)
 d_out = dalloc(rows * out_cw * 8)
-cp = _lib.make_plan(plan_gpu(max(da, db), min(da, db), n_in))
+km = os.environ.get("AB_KM")          # explicit digit split "K,M"
+kw = dict(zip(("K", "M"), map(int, km.split(",")))) if km else {}
+cp = _lib.make_plan(plan_gpu(max(da, db), min(da, db), n_in, **kw))
 def step():
     lib.tc_stage_inputs(h, d_a, da, aw.shape[1], d_b, db, bw.shape[1], 1, None)
     err = ctypes.c_int64(-1)
