@@ -376,21 +376,21 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     return TC_OK;
 }
 
-template <int NT, int U, int MODE>
+template <int NT, int U, int MODE, int CB>
 cudaError_t launch_high_ct_mode(const HighArgs& A, dim3 grid, uint32_t n, cudaStream_t st) {
     const size_t smem = (size_t)ct_tw_offset_words(n) * 4 + (MODE == MODE_MID ? 2 : 1) * ((size_t)8 << U);
     cudaError_t e = cudaSuccess;
-    e = ensure_smem((const void*)k_high_ct<MODE, NT, U>, smem);
+    e = ensure_smem((const void*)k_high_ct<MODE, NT, U, CB>, smem);
     if (e != cudaSuccess) return e;
-    k_high_ct<MODE, NT, U><<<grid, NT, smem, st>>>(A);
+    k_high_ct<MODE, NT, U, CB><<<grid, NT, smem, st>>>(A);
     return cudaGetLastError();
 }
 
-template <int NT, int U>
+template <int NT, int U, int CB = 4>
 cudaError_t launch_high_ct(int mode, const HighArgs& A, dim3 grid, uint32_t n, cudaStream_t st) {
-    if (mode == MODE_FWD) return launch_high_ct_mode<NT, U, MODE_FWD>(A, grid, n, st);
-    if (mode == MODE_INV) return launch_high_ct_mode<NT, U, MODE_INV>(A, grid, n, st);
-    return launch_high_ct_mode<NT, U, MODE_MID>(A, grid, n, st);
+    if (mode == MODE_FWD) return launch_high_ct_mode<NT, U, MODE_FWD, CB>(A, grid, n, st);
+    if (mode == MODE_INV) return launch_high_ct_mode<NT, U, MODE_INV, CB>(A, grid, n, st);
+    return launch_high_ct_mode<NT, U, MODE_MID, CB>(A, grid, n, st);
 }
 
 int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint32_t* other, int u0, int U,
@@ -410,6 +410,7 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
                                : (n >= 16384 ? 512 : (n >= 4096 ? 256 : 64));
     dim3 grid((unsigned)(G.S / n / sh.world), (unsigned)G.P);
     // compile-time pass shapes (k_high_ct): cb = 4, rows below u0 fixed per CTA
+    // (8K-slot tiles with cb = 3 at 4 CTAs per SM measured slower: C2 MID 131 -> 180 us)
     if (A.cb == 4 && G.lgL >= 4 && env_int("TC_HIGH_CT", 1)) {
         cudaError_t e = cudaErrorNotSupported;
         if (U == 10 && nth == 512) e = launch_high_ct<512, 10>(mode, A, grid, n, c->st);
@@ -496,6 +497,18 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
         int rc = ensure_nbias(c, M, G.P, G.L, W32);
         if (rc) return rc;
         A.nbias = c->nbias.as<uint32_t>();
+    }
+    // grouped CRT + ConvertOut (crt_convert_grouped): M = 32 AW + {0, 1}
+    {
+        static const int grouped = env_int("TC_CO_GROUPED", 1);
+        const int aw = M >> 5;
+        const int NA = 3 * aw + G.P + 1;
+        const int64_t u_last = ((int64_t)M * (G.L - 4)) >> 5;
+        if (grouped && !dump && W32 > 0 && G.L >= 4 && (M & 31) <= 1 &&
+            ((aw == 1 && G.P <= 3) || (aw == 2 && G.P >= 2 && G.P <= 8)) && W32 <= u_last + NA)
+            A.co_aw = aw;
+        static const int fused = env_int("TC_CO_FUSED", 0);
+        A.co_fused = fused;
     }
     const uint32_t n = 1u << (G.lgL + G.yl);
     const size_t smem = (size_t)G.P * padded_words(n) * 4;

@@ -29,6 +29,7 @@
 #pragma once
 #include <stdint.h>
 #include <mutex>
+#include <type_traits>
 #include <unordered_map>
 #include "tc_field.cuh"
 
@@ -60,6 +61,9 @@ constexpr int kMaxPrimes = 16;
 #endif
 #ifndef TC_HIGH_ASYNC
 #define TC_HIGH_ASYNC 0     // k_high_ct: whole-tile cp.async loads (all in flight) instead of LDG batches
+#endif
+#ifndef TC_HIGH_BATCH
+#define TC_HIGH_BATCH 4     // k_high_ct: 16-byte tile loads in flight per thread
 #endif
 #ifndef TC_MID_BATCH
 #define TC_MID_BATCH 8      // k_high_ct MID: 16-byte loads of A in flight per thread (8: C2 MID 168 -> 157 us)
@@ -159,18 +163,18 @@ __device__ __forceinline__ void cp_async_wait_dyn(int n) {      // n = pending g
     }
 }
 
-template <class F>
+template <int NBATCH = kBatch, class F>
 __device__ __forceinline__ void tile_load(uint32_t* s, const uint32_t* g, uint32_t n, F gidx) {
     const uint32_t nv = n >> 2, st = blockDim.x;
-    for (uint32_t v0 = threadIdx.x; v0 < nv; v0 += kBatch * st) {
-        uint4 v[kBatch];
+    for (uint32_t v0 = threadIdx.x; v0 < nv; v0 += NBATCH * st) {
+        uint4 v[NBATCH];
 #pragma unroll
-        for (int k = 0; k < kBatch; ++k) {
+        for (int k = 0; k < NBATCH; ++k) {
             const uint32_t vi = v0 + k * st;
             v[k] = vi < nv ? *reinterpret_cast<const uint4*>(g + gidx(vi << 2)) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int k = 0; k < kBatch; ++k) {
+        for (int k = 0; k < NBATCH; ++k) {
             const uint32_t vi = v0 + k * st;
             if (vi < nv) {
                 uint32_t* d = s + padi(vi << 2);
@@ -1121,9 +1125,9 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (NT <= 256 ? TC_HIGH_MINB :
 // gathered once into shared memory: level v' entry a' at index 2^v' + a',
 // = twy[2^(u0+v') + rb + (a' << u0)] (TwHigh's index).
 // ---------------------------------------------------------------------------
-template <int TB, int BL, int NB, bool DIF, int NT>
+template <int TB, int BL, int NB, bool DIF, int NT, int CB>
 __device__ __forceinline__ void ct_round(uint32_t* s, const uint2* stw, uint32_t p, uint32_t two_p) {
-    constexpr int R = 1 << NB, CB = 4;
+    constexpr int R = 1 << NB;
     constexpr uint32_t ngroups = 1u << (TB - NB);
     constexpr uint32_t lowmask = (1u << BL) - 1;
     constexpr bool PERM = BL >= 1 && BL <= 4 && BL >= NB && TB >= 10;
@@ -1163,61 +1167,61 @@ __device__ __forceinline__ void ct_round(uint32_t* s, const uint2* stw, uint32_t
     __syncthreads();
 }
 
-// Round schedule of a pass of U levels on tile bits [4, 4 + U).
-template <int U, bool DIF, int NT>
+// Round schedule of a pass of U levels on tile bits [CB, CB + U).
+template <int U, bool DIF, int NT, int CB>
 __device__ __forceinline__ void ct_pass(uint32_t* s, const uint2* stw, uint32_t p, uint32_t two_p) {
-    constexpr int TB = U + 4;
+    constexpr int TB = U + CB;
 #if TC_CT_R32
     if constexpr (U == 10) {            // two radix-32 rounds (bit 4's half-warps 512 slots apart: no permutation)
         if (!DIF) {
-            ct_round<TB, 4, 5, false, NT>(s, stw, p, two_p);
-            ct_round<TB, 9, 5, false, NT>(s, stw, p, two_p);
+            ct_round<TB, CB, 5, false, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB + 5, 5, false, NT, CB>(s, stw, p, two_p);
         } else {
-            ct_round<TB, 9, 5, true, NT>(s, stw, p, two_p);
-            ct_round<TB, 4, 5, true, NT>(s, stw, p, two_p);
+            ct_round<TB, CB + 5, 5, true, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB, 5, true, NT, CB>(s, stw, p, two_p);
         }
     } else if constexpr (U == 9) {
         if (!DIF) {
-            ct_round<TB, 4, 5, false, NT>(s, stw, p, two_p);
-            ct_round<TB, 9, 4, false, NT>(s, stw, p, two_p);
+            ct_round<TB, CB, 5, false, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB + 5, 4, false, NT, CB>(s, stw, p, two_p);
         } else {
-            ct_round<TB, 9, 4, true, NT>(s, stw, p, two_p);
-            ct_round<TB, 4, 5, true, NT>(s, stw, p, two_p);
+            ct_round<TB, CB + 5, 4, true, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB, 5, true, NT, CB>(s, stw, p, two_p);
         }
     } else {
 #else
     if constexpr (U == 10) {
         if (!DIF) {
-            ct_round<TB, 4, 4, false, NT>(s, stw, p, two_p);
-            ct_round<TB, 8, 3, false, NT>(s, stw, p, two_p);
-            ct_round<TB, 11, 3, false, NT>(s, stw, p, two_p);
+            ct_round<TB, CB, 4, false, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB + 4, 3, false, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB + 7, 3, false, NT, CB>(s, stw, p, two_p);
         } else {
-            ct_round<TB, 11, 3, true, NT>(s, stw, p, two_p);
-            ct_round<TB, 8, 3, true, NT>(s, stw, p, two_p);
-            ct_round<TB, 4, 4, true, NT>(s, stw, p, two_p);
+            ct_round<TB, CB + 7, 3, true, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB + 4, 3, true, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB, 4, true, NT, CB>(s, stw, p, two_p);
         }
     } else if constexpr (U == 9) {
         if (!DIF) {
-            ct_round<TB, 4, 3, false, NT>(s, stw, p, two_p);
-            ct_round<TB, 7, 3, false, NT>(s, stw, p, two_p);
-            ct_round<TB, 10, 3, false, NT>(s, stw, p, two_p);
+            ct_round<TB, CB, 3, false, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB + 3, 3, false, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB + 6, 3, false, NT, CB>(s, stw, p, two_p);
         } else {
-            ct_round<TB, 10, 3, true, NT>(s, stw, p, two_p);
-            ct_round<TB, 7, 3, true, NT>(s, stw, p, two_p);
-            ct_round<TB, 4, 3, true, NT>(s, stw, p, two_p);
+            ct_round<TB, CB + 6, 3, true, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB + 3, 3, true, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB, 3, true, NT, CB>(s, stw, p, two_p);
         }
     } else {
 #endif
         static_assert(U == 4, "unsupported compile-time pass");
-        ct_round<TB, 4, 4, DIF, NT>(s, stw, p, two_p);
+        ct_round<TB, CB, 4, DIF, NT, CB>(s, stw, p, two_p);
     }
 }
 
 __host__ __device__ constexpr uint32_t ct_tw_offset_words(uint32_t n) { return (padded_words(n) + 1) & ~1u; }
 
-template <int MODE, int NT, int U>
-__global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (NT <= 256 ? TC_HIGH_MINB : 2)) k_high_ct(HighArgs A) {
-    constexpr int CB = 4, TB = U + CB;
+template <int MODE, int NT, int U, int CB = 4>
+__global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (CB == 3 ? 4 : (NT <= 256 ? TC_HIGH_MINB : 2))) k_high_ct(HighArgs A) {
+    constexpr int TB = U + CB;
     constexpr uint32_t n = 1u << TB, ntw = 1u << U;
     extern __shared__ __align__(16) uint32_t s[];
     uint2* stw_f = reinterpret_cast<uint2*>(s + ct_tw_offset_words(n));
@@ -1266,10 +1270,10 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (NT <= 256 ? TC_HIGH_MINB :
 #if TC_HIGH_ASYNC
     cp_async_wait<0>();
 #else
-    tile_load(s, g, n, hidx);
+    tile_load<TC_HIGH_BATCH>(s, g, n, hidx);
 #endif
     __syncthreads();
-    if (MODE == MODE_FWD || MODE == MODE_MID) ct_pass<U, false, NT>(s, stw_f, pc.p, pc.two_p);
+    if (MODE == MODE_FWD || MODE == MODE_MID) ct_pass<U, false, NT, CB>(s, stw_f, pc.p, pc.two_p);
     if (MODE == MODE_MID) {
         const uint32_t* ga = A.other + (int64_t)q * qstride;
         constexpr uint32_t nv = n >> 2;
@@ -1299,7 +1303,7 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (NT <= 256 ? TC_HIGH_MINB :
         }
         __syncthreads();
     }
-    if (MODE == MODE_INV || MODE == MODE_MID) ct_pass<U, true, NT>(s, stw_i, pc.p, pc.two_p);
+    if (MODE == MODE_INV || MODE == MODE_MID) ct_pass<U, true, NT, CB>(s, stw_i, pc.p, pc.two_p);
     tile_store(g, s, n, hidx);
 }
 
@@ -1410,7 +1414,213 @@ struct FinalArgs {
     // (rows k*T + x): the host copies it while later chunks compute.
     uint32_t x0; int lgT;
     int64_t inject;                // >= 0: corrupt the residue of flat slot row*L + j (plan.flags)
+    int co_aw;                     // > 0: grouped ConvertOut with M = 32 co_aw + {0, 1} (host-checked)
+    int co_fused;                  // grouped ConvertOut lifts the residues itself (no in-place CRT pass)
 };
+
+// ---------------------------------------------------------------------------
+// Grouped CRT + ConvertOut for M = 32 AW + b, b in {0, 1} (every BASELINE
+// plan: M = 33, 64, 65).  A thread owns G = 4 consecutive terms j0..j0+3 of a
+// row (j0 = 4m): it lifts their residues by CRT straight from the transform
+// tiles and adds each biased P-limb term, shifted, into accumulators of the
+// words from u0 = floor(M j0 / 32) on.  Term j0+i starts at word u0 + AW i
+// with shift r0 + b i (r0 = M j0 mod 32 <= 28: an aligned group never wraps a
+// word), so every accumulator index is a compile-time constant and each limb
+// is read once.  The thread owns words [u0, u(j0+4)) -- AW G of them, or
+// AW G + 1 when the group ends a 32-term block (b = 1) -- and passes its
+// remaining NT = P + 1 - AW word sums to the next group (the next lane; lane
+// 31 through shared memory), with the high half of its last owned word for
+// the next thread's first carry term; the last group of a row owns all its
+// words (host: W32 <= u(L-4) + NA).  Then the same binary carry chain as the
+// word-per-thread path: t_w = lo(S_w) + hi(S_(w-1)), generate / propagate per
+// thread, ballot add per warp, warp 0's scan across warps.  Rows never carry
+// into each other (a row's top word neither generates nor propagates).
+// ---------------------------------------------------------------------------
+// Word accumulators: 32-bit low halves plus 4-bit carry counts packed eight
+// to a register (a word collects at most ~5 pieces, so counts stay < 16):
+// about half the registers of 64-bit sums.
+template <int NA>
+struct WordAcc {
+    uint32_t lo[NA];
+    uint32_t hc[(NA + 7) / 8];
+    __device__ __forceinline__ void clear() {
+#pragma unroll
+        for (int k = 0; k < NA; ++k) lo[k] = 0;
+#pragma unroll
+        for (int k = 0; k < (NA + 7) / 8; ++k) hc[k] = 0;
+    }
+    template <int K>
+    __device__ __forceinline__ void add(uint32_t v) {
+        lo[K] += v;
+        hc[K / 8] += (uint32_t)(lo[K] < v) << (4 * (K % 8));
+    }
+    template <int K>
+    __device__ __forceinline__ uint32_t hi() const { return (hc[K / 8] >> (4 * (K % 8))) & 15u; }
+    template <int K>
+    __device__ __forceinline__ uint64_t sum() const { return ((uint64_t)hi<K>() << 32) | lo[K]; }
+};
+
+template <int K, int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+    if constexpr (K < N) { f(std::integral_constant<int, K>{}); static_for<K + 1, N>(f); }
+}
+
+template <int P, int AW, bool FUSED>
+__device__ __forceinline__ void crt_convert_grouped(const FinalArgs& A, const CrtConst& cc, const uint32_t* sm,
+                                                    uint32_t stride, int R, uint32_t pos0, bool sharded) {
+    constexpr int G = 4, NA = AW * (G - 1) + P + 1, NT = NA - AW * G;
+    static_assert(NT >= 1 && AW * G - 1 >= NT, "tail must not reach the sender's last owned word");
+    static_assert(NT <= 8, "tail carry counts are packed in one register");
+    __shared__ uint32_t stail[2][32][NT + 1];
+    __shared__ uint32_t shi[2][32];
+    __shared__ uint32_t gwtf[32], gwcin[32], gcarry;
+    const int L = 1 << A.lgL, lgng = A.lgL - 2, ngr = L >> 2;
+    const int M = A.M, W32 = A.W32;
+    const bool bodd = (M & 31) != 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t ntask = (int64_t)R << lgng;
+    if (threadIdx.x == 0) gcarry = 0;
+    int par = 0;
+    for (int64_t base = 0; base < ntask; base += blockDim.x, par ^= 1) {
+        const int64_t task = base + threadIdx.x;
+        const bool valid = task < ntask;
+        const int r = valid ? (int)(task >> lgng) : 0;
+        const int m = (int)(task & (ngr - 1));
+        const int j0 = m * G;
+        const uint32_t rowbase = (uint32_t)r << A.lgL;
+        const uint32_t prow = bitrev(pos0 + (uint32_t)r, A.lgS);
+        const int ub = (M * j0) >> 5, r0 = (M * j0) & 31;
+        WordAcc<NA> acc;
+        acc.clear();
+        if (valid) {
+#pragma unroll
+            for (int i = 0; i < G; ++i) {
+                const int j = j0 + i;
+                const uint32_t e = padi(rowbase + (uint32_t)j);
+                uint32_t x[P];
+                if constexpr (FUSED) {
+                    uint32_t rr[P];
+                    rr[0] = canon(sm[e], cc.p[0]);
+#pragma unroll
+                    for (int q = 1; q < P; ++q) rr[q] = reduce_2p(sm[q * stride + e], 2 * cc.p[q]);
+                    if (A.inject >= 0 && (int64_t)prow * L + j == A.inject)
+                        rr[0] = rr[0] ? rr[0] - 1 : cc.p[0] - 1;     // fault injection (tests of the bound check)
+                    const bool bad = crt_term<P>(rr, cc, x);
+                    if (bad && prow < A.rows_out)
+                        atomicMin(&A.err[2], (int)min((int64_t)prow * L + j, (int64_t)0x7fffffff));
+                    x[P - 1] ^= 0x80000000u;                      // biased: c_ij + 2^(32P-1) >= 0
+                } else {                                          // biased limbs from the in-place CRT pass
+#pragma unroll
+                    for (int q = 0; q < P; ++q) x[q] = sm[q * stride + e];
+                }
+                if (j <= L - 2) {
+                    const int sh = r0 + (bodd ? i : 0);
+                    static_for<0, P + 1>([&](auto kc) {
+                        constexpr int k = decltype(kc)::value;
+                        const uint32_t lo = k > 0 ? x[k > 0 ? k - 1 : 0] : 0u, hi = k < P ? x[k < P ? k : 0] : 0u;
+                        // term i's piece k lands in word AW*i + k (i is unrolled: constant)
+                        switch (i) {
+                            case 0: acc.template add<0 * AW + k>(__funnelshift_l(lo, hi, sh)); break;
+                            case 1: acc.template add<1 * AW + k>(__funnelshift_l(lo, hi, sh)); break;
+                            case 2: acc.template add<2 * AW + k>(__funnelshift_l(lo, hi, sh)); break;
+                            default: acc.template add<3 * AW + k>(__funnelshift_l(lo, hi, sh)); break;
+                        }
+                    });
+                }
+            }
+        }
+        const bool last = m == ngr - 1;
+        const bool wide1 = bodd && r0 + G == 32;
+        const int nown = last ? NA : AW * G + (wide1 ? 1 : 0);
+        // the sender's last owned word with its bias: its high half is the
+        // receiver's first carry term
+        const int wl = ub + nown - 1;
+        uint64_t slast = last ? acc.template sum<NA - 1>() : (wide1 ? acc.template sum<AW * G>() : acc.template sum<AW * G - 1>());
+        if (wl < W32) slast += __ldg(A.nbias + wl);
+        // tail words (after the owned ones) -> the next group
+        uint32_t tlo[NT], thc = 0;
+        static_for<0, NT>([&](auto ic) {
+            constexpr int t = decltype(ic)::value;
+            constexpr int k0 = AW * G + t, k1 = AW * G + 1 + t;
+            const uint32_t l0 = acc.lo[k0], h0 = acc.template hi<k0>();
+            uint32_t l1 = 0, h1 = 0;
+            if constexpr (k1 < NA) { l1 = acc.lo[k1]; h1 = acc.template hi<k1>(); }
+            tlo[t] = last ? 0u : (wide1 ? l1 : l0);
+            thc |= (last ? 0u : (wide1 ? h1 : h0)) << (4 * t);
+        });
+        const uint32_t hsend = (uint32_t)(slast >> 32);
+        uint32_t tin[NT], tinc, hin;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) tin[t] = __shfl_up_sync(0xffffffffu, tlo[t], 1);
+        tinc = __shfl_up_sync(0xffffffffu, thc, 1);
+        hin = __shfl_up_sync(0xffffffffu, hsend, 1);
+        if (lane == 31) {
+#pragma unroll
+            for (int t = 0; t < NT; ++t) stail[par][warp][t] = tlo[t];
+            stail[par][warp][NT] = thc;
+            shi[par][warp] = hsend;
+        }
+        __syncthreads();
+        if (lane == 0) {
+            const int pw = warp > 0 ? warp - 1 : nw - 1;          // warp 0: the previous iteration's last warp
+            const int pp = warp > 0 ? par : par ^ 1;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) tin[t] = stail[pp][pw][t];
+            tinc = stail[pp][pw][NT];
+            hin = shi[pp][pw];
+        }
+        if (m == 0) {                                             // a row starts: nothing flows in
+#pragma unroll
+            for (int t = 0; t < NT; ++t) tin[t] = 0;
+            tinc = 0;
+            hin = 0;
+        }
+        static_for<0, NT>([&](auto ic) {
+            constexpr int t = decltype(ic)::value;
+            acc.template add<t>(tin[t]);
+            acc.hc[t / 8] += ((tinc >> (4 * t)) & 15u) << (4 * (t % 8));
+        });
+        // S_w with bias; carry terms t_w = lo(S_w) + hi(S_(w-1))
+        uint32_t tw[NA], gm = 0, pm = 0, om = 0;
+        uint32_t hprev = hin;
+        static_for<0, NA>([&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            const int w = ub + k;
+            const bool own = valid && k < nown && w < W32;
+            uint64_t S = acc.template sum<k>();
+            if (own) S += __ldg(A.nbias + w);
+            const uint64_t t = (S & 0xffffffffull) + (uint64_t)hprev;
+            hprev = (uint32_t)(S >> 32);
+            tw[k] = (uint32_t)t;
+            const bool live = own && w != W32 - 1;                // a row's top word never carries on
+            if (own) om |= 1u << k;
+            if (live && (t >> 32)) gm |= 1u << k;
+            if ((live && (uint32_t)t == 0xffffffffu) || !own) pm |= 1u << k;   // words not owned: transparent
+        });
+        uint32_t c0 = 0, c1 = 1;
+#pragma unroll
+        for (int k = 0; k < NA; ++k) {
+            const uint32_t g = (gm >> k) & 1u, p = (pm >> k) & 1u;
+            c0 = g | (p & c0);
+            c1 = g | (p & c1);
+        }
+        const unsigned G1 = __ballot_sync(0xffffffffu, c0);
+        const unsigned P1 = __ballot_sync(0xffffffffu, c1 & !c0);
+        const uint64_t A1 = (uint64_t)(G1 | P1), B1 = (uint64_t)G1;
+        if (lane == 0) gwtf[warp] = (uint32_t)((A1 + B1) >> 32) | ((uint32_t)((A1 + B1 + 1) >> 32) << 1);
+        __syncthreads();
+        if (warp == 0) warp_carry_scan(gwtf, gwcin, &gcarry, nw, lane);
+        __syncthreads();
+        uint32_t c = (uint32_t)(((A1 + B1 + gwcin[warp]) ^ A1 ^ B1) >> lane) & 1u;
+        uint32_t* orow = sharded ? A.out + ((int64_t)blockIdx.x * R + r) * W32 : A.out + (int64_t)prow * W32;
+        const bool store = sharded || prow < A.rows_out;
+#pragma unroll
+        for (int k = 0; k < NA; ++k) {
+            if (((om >> k) & 1u) && store) orow[ub + k] = tw[k] + c;
+            c = ((gm >> k) & 1u) | (((pm >> k) & 1u) & c);
+        }
+    }
+}
 
 template <int P, bool DUMP, int NT>
 __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_final(FinalArgs A, const __grid_constant__ CrtConst cc) {
@@ -1459,6 +1669,17 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
             run_bits<true>(t, tile_bits, A.lgL, tile_bits, tw, pc.p, pc.two_p);
         x_transform<false>(t, A.lgL, tile_bits, tw.twx, pc.p, pc.two_p);      // x: DIT
     }
+#ifndef TC_CO_FUSED_BUILD
+#define TC_CO_FUSED_BUILD 0     // fused CRT in the grouped path: spills at 64 registers (P >= 5)
+#endif
+    if constexpr (!DUMP && P <= 8 && TC_CO_FUSED_BUILD) {
+        if (A.co_fused) {
+            if constexpr (P >= 2)
+                if (A.co_aw == 2) { crt_convert_grouped<P, 2, true>(A, cc, sm, stride, R, pos0, sharded); return; }
+            if constexpr (P <= 3)
+                if (A.co_aw == 1) { crt_convert_grouped<P, 1, true>(A, cc, sm, stride, R, pos0, sharded); return; }
+        }
+    }
     // CRT in place
     for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
         uint32_t r[P], x[P];
@@ -1483,6 +1704,12 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
     }
     if (DUMP) return;
     __syncthreads();
+    if constexpr (P <= 8) {
+        if constexpr (P >= 2)
+            if (A.co_aw == 2) { crt_convert_grouped<P, 2, false>(A, cc, sm, stride, R, pos0, sharded); return; }
+        if constexpr (P <= 3)
+            if (A.co_aw == 1) { crt_convert_grouped<P, 1, false>(A, cc, sm, stride, R, pos0, sharded); return; }
+    }
 
     // ConvertOut over the tile's rows, kW words per thread (rows padded to a
     // multiple of kW words).  Terms are stored biased (c_ij + 2^(32P-1), an
