@@ -357,10 +357,20 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     a.pcs = c->pcs.as<PrimeC>(); a.P = G.P;
     const int Rc = G.yl >= 1 ? 1 << (G.yl - 1) : 1;      // computed (even) rows, see k_low
     const uint32_t n = 1u << (G.lgL + G.yl);
-    const size_t smem = (size_t)Rc * G.K * (pl->M > 63 ? 16 : 8) + (size_t)Rc * 8 + (size_t)padded_words(n) * 4;
+    size_t smem = (size_t)Rc * G.K * (pl->M > 63 ? 16 : 8) + (size_t)Rc * 8 + (size_t)padded_words(n) * 4;
     const int64_t ctas = sh.world > 1 ? sh.Tl : G.S / n;
     // a tile too large for two CTAs per SM gets 32 warps in one CTA
     const int lt = env_int("TC_LOW_THREADS", 0);
+    // two primes side by side when a compact tile's radix-16 rounds fill at
+    // most half of a 256-thread CTA (and the fused duplication + y round
+    // covers the shape): L = 256 plans
+    static const int dual_env = env_int("TC_LOW_DUAL", 1);
+    const uint32_t nc = n >> 1;
+    if (dual_env && G.P >= 2 && sh.world == 1 && G.lgL >= 5 && G.yl >= 2 && G.yl <= 5 &&
+        (nc >> 4) <= 128 && (lt == 0 || lt == 256) && smem + (size_t)padded_words(n) * 4 <= 112 * 1024) {
+        a.dual = 1;
+        smem += (size_t)padded_words(n) * 4;
+    }
     if (smem > 112 * 1024 || lt >= 1024) {
         CK(ensure_smem((const void*)k_low<1024>, smem));
         k_low<1024><<<(unsigned)ctas, 1024, smem, st>>>(a);
@@ -509,6 +519,8 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
             A.co_aw = aw;
         static const int fused = env_int("TC_CO_FUSED", 0);
         A.co_fused = fused;
+        static const int fdual = env_int("TC_FINAL_DUAL", 1);
+        A.dual_ok = fdual;
     }
     const uint32_t n = 1u << (G.lgL + G.yl);
     const size_t smem = (size_t)G.P * padded_words(n) * 4;

@@ -621,15 +621,23 @@ __device__ __forceinline__ void run_bits(uint32_t* s, int tile_bits, int lo, int
 // bits lo below stage bit b uses entry 2^b + lo).  The tile size stays a
 // runtime value (only the group count depends on it).
 // ---------------------------------------------------------------------------
+// The threads sharing one tile: this thread's first group index and the
+// stride (the whole CTA, or half of it when two primes' tiles are
+// transformed side by side).  Threads with t0 >= the group count only join
+// the barriers.
+struct Span { uint32_t t0, nt; };
+__device__ __forceinline__ Span cta_span() { return Span{threadIdx.x, blockDim.x}; }
+
 template <int BL, int NB, bool DIF>
-__device__ __forceinline__ void xct_round(uint32_t* s, int tile_bits, const uint2* twx, uint32_t p, uint32_t two_p) {
+__device__ __forceinline__ void xct_round(uint32_t* s, int tile_bits, const uint2* twx, uint32_t p, uint32_t two_p,
+                                          Span sp) {
     constexpr int R = 1 << NB;
     constexpr uint32_t lowmask = (1u << BL) - 1;
     constexpr bool PERMC = BL >= 1 && BL <= 4 && BL >= NB;
     constexpr uint32_t pa = BL, pb = BL + 5 - NB;
     const uint32_t pm = (PERMC && tile_bits >= 10) ? (1u << (5 - BL)) - 1 : 0u;
     const uint32_t ngroups = 1u << (tile_bits - NB);
-    for (uint32_t g0 = threadIdx.x; g0 < ngroups; g0 += blockDim.x) {
+    for (uint32_t g0 = sp.t0; g0 < ngroups; g0 += sp.nt) {
         uint32_t g = g0;
         if (PERMC) {
             const uint32_t t = ((g >> pa) ^ (g >> pb)) & pm;
@@ -663,54 +671,55 @@ __device__ __forceinline__ void xct_round(uint32_t* s, int tile_bits, const uint
 
 // bits [LO, HI) in rounds of <= 4 bits (run_segment's partition)
 template <int LO, int HI, bool DIF>
-__device__ __forceinline__ void xct_seg(uint32_t* s, int tile_bits, const uint2* twx, uint32_t p, uint32_t two_p) {
+__device__ __forceinline__ void xct_seg(uint32_t* s, int tile_bits, const uint2* twx, uint32_t p, uint32_t two_p,
+                                        Span sp) {
     constexpr int nbits = HI - LO;
     if constexpr (nbits > 0) {
         constexpr int nr = (nbits + 3) / 4;
         constexpr int nb = nbits / nr + (nbits % nr ? 1 : 0);
         if constexpr (!DIF) {
-            xct_round<LO, nb, false>(s, tile_bits, twx, p, two_p);
-            xct_seg<LO + nb, HI, false>(s, tile_bits, twx, p, two_p);
+            xct_round<LO, nb, false>(s, tile_bits, twx, p, two_p, sp);
+            xct_seg<LO + nb, HI, false>(s, tile_bits, twx, p, two_p, sp);
         } else {
-            xct_round<HI - nb, nb, true>(s, tile_bits, twx, p, two_p);
-            xct_seg<LO, HI - nb, true>(s, tile_bits, twx, p, two_p);
+            xct_round<HI - nb, nb, true>(s, tile_bits, twx, p, two_p, sp);
+            xct_seg<LO, HI - nb, true>(s, tile_bits, twx, p, two_p, sp);
         }
     }
 }
 
 template <int LGL, bool DIF>
-__device__ __forceinline__ void xct(uint32_t* s, int tile_bits, const uint2* twx, uint32_t p, uint32_t two_p) {
+__device__ __forceinline__ void xct(uint32_t* s, int tile_bits, const uint2* twx, uint32_t p, uint32_t two_p, Span sp) {
     constexpr int mid = LGL > 4 ? 4 : LGL;
     if (!DIF) {
-        xct_seg<0, mid, false>(s, tile_bits, twx, p, two_p);
-        xct_seg<mid, LGL, false>(s, tile_bits, twx, p, two_p);
+        xct_seg<0, mid, false>(s, tile_bits, twx, p, two_p, sp);
+        xct_seg<mid, LGL, false>(s, tile_bits, twx, p, two_p, sp);
     } else {
-        xct_seg<mid, LGL, true>(s, tile_bits, twx, p, two_p);
-        xct_seg<0, mid, true>(s, tile_bits, twx, p, two_p);
+        xct_seg<mid, LGL, true>(s, tile_bits, twx, p, two_p, sp);
+        xct_seg<0, mid, true>(s, tile_bits, twx, p, two_p, sp);
     }
 }
 
 // The x transform of a tile: one out-of-line copy per direction, dispatched on lgL.
 template <bool DIF>
 __device__ __noinline__ void x_transform(uint32_t* s, int lgL, int tile_bits, const uint2* twx,
-                                         uint32_t p, uint32_t two_p) {
+                                         uint32_t p, uint32_t two_p, Span sp) {
     switch (lgL) {
         case 0: break;
-        case 1: xct<1, DIF>(s, tile_bits, twx, p, two_p); break;
-        case 2: xct<2, DIF>(s, tile_bits, twx, p, two_p); break;
-        case 3: xct<3, DIF>(s, tile_bits, twx, p, two_p); break;
-        case 4: xct<4, DIF>(s, tile_bits, twx, p, two_p); break;
-        case 5: xct<5, DIF>(s, tile_bits, twx, p, two_p); break;
-        case 6: xct<6, DIF>(s, tile_bits, twx, p, two_p); break;
-        case 7: xct<7, DIF>(s, tile_bits, twx, p, two_p); break;
-        case 8: xct<8, DIF>(s, tile_bits, twx, p, two_p); break;
-        case 9: xct<9, DIF>(s, tile_bits, twx, p, two_p); break;
-        case 10: xct<10, DIF>(s, tile_bits, twx, p, two_p); break;
-        case 11: xct<11, DIF>(s, tile_bits, twx, p, two_p); break;
-        case 12: xct<12, DIF>(s, tile_bits, twx, p, two_p); break;
-        case 13: xct<13, DIF>(s, tile_bits, twx, p, two_p); break;
-        case 14: xct<14, DIF>(s, tile_bits, twx, p, two_p); break;
-        case 15: xct<15, DIF>(s, tile_bits, twx, p, two_p); break;
+        case 1: xct<1, DIF>(s, tile_bits, twx, p, two_p, sp); break;
+        case 2: xct<2, DIF>(s, tile_bits, twx, p, two_p, sp); break;
+        case 3: xct<3, DIF>(s, tile_bits, twx, p, two_p, sp); break;
+        case 4: xct<4, DIF>(s, tile_bits, twx, p, two_p, sp); break;
+        case 5: xct<5, DIF>(s, tile_bits, twx, p, two_p, sp); break;
+        case 6: xct<6, DIF>(s, tile_bits, twx, p, two_p, sp); break;
+        case 7: xct<7, DIF>(s, tile_bits, twx, p, two_p, sp); break;
+        case 8: xct<8, DIF>(s, tile_bits, twx, p, two_p, sp); break;
+        case 9: xct<9, DIF>(s, tile_bits, twx, p, two_p, sp); break;
+        case 10: xct<10, DIF>(s, tile_bits, twx, p, two_p, sp); break;
+        case 11: xct<11, DIF>(s, tile_bits, twx, p, two_p, sp); break;
+        case 12: xct<12, DIF>(s, tile_bits, twx, p, two_p, sp); break;
+        case 13: xct<13, DIF>(s, tile_bits, twx, p, two_p, sp); break;
+        case 14: xct<14, DIF>(s, tile_bits, twx, p, two_p, sp); break;
+        case 15: xct<15, DIF>(s, tile_bits, twx, p, two_p, sp); break;
         default: __trap();
     }
 }
@@ -725,19 +734,19 @@ __device__ __noinline__ void x_transform(uint32_t* s, int lgL, int tile_bits, co
 // ---------------------------------------------------------------------------
 template <int RB, int NB, bool DIF>
 __device__ __forceinline__ void yct_round(uint32_t* s, int tile_bits, int lgL, const uint2* twy,
-                                          uint32_t p, uint32_t two_p) {
+                                          uint32_t p, uint32_t two_p, Span sp) {
     constexpr int R = 1 << NB;
     const int bl = lgL + RB;
     const uint32_t lowmask = (1u << bl) - 1;
     const uint32_t astep = (1u << bl) + (1u << (bl - 5));
     const uint32_t ngroups = 1u << (tile_bits - NB);
-    for (uint32_t g = threadIdx.x; g < ngroups; g += blockDim.x) {
+    for (uint32_t g = sp.t0; g < ngroups; g += sp.nt) {
         const uint32_t lo = g & lowmask;
-        uint32_t* sp = s + padi(((g & ~lowmask) << NB) | lo);
+        uint32_t* sq = s + padi(((g & ~lowmask) << NB) | lo);
         const uint2* tq = twy + (lo >> lgL);
         uint32_t x[R];
 #pragma unroll
-        for (int k = 0; k < R; ++k) x[k] = sp[k * astep];
+        for (int k = 0; k < R; ++k) x[k] = sq[k * astep];
 #pragma unroll
         for (int it = 0; it < NB; ++it) {
             const int lv = DIF ? NB - 1 - it : it;
@@ -753,24 +762,24 @@ __device__ __forceinline__ void yct_round(uint32_t* s, int tile_bits, int lgL, c
             }
         }
 #pragma unroll
-        for (int k = 0; k < R; ++k) sp[k * astep] = x[k];
+        for (int k = 0; k < R; ++k) sq[k * astep] = x[k];
     }
     __syncthreads();
 }
 
 template <int LO, int HI, bool DIF>
 __device__ __forceinline__ void yct_seg(uint32_t* s, int tile_bits, int lgL, const uint2* twy, uint32_t p,
-                                        uint32_t two_p) {
+                                        uint32_t two_p, Span sp) {
     constexpr int nbits = HI - LO;
     if constexpr (nbits > 0) {
         constexpr int nr = (nbits + 3) / 4;
         constexpr int nb = nbits / nr + (nbits % nr ? 1 : 0);
         if constexpr (!DIF) {
-            yct_round<LO, nb, false>(s, tile_bits, lgL, twy, p, two_p);
-            yct_seg<LO + nb, HI, false>(s, tile_bits, lgL, twy, p, two_p);
+            yct_round<LO, nb, false>(s, tile_bits, lgL, twy, p, two_p, sp);
+            yct_seg<LO + nb, HI, false>(s, tile_bits, lgL, twy, p, two_p, sp);
         } else {
-            yct_round<HI - nb, nb, true>(s, tile_bits, lgL, twy, p, two_p);
-            yct_seg<LO, HI - nb, true>(s, tile_bits, lgL, twy, p, two_p);
+            yct_round<HI - nb, nb, true>(s, tile_bits, lgL, twy, p, two_p, sp);
+            yct_seg<LO, HI - nb, true>(s, tile_bits, lgL, twy, p, two_p, sp);
         }
     }
 }
@@ -779,10 +788,10 @@ __device__ __forceinline__ void yct_seg(uint32_t* s, int tile_bits, int lgL, con
 // compile-time schedule (caller runs the generic rounds).
 template <bool DIF>
 __device__ __noinline__ bool y_transform(uint32_t* s, int lgL, int rb0, int tile_bits, const uint2* twy,
-                                         uint32_t p, uint32_t two_p) {
+                                         uint32_t p, uint32_t two_p, Span sp) {
     const int ny = tile_bits - lgL - rb0;
     if (lgL < 5 || ny < 0 || ny > 12 || rb0 > 1) return false;
-#define TC_YCASE(R0, N) case (R0) * 16 + (N): yct_seg<R0, R0 + N, DIF>(s, tile_bits, lgL, twy, p, two_p); break;
+#define TC_YCASE(R0, N) case (R0) * 16 + (N): yct_seg<R0, R0 + N, DIF>(s, tile_bits, lgL, twy, p, two_p, sp); break;
     switch (rb0 * 16 + ny) {
         case 0: case 16: break;
         TC_YCASE(0, 1) TC_YCASE(0, 2) TC_YCASE(0, 3) TC_YCASE(0, 4) TC_YCASE(0, 5) TC_YCASE(0, 6)
@@ -805,10 +814,10 @@ __device__ __noinline__ bool y_transform(uint32_t* s, int lgL, int rb0, int tile
 // and no other thread touches the column, so no barrier between read and write.
 template <int NB>
 __device__ __forceinline__ void yct_expand_columns(uint32_t* s, int lgL, const uint2* twy, uint32_t p,
-                                                   uint32_t two_p, uint32_t* gout) {
+                                                   uint32_t two_p, uint32_t* gout, Span sp) {
     constexpr int R = 1 << NB;
     const uint32_t L = 1u << lgL;
-    for (uint32_t col = threadIdx.x; col < L; col += blockDim.x) {
+    for (uint32_t col = sp.t0; col < L; col += sp.nt) {
         uint32_t xa[R];
 #pragma unroll
         for (int k = 0; k < R; ++k) xa[k] = s[padi(((uint32_t)k << lgL) | col)];
@@ -845,13 +854,13 @@ __device__ __forceinline__ void yct_expand_columns(uint32_t* s, int lgL, const u
 // false: shape not covered (caller expands and runs y_transform / run_bits).
 // gout != NULL: the finished tile goes straight to the grid (contiguous tile).
 static __device__ __noinline__ bool y_transform_expand(uint32_t* s, int lgL, int tile_bits, const uint2* twy,
-                                                       uint32_t p, uint32_t two_p, uint32_t* gout) {
+                                                       uint32_t p, uint32_t two_p, uint32_t* gout, Span sp) {
     const int ny = tile_bits - lgL - 1;          // y levels after the duplication
     switch (lgL >= 5 ? ny : 0) {
-        case 1: yct_expand_columns<1>(s, lgL, twy, p, two_p, gout); return true;
-        case 2: yct_expand_columns<2>(s, lgL, twy, p, two_p, gout); return true;
-        case 3: yct_expand_columns<3>(s, lgL, twy, p, two_p, gout); return true;
-        case 4: yct_expand_columns<4>(s, lgL, twy, p, two_p, gout); return true;
+        case 1: yct_expand_columns<1>(s, lgL, twy, p, two_p, gout, sp); return true;
+        case 2: yct_expand_columns<2>(s, lgL, twy, p, two_p, gout, sp); return true;
+        case 3: yct_expand_columns<3>(s, lgL, twy, p, two_p, gout, sp); return true;
+        case 4: yct_expand_columns<4>(s, lgL, twy, p, two_p, gout, sp); return true;
         default: return false;
     }
 }
@@ -913,6 +922,7 @@ struct LowArgs {
     uint32_t* g; int64_t S;
     const uint2* twx; const uint2* twy; int64_t twy_stride;
     const PrimeC* pcs; int P;
+    int dual;              // two primes side by side in two tile buffers (host-checked shape)
 };
 
 template <int NT>
@@ -966,31 +976,54 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
         if (staged) compute_digits_staged<__int128>(A.src, Rc, coeff, dig2, ds, reinterpret_cast<uint64_t*>(tile));
         else compute_digits<__int128>(A.src, Rc, coeff, dig2, ds);
     }
+    // residues of the K digit columns of prime q into tile tb; the top x level
+    // (DIF on (x_j, 0) pairs, the theta-twist) is fused here: columns j and
+    // j + K get x_j and x_j w_j
+    auto residues = [&](int q, uint32_t* tb, Span sp) {
+        const PrimeC pc = A.pcs[q];
+        const uint2* wtop = A.twx + (int64_t)q * L + (L >> 1);   // level lgL-1, entry 2^(lgL-1) + j
+        const uint32_t kk = (uint32_t)A.src.K, nk = (uint32_t)Rc * kk;
+        for (uint32_t t = sp.t0; t < nk; t += sp.nt) {
+            const uint32_t r = t >> A.src.lgK, j = t & (kk - 1);
+            const uint32_t e = (r << A.lgL) | j;
+            uint32_t x = 0, y = 0;
+            if (coeff[r] >= 0) {
+                x = wide ? digit_residue(dig2[t], pc) : digit_residue(dig[t], pc);
+                const uint2 w = __ldg(wtop + j);
+                y = shoup_mul(x, w.x, w.y, pc.p);
+            }
+            tb[padi(e)] = x;
+            tb[padi(e + kk)] = y;
+        }
+    };
+    if (A.dual) {
+        // two primes side by side, one per half of the CTA (a compact tile's
+        // radix-16 rounds occupy at most half the threads), each in its own
+        // tile buffer, written straight to the grid by the fused y round
+        const uint32_t halfT = blockDim.x >> 1;
+        const int hsel = threadIdx.x >= halfT ? 1 : 0;
+        uint32_t* tb = tile + (hsel ? padded_words(n) : 0u);
+        for (int q0 = 0; q0 < A.P; q0 += 2) {
+            const int q = q0 + hsel;
+            const bool act = q < A.P;
+            const int qq = act ? q : q0;
+            const Span sp{act ? threadIdx.x - hsel * halfT : 0x7fffffffu, halfT};
+            const PrimeC pc = A.pcs[qq];
+            residues(qq, tb, sp);
+            __syncthreads();
+            x_transform<true>(tb, A.lgL - 1, cbits, A.twx + (int64_t)qq * L, pc.p, pc.two_p, sp);
+            y_transform_expand(tb, A.lgL, tile_bits, A.twy + (int64_t)qq * A.twy_stride, pc.p, pc.two_p, dst(qq), sp);
+        }
+        return;
+    }
     for (int q = 0; q < A.P; ++q) {
         const PrimeC pc = A.pcs[q];
         const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
-        // residues of the K digit columns; the top x level (DIF on (x_j, 0) pairs,
-        // the theta-twist) is fused here: columns j and j + K get x_j and x_j w_j
-        {
-            const uint2* wtop = tw.twx + (L >> 1);             // level lgL-1, entry 2^(lgL-1) + j
-            const uint32_t kk = (uint32_t)A.src.K, nk = (uint32_t)Rc * kk;
-            for (uint32_t t = threadIdx.x; t < nk; t += blockDim.x) {
-                const uint32_t r = t >> A.src.lgK, j = t & (kk - 1);
-                const uint32_t e = (r << A.lgL) | j;
-                uint32_t x = 0, y = 0;
-                if (coeff[r] >= 0) {
-                    x = wide ? digit_residue(dig2[t], pc) : digit_residue(dig[t], pc);
-                    const uint2 w = __ldg(wtop + j);
-                    y = shoup_mul(x, w.x, w.y, pc.p);
-                }
-                tile[padi(e)] = x;
-                tile[padi(e + kk)] = y;
-            }
-        }
+        residues(q, tile, cta_span());
         __syncthreads();
-        x_transform<true>(tile, A.lgL - 1, cbits, tw.twx, pc.p, pc.two_p);       // x: DIF, levels below the twist
+        x_transform<true>(tile, A.lgL - 1, cbits, tw.twx, pc.p, pc.two_p, cta_span());   // x: DIF, levels below the twist
         const bool fused = prune && y_transform_expand(tile, A.lgL, tile_bits, tw.twy, pc.p, pc.two_p,
-                                                       sharded ? nullptr : dst(q));
+                                                       sharded ? nullptr : dst(q), cta_span());
         if (prune && !fused) {
             // expand in place, highest chunk first: compact e -> rows 2r', 2r'+1
             const uint32_t chunk = 8u * blockDim.x;
@@ -1014,7 +1047,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
                 __syncthreads();
             }
         }
-        if (!fused && !y_transform<false>(tile, A.lgL, prune ? 1 : 0, tile_bits, tw.twy, pc.p, pc.two_p))   // y: DIT
+        if (!fused && !y_transform<false>(tile, A.lgL, prune ? 1 : 0, tile_bits, tw.twy, pc.p, pc.two_p, cta_span()))   // y: DIT
             run_bits<false>(tile, tile_bits, A.lgL + (prune ? 1 : 0), tile_bits, tw, pc.p, pc.two_p);
         uint32_t* g = dst(q);
         if (sharded) tile_store(g, tile, n, XchgIdx{A.sh, blockIdx.x});
@@ -1416,6 +1449,7 @@ struct FinalArgs {
     int64_t inject;                // >= 0: corrupt the residue of flat slot row*L + j (plan.flags)
     int co_aw;                     // > 0: grouped ConvertOut with M = 32 co_aw + {0, 1} (host-checked)
     int co_fused;                  // grouped ConvertOut lifts the residues itself (no in-place CRT pass)
+    int dual_ok;                   // allow two primes' transforms side by side (small tiles)
 };
 
 // ---------------------------------------------------------------------------
@@ -1659,15 +1693,36 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
         }
         cp_async_commit();
     }
-    for (int q = 0; q < P; ++q) {
-        const PrimeC pc = A.pcs[q];
-        uint32_t* t = sm + q * stride;
-        cp_async_wait_dyn(P - 1 - q);
-        __syncthreads();
-        const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
-        if (!y_transform<true>(t, A.lgL, 0, tile_bits, tw.twy, pc.p, pc.two_p))   // y low: DIF
-            run_bits<true>(t, tile_bits, A.lgL, tile_bits, tw, pc.p, pc.two_p);
-        x_transform<false>(t, A.lgL, tile_bits, tw.twx, pc.p, pc.two_p);      // x: DIT
+    // A tile whose radix-16 rounds occupy at most half the threads (L = 256
+    // tiles of 512-thread CTAs): two primes side by side, one per half.
+    const uint32_t halfT = blockDim.x >> 1;
+    const bool dual = A.dual_ok && P >= 2 && A.lgL >= 5 && A.yl <= 12 && (n >> 4) <= halfT;
+    if (dual) {
+        const int hsel = threadIdx.x >= halfT ? 1 : 0;
+        for (int q0 = 0; q0 < P; q0 += 2) {
+            const int q = q0 + hsel;
+            cp_async_wait_dyn(P - 1 - min(q0 + 1, P - 1));
+            __syncthreads();
+            const bool act = q < P;
+            const int qq = act ? q : q0;
+            const PrimeC pc = A.pcs[qq];
+            uint32_t* t = sm + qq * stride;
+            const Span sp{act ? threadIdx.x - hsel * halfT : 0x7fffffffu, halfT};
+            const TwRows tw{A.twx + (int64_t)qq * L, A.twy + (int64_t)qq * A.twy_stride, A.lgL};
+            y_transform<true>(t, A.lgL, 0, tile_bits, tw.twy, pc.p, pc.two_p, sp);   // y low: DIF
+            x_transform<false>(t, A.lgL, tile_bits, tw.twx, pc.p, pc.two_p, sp);     // x: DIT
+        }
+    } else {
+        for (int q = 0; q < P; ++q) {
+            const PrimeC pc = A.pcs[q];
+            uint32_t* t = sm + q * stride;
+            cp_async_wait_dyn(P - 1 - q);
+            __syncthreads();
+            const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
+            if (!y_transform<true>(t, A.lgL, 0, tile_bits, tw.twy, pc.p, pc.two_p, cta_span()))   // y low: DIF
+                run_bits<true>(t, tile_bits, A.lgL, tile_bits, tw, pc.p, pc.two_p);
+            x_transform<false>(t, A.lgL, tile_bits, tw.twx, pc.p, pc.two_p, cta_span());      // x: DIT
+        }
     }
 #ifndef TC_CO_FUSED_BUILD
 #define TC_CO_FUSED_BUILD 0     // fused CRT in the grouped path: spills at 64 registers (P >= 5)
