@@ -103,6 +103,7 @@ struct Ctx {
     cudaEvent_t xev[24] = {};            // cross-stream events of tc_multiply_host: 0 A up, 1 widths back, 2.. chunks, 20 B up, 21 A width
     int* hinfo = nullptr;                // pinned: widths read back early
     cudaEvent_t fev[2] = {};             // fork / join of the resident pipeline's two branches
+    int sms = 148;                       // multiprocessors of the device
 };
 
 int ilog2(int64_t x) { int l = 0; while ((1ll << l) < x) ++l; return l; }
@@ -374,7 +375,9 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     if (smem > 112 * 1024 || lt >= 1024) {
         CK(ensure_smem((const void*)k_low<1024>, smem));
         k_low<1024><<<(unsigned)ctas, 1024, smem, st>>>(a);
-    } else if (lt == 256 || lt == 0) {            // 256 threads: measured faster (C2 0.268 -> 0.228 ms)
+    } else if (lt == 256 || (lt == 0 && (G.yl >= 1 ? n >> 1 : n) < 8192)) {
+        // 256 threads: measured faster (C2 0.268 -> 0.228 ms); 512 once a tile's
+        // radix-16 rounds have >= 512 groups (C5 k_low 236 -> 204 us)
         CK(ensure_smem((const void*)k_low<256>, smem));
         k_low<256><<<(unsigned)ctas, 256, smem, st>>>(a);
     } else {
@@ -413,6 +416,7 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
     A.twf = c->twy_f.as<uint2>(); A.twi = c->twy_i.as<uint2>();
     A.tw_stride = G.s_y;
     A.pcs = c->pcs.as<PrimeC>();
+    // (L2 prefetch of MID's A tile / of the next wave's tiles measured slower: C2 MID 131 -> 139 us)
     const uint32_t n = 1u << (U + A.cb);
     const size_t smem = (size_t)padded_words(n) * 4;
     // 32 slots per thread: 512 threads for 2^14-slot tiles, 256 below (C3: 93 -> 81 ms)
@@ -724,6 +728,7 @@ int tc_ctx_create(int device, void** out) {
     } else {
         cudaGetDevice(&c->device);
     }
+    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device);
     cudaError_t e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
     if (e != cudaSuccess) { delete c; return set_err(TC_ERR_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e)); }
     for (auto& ev : c->ev) cudaEventCreate(&ev);
