@@ -331,7 +331,22 @@ def run_ours(args, rank, world, local):
     else:
         roof = {"bound": "hbm", "achieved": ds["GBps"], "peak": hbm_peak, "unit": "GB/s",
                 "frac": ds["hbm_frac"]}
-    roof.update({"kernel": dom, "traffic": None,
+    # DRAM traffic per launch of the dominant stage's kernel, from the committed
+    # ncu --set full capture of this config (profiles/r1_traffic.json)
+    traffic, tsrc = None, None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json"))).get(args.config)
+        if tj and dom in tj["stages"]:
+            ls = tj["stages"][dom]
+            traffic = round(sum(x["dram_bytes"] for x in ls) / len(ls))
+            tsrc = f"{tj['source']}: {ls[0]['kernel']}, {len(ls)} launch(es) per product"
+    except (OSError, ValueError, KeyError):
+        pass
+    from paper_1612_05778_b200.params import pass_layout
+    nh = len(pass_layout(plan.L.bit_length() - 1, plan.s_y.bit_length() - 1, plan.P)[1])
+    nlaunch = {"convert": 2, "ntt_forward": max(1, 2 * nh - 1), "ntt_inverse": max(1, nh - 1)}.get(dom, 1)
+    roof.update({"kernel": dom, "traffic": traffic, "traffic_source": tsrc,
+                 "algorithmic_bytes_per_launch": int(model[dom]["bytes"] // nlaunch),
                  "peak_source": "hbm: MEASURED_PEAKS.json hbm_gbs (measured); int: tc_int_peak "
                                 "register-only butterfly chain, measured live",
                  "stages": stages})
