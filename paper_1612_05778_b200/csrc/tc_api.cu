@@ -429,6 +429,7 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
         cudaError_t e = cudaErrorNotSupported;
         if (U == 10 && nth == 512) e = launch_high_ct<512, 10>(mode, A, grid, n, c->st);
         else if (U == 9 && nth == 256) e = launch_high_ct<256, 9>(mode, A, grid, n, c->st);
+        else if (U == 8 && nth == 256) e = launch_high_ct<256, 8>(mode, A, grid, n, c->st);
         else if (U == 4 && nth == 64) e = launch_high_ct<64, 4>(mode, A, grid, n, c->st);
         if (e != cudaErrorNotSupported) {
             c->launches++;

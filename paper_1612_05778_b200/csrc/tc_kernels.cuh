@@ -1221,6 +1221,14 @@ __device__ __forceinline__ void ct_pass(uint32_t* s, const uint2* stw, uint32_t 
             ct_round<TB, CB + 5, 4, true, NT, CB>(s, stw, p, two_p);
             ct_round<TB, CB, 5, true, NT, CB>(s, stw, p, two_p);
         }
+    } else if constexpr (U == 8) {      // two radix-16 rounds
+        if (!DIF) {
+            ct_round<TB, CB, 4, false, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB + 4, 4, false, NT, CB>(s, stw, p, two_p);
+        } else {
+            ct_round<TB, CB + 4, 4, true, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB, 4, true, NT, CB>(s, stw, p, two_p);
+        }
     } else {
 #else
     if constexpr (U == 10) {

@@ -38,8 +38,10 @@ cp = _lib.make_plan(plan_gpu(max(da, db), min(da, db), n_in, **kw))
 def step():
     lib.tc_stage_inputs(h, d_a, da, aw.shape[1], d_b, db, bw.shape[1], 1, None)
     err = ctypes.c_int64(-1)
-    _lib.check(lib.tc_execute(h, ctypes.byref(cp), ab, bb, d_out, rows, out_cw, 1, None, ctypes.byref(err)), "exec")
-    assert err.value < 0
+    rc = lib.tc_execute(h, ctypes.byref(cp), ab, bb, d_out, rows, out_cw, 1, None, ctypes.byref(err))
+    if not os.environ.get("AB_NOCHECK"):          # timing experiments with deliberately wrong results
+        _lib.check(rc, "exec")
+        assert err.value < 0
 step()
 out = np.empty((rows, out_cw), dtype=np.uint64)
 lib.tc_memcpy(h, _lib.ptr(out), d_out, out.nbytes, 2)
