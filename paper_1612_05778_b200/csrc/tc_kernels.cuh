@@ -1012,7 +1012,16 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
             residues(qq, tb, sp);
             __syncthreads();
             x_transform<true>(tb, A.lgL - 1, cbits, A.twx + (int64_t)qq * L, pc.p, pc.two_p, sp);
-            y_transform_expand(tb, A.lgL, tile_bits, A.twy + (int64_t)qq * A.twy_stride, pc.p, pc.two_p, dst(qq), sp);
+            if (prune) {
+                y_transform_expand(tb, A.lgL, tile_bits, A.twy + (int64_t)qq * A.twy_stride, pc.p, pc.two_p, dst(qq), sp);
+            } else {                                   // yl = 0: one row per tile, no y levels here
+                uint32_t* g = dst(qq);
+                for (uint32_t v = sp.t0; v < (n >> 2); v += sp.nt) {
+                    const uint32_t* d = tb + padi(v << 2);
+                    *reinterpret_cast<uint4*>(g + (v << 2)) = make_uint4(d[0], d[1], d[2], d[3]);
+                }
+                __syncthreads();
+            }
         }
         return;
     }
