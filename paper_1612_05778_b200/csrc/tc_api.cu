@@ -368,7 +368,7 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     static const int dual_env = env_int("TC_LOW_DUAL", 1);
     const uint32_t nc = n >> 1;
     const uint32_t ncomp = G.yl >= 1 ? nc : n;         // slots of the computed rows
-    if (dual_env && G.P >= 2 && sh.world == 1 && G.lgL >= 5 && (G.yl == 0 || (G.yl >= 2 && G.yl <= 5)) &&
+    if (dual_env && G.P >= 2 && sh.world == 1 && G.lgL >= 5 && G.yl <= 5 &&
         (ncomp >> 4) <= 128 && (lt == 0 || lt == 256) && smem + (size_t)padded_words(n) * 4 <= 112 * 1024) {
         a.dual = 1;
         smem += (size_t)padded_words(n) * 4;

@@ -86,7 +86,9 @@ __device__ __forceinline__ uint32_t digit_residue(int64_t dg, const PrimeC& c) {
 // part through a Montgomery product with 2^96 mod p.
 __device__ __forceinline__ uint32_t digit_residue(__int128 dg, const PrimeC& c) {
     const unsigned __int128 a = dg < 0 ? (unsigned __int128)(-(dg + 1)) + 1 : (unsigned __int128)dg;
-    const uint32_t lo = u64_mod((uint64_t)a, c), hi = u64_mod((uint64_t)(a >> 64), c);
+    const uint64_t h = (uint64_t)(a >> 64);
+    // M <= 96: the high word is below 2^32 and enters the Montgomery product as is
+    const uint32_t lo = u64_mod((uint64_t)a, c), hi = (h >> 32) ? u64_mod(h, c) : (uint32_t)h;
     uint32_t r = canon(lo + mont_mul(hi, c.c96, c.p, c.pinv_neg), c.p);
     if (dg < 0 && r) r = c.p - r;
     return r;

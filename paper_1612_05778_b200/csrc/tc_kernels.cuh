@@ -856,7 +856,9 @@ __device__ __forceinline__ void yct_expand_columns(uint32_t* s, int lgL, const u
 static __device__ __noinline__ bool y_transform_expand(uint32_t* s, int lgL, int tile_bits, const uint2* twy,
                                                        uint32_t p, uint32_t two_p, uint32_t* gout, Span sp) {
     const int ny = tile_bits - lgL - 1;          // y levels after the duplication
-    switch (lgL >= 5 ? ny : 0) {
+    if (lgL < 5) return false;
+    switch (ny) {
+        case 0: yct_expand_columns<0>(s, lgL, twy, p, two_p, gout, sp); return true;   // the duplication alone
         case 1: yct_expand_columns<1>(s, lgL, twy, p, two_p, gout, sp); return true;
         case 2: yct_expand_columns<2>(s, lgL, twy, p, two_p, gout, sp); return true;
         case 3: yct_expand_columns<3>(s, lgL, twy, p, two_p, gout, sp); return true;
