@@ -345,7 +345,15 @@ def run_ours(args, rank, world, local):
     from paper_1612_05778_b200.params import pass_layout
     nh = len(pass_layout(plan.L.bit_length() - 1, plan.s_y.bit_length() - 1, plan.P)[1])
     nlaunch = {"convert": 2, "ntt_forward": max(1, 2 * nh - 1), "ntt_inverse": max(1, nh - 1)}.get(dom, 1)
-    roof.update({"kernel": dom, "traffic": traffic, "traffic_source": tsrc,
+    # the same capture's pipe counters per stage kernel (north_star: each kernel
+    # justified by ncu counters -- HBM GB/s and integer-pipe utilisation)
+    ncu = None
+    try:
+        nj = json.load(open(os.path.join(ROOT, "profiles", "r1_ncu_metrics.json"))).get(args.config)
+        ncu = nj["kernels"] if nj else None
+    except (OSError, ValueError, KeyError):
+        pass
+    roof.update({"kernel": dom, "traffic": traffic, "traffic_source": tsrc, "ncu": ncu,
                  "algorithmic_bytes_per_launch": int(model[dom]["bytes"] // nlaunch),
                  "peak_source": "hbm: MEASURED_PEAKS.json hbm_gbs (measured); int: tc_int_peak "
                                 "register-only butterfly chain, measured live",
