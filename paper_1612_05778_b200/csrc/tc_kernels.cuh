@@ -784,12 +784,113 @@ __device__ __forceinline__ void yct_seg(uint32_t* s, int tile_bits, int lgL, con
     }
 }
 
+// y levels of tiles with narrow rows (lgL <= 4, e.g. C4's K = 1): the rounds
+// sit on absolute tile bits [BL, BL + NB) with lgL a template parameter, so
+// they are xct_round's rounds (same addressing and lane permutation) with the
+// y table's twiddles: stage bit b uses entry 2^(b - LGL) + (row bits below b).
+template <int LGL, int BL, int NB, bool DIF>
+__device__ __forceinline__ void ysm_round(uint32_t* s, int tile_bits, const uint2* twy, uint32_t p, uint32_t two_p,
+                                          Span sp) {
+    constexpr int R = 1 << NB;
+    static_assert(BL >= LGL, "y rounds start at the row bits");
+    constexpr uint32_t lowmask = (1u << BL) - 1;
+    constexpr bool PERMC = BL >= 1 && BL <= 4 && BL >= NB;
+    constexpr uint32_t pa = BL, pb = BL + 5 - NB;
+    const uint32_t pm = (PERMC && tile_bits >= 10) ? (1u << (5 - BL)) - 1 : 0u;
+    const uint32_t ngroups = 1u << (tile_bits - NB);
+    for (uint32_t g0 = sp.t0; g0 < ngroups; g0 += sp.nt) {
+        uint32_t g = g0;
+        if (PERMC) {
+            const uint32_t t = ((g >> pa) ^ (g >> pb)) & pm;
+            g ^= (t << pa) ^ (t << pb);
+        }
+        const uint32_t lo = g & lowmask;
+        uint32_t* sq = s + padi(((g & ~lowmask) << NB) | lo);
+        const uint2* tq = twy + (lo >> LGL);
+        uint32_t x[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) x[k] = sq[(k << BL) + ((k << BL) >> 5)];
+#pragma unroll
+        for (int it = 0; it < NB; ++it) {
+            const int lv = DIF ? NB - 1 - it : it;
+#pragma unroll
+            for (int m = 0; m < (1 << lv); ++m) {
+                const uint2 w = __ldg(tq + (1 << (BL + lv - LGL)) + ((m << BL) >> LGL));
+#pragma unroll
+                for (int jj = 0; jj < R / (2 << lv); ++jj) {
+                    const int k = m + jj * (2 << lv);
+                    if (DIF) bfly_dif(x[k], x[k + (1 << lv)], w.x, w.y, p, two_p);
+                    else bfly_dit(x[k], x[k + (1 << lv)], w.x, w.y, p, two_p);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) sq[(k << BL) + ((k << BL) >> 5)] = x[k];
+    }
+    __syncthreads();
+}
+
+// tile bits [LO, HI) in rounds of <= 4 bits (run_segment's partition)
+template <int LGL, int LO, int HI, bool DIF>
+__device__ __forceinline__ void ysm_seg(uint32_t* s, int tile_bits, const uint2* twy, uint32_t p, uint32_t two_p,
+                                        Span sp) {
+    constexpr int nbits = HI - LO;
+    if constexpr (nbits > 0) {
+        constexpr int nr = (nbits + 3) / 4;
+        constexpr int nb = nbits / nr + (nbits % nr ? 1 : 0);
+        if constexpr (!DIF) {
+            ysm_round<LGL, LO, nb, false>(s, tile_bits, twy, p, two_p, sp);
+            ysm_seg<LGL, LO + nb, HI, false>(s, tile_bits, twy, p, two_p, sp);
+        } else {
+            ysm_round<LGL, HI - nb, nb, true>(s, tile_bits, twy, p, two_p, sp);
+            ysm_seg<LGL, LO, HI - nb, true>(s, tile_bits, twy, p, two_p, sp);
+        }
+    }
+}
+
+// bits [LO, TB) split at bit 4 (rounds never straddle it)
+template <int LGL, int LO, int TB, bool DIF>
+__device__ __forceinline__ void ysm(uint32_t* s, const uint2* twy, uint32_t p, uint32_t two_p, Span sp) {
+    constexpr int mid = LO < 4 && TB > 4 ? 4 : LO;
+    if constexpr (mid == LO) {
+        ysm_seg<LGL, LO, TB, DIF>(s, TB, twy, p, two_p, sp);
+    } else if constexpr (!DIF) {
+        ysm_seg<LGL, LO, mid, false>(s, TB, twy, p, two_p, sp);
+        ysm_seg<LGL, mid, TB, false>(s, TB, twy, p, two_p, sp);
+    } else {
+        ysm_seg<LGL, mid, TB, true>(s, TB, twy, p, two_p, sp);
+        ysm_seg<LGL, LO, mid, true>(s, TB, twy, p, two_p, sp);
+    }
+}
+
+template <int LGL, bool DIF>
+__device__ __forceinline__ bool ysm_dispatch(uint32_t* s, int rb0, int tile_bits, const uint2* twy, uint32_t p,
+                                             uint32_t two_p, Span sp) {
+#define TC_YSCASE(R0, TB) case (R0) * 16 + (TB): ysm<LGL, LGL + R0, TB, DIF>(s, twy, p, two_p, sp); return true;
+    switch (rb0 * 16 + tile_bits) {
+        TC_YSCASE(0, 6) TC_YSCASE(0, 7) TC_YSCASE(0, 8) TC_YSCASE(0, 9) TC_YSCASE(0, 10) TC_YSCASE(0, 11)
+        TC_YSCASE(0, 12) TC_YSCASE(0, 13)
+        TC_YSCASE(1, 6) TC_YSCASE(1, 7) TC_YSCASE(1, 8) TC_YSCASE(1, 9) TC_YSCASE(1, 10) TC_YSCASE(1, 11)
+        TC_YSCASE(1, 12) TC_YSCASE(1, 13)
+        default: return false;
+    }
+#undef TC_YSCASE
+}
+
 // y levels [lgL + rb0, tile_bits) of a tile; false if the shape has no
 // compile-time schedule (caller runs the generic rounds).
 template <bool DIF>
 __device__ __noinline__ bool y_transform(uint32_t* s, int lgL, int rb0, int tile_bits, const uint2* twy,
                                          uint32_t p, uint32_t two_p, Span sp) {
     const int ny = tile_bits - lgL - rb0;
+    if (lgL >= 1 && lgL <= 4 && rb0 <= 1 && ny >= 1) {      // narrow rows
+        switch (lgL) {
+            case 1: return ysm_dispatch<1, DIF>(s, rb0, tile_bits, twy, p, two_p, sp);
+            case 2: return ysm_dispatch<2, DIF>(s, rb0, tile_bits, twy, p, two_p, sp);
+            case 3: return ysm_dispatch<3, DIF>(s, rb0, tile_bits, twy, p, two_p, sp);
+            default: return ysm_dispatch<4, DIF>(s, rb0, tile_bits, twy, p, two_p, sp);
+        }
+    }
     if (lgL < 5 || ny < 0 || ny > 12 || rb0 > 1) return false;
 #define TC_YCASE(R0, N) case (R0) * 16 + (N): yct_seg<R0, R0 + N, DIF>(s, tile_bits, lgL, twy, p, two_p, sp); break;
     switch (rb0 * 16 + ny) {
