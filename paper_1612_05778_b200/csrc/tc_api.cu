@@ -390,21 +390,21 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     return TC_OK;
 }
 
-template <int NT, int U, int MODE, int CB>
+template <int NT, int U, int MODE, int CB, bool GTW>
 cudaError_t launch_high_ct_mode(const HighArgs& A, dim3 grid, uint32_t n, cudaStream_t st) {
-    const size_t smem = (size_t)ct_tw_offset_words(n) * 4 + (MODE == MODE_MID ? 2 : 1) * ((size_t)8 << U);
+    const size_t smem = (size_t)ct_tw_offset_words(n) * 4 + (GTW ? 0 : (MODE == MODE_MID ? 2 : 1) * ((size_t)8 << U));
     cudaError_t e = cudaSuccess;
-    e = ensure_smem((const void*)k_high_ct<MODE, NT, U, CB>, smem);
+    e = ensure_smem((const void*)k_high_ct<MODE, NT, U, CB, GTW>, smem);
     if (e != cudaSuccess) return e;
-    k_high_ct<MODE, NT, U, CB><<<grid, NT, smem, st>>>(A);
+    k_high_ct<MODE, NT, U, CB, GTW><<<grid, NT, smem, st>>>(A);
     return cudaGetLastError();
 }
 
-template <int NT, int U, int CB = 4>
+template <int NT, int U, int CB = 4, bool GTW = false>
 cudaError_t launch_high_ct(int mode, const HighArgs& A, dim3 grid, uint32_t n, cudaStream_t st) {
-    if (mode == MODE_FWD) return launch_high_ct_mode<NT, U, MODE_FWD, CB>(A, grid, n, st);
-    if (mode == MODE_INV) return launch_high_ct_mode<NT, U, MODE_INV, CB>(A, grid, n, st);
-    return launch_high_ct_mode<NT, U, MODE_MID, CB>(A, grid, n, st);
+    if (mode == MODE_FWD) return launch_high_ct_mode<NT, U, MODE_FWD, CB, GTW>(A, grid, n, st);
+    if (mode == MODE_INV) return launch_high_ct_mode<NT, U, MODE_INV, CB, GTW>(A, grid, n, st);
+    return launch_high_ct_mode<NT, U, MODE_MID, CB, GTW>(A, grid, n, st);
 }
 
 int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint32_t* other, int u0, int U,
@@ -426,7 +426,16 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
     dim3 grid((unsigned)(G.S / n / sh.world), (unsigned)G.P);
     // compile-time pass shapes (k_high_ct): cb = 4, rows below u0 fixed per CTA
     // (8K-slot tiles with cb = 3 at 4 CTAs per SM measured slower: C2 MID 131 -> 180 us)
-    if (A.cb == 4 && G.lgL >= 4 && env_int("TC_HIGH_CT", 1)) {
+    static const int ct_env = env_int("TC_HIGH_CT", 1);
+    if (A.cb == 4 && G.lgL < 4 && ct_env && U == 10 && nth == 512) {
+        // narrow rows: the compile-time pass with its twiddles read through L1
+        const cudaError_t e = launch_high_ct<512, 10, 4, true>(mode, A, grid, n, c->st);
+        c->launches++;
+        if (e != cudaSuccess) return set_err(TC_ERR_CUDA, "k_high_ct launch failed: %s", cudaGetErrorString(e));
+        CKL();
+        return TC_OK;
+    }
+    if (A.cb == 4 && G.lgL >= 4 && ct_env) {
         cudaError_t e = cudaErrorNotSupported;
         if (U == 10 && nth == 512) e = launch_high_ct<512, 10>(mode, A, grid, n, c->st);
         else if (U == 9 && nth == 256) e = launch_high_ct<256, 9>(mode, A, grid, n, c->st);

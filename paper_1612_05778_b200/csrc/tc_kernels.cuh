@@ -1270,8 +1270,14 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (NT <= 256 ? TC_HIGH_MINB :
 // gathered once into shared memory: level v' entry a' at index 2^v' + a',
 // = twy[2^(u0+v') + rb + (a' << u0)] (TwHigh's index).
 // ---------------------------------------------------------------------------
-template <int TB, int BL, int NB, bool DIF, int NT, int CB>
-__device__ __forceinline__ void ct_round(uint32_t* s, const uint2* stw, uint32_t p, uint32_t two_p) {
+// Twiddles of a k_high_ct pass.  GTW = false: the CTA's 2^U - 1 twiddles staged
+// in shared memory (stw).  GTW = true (narrow rows, lgL < cb: the row offset
+// below u0 varies inside the tile): TwHigh's entries read through L1 (tw,
+// midc = mid << cb, lgL, u0).
+struct CtTw { const uint2* stw; const uint2* tw; uint32_t midc; int lgL, u0; };
+
+template <int TB, int BL, int NB, bool DIF, int NT, int CB, bool GTW = false>
+__device__ __forceinline__ void ct_round(uint32_t* s, const CtTw& T, uint32_t p, uint32_t two_p) {
     constexpr int R = 1 << NB;
     constexpr uint32_t ngroups = 1u << (TB - NB);
     constexpr uint32_t lowmask = (1u << BL) - 1;
@@ -1287,7 +1293,8 @@ __device__ __forceinline__ void ct_round(uint32_t* s, const uint2* stw, uint32_t
         }
         const uint32_t lo = g & lowmask;
         uint32_t* sp = s + padi(((g & ~lowmask) << NB) | lo);
-        const uint2* tq = stw + (lo >> CB);
+        const uint2* tq = GTW ? T.tw + ((T.midc | (lo & ((1u << CB) - 1))) >> T.lgL) + ((lo >> CB) << T.u0)
+                              : T.stw + (lo >> CB);
         uint32_t x[R];
 #pragma unroll
         for (int k = 0; k < R; ++k) x[k] = sp[(k << BL) + ((k << BL) >> 5)];
@@ -1297,7 +1304,8 @@ __device__ __forceinline__ void ct_round(uint32_t* s, const uint2* stw, uint32_t
             const int vp = BL + lv - CB;                       // level inside the pass
 #pragma unroll
             for (int m = 0; m < (1 << lv); ++m) {
-                const uint2 w = tq[(1 << vp) + (m << (BL - CB))];
+                const uint2 w = GTW ? __ldg(tq + (1u << (T.u0 + vp)) + ((uint32_t)m << (BL - CB + T.u0)))
+                                    : tq[(1 << vp) + (m << (BL - CB))];
 #pragma unroll
                 for (int jj = 0; jj < R / (2 << lv); ++jj) {
                     const int k = m + jj * (2 << lv);
@@ -1313,66 +1321,66 @@ __device__ __forceinline__ void ct_round(uint32_t* s, const uint2* stw, uint32_t
 }
 
 // Round schedule of a pass of U levels on tile bits [CB, CB + U).
-template <int U, bool DIF, int NT, int CB>
-__device__ __forceinline__ void ct_pass(uint32_t* s, const uint2* stw, uint32_t p, uint32_t two_p) {
+template <int U, bool DIF, int NT, int CB, bool GTW = false>
+__device__ __forceinline__ void ct_pass(uint32_t* s, const CtTw& stw, uint32_t p, uint32_t two_p) {
     constexpr int TB = U + CB;
 #if TC_CT_R32
     if constexpr (U == 10) {            // two radix-32 rounds (bit 4's half-warps 512 slots apart: no permutation)
         if (!DIF) {
-            ct_round<TB, CB, 5, false, NT, CB>(s, stw, p, two_p);
-            ct_round<TB, CB + 5, 5, false, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB, 5, false, NT, CB, GTW>(s, stw, p, two_p);
+            ct_round<TB, CB + 5, 5, false, NT, CB, GTW>(s, stw, p, two_p);
         } else {
-            ct_round<TB, CB + 5, 5, true, NT, CB>(s, stw, p, two_p);
-            ct_round<TB, CB, 5, true, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB + 5, 5, true, NT, CB, GTW>(s, stw, p, two_p);
+            ct_round<TB, CB, 5, true, NT, CB, GTW>(s, stw, p, two_p);
         }
     } else if constexpr (U == 9) {
         if (!DIF) {
-            ct_round<TB, CB, 5, false, NT, CB>(s, stw, p, two_p);
-            ct_round<TB, CB + 5, 4, false, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB, 5, false, NT, CB, GTW>(s, stw, p, two_p);
+            ct_round<TB, CB + 5, 4, false, NT, CB, GTW>(s, stw, p, two_p);
         } else {
-            ct_round<TB, CB + 5, 4, true, NT, CB>(s, stw, p, two_p);
-            ct_round<TB, CB, 5, true, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB + 5, 4, true, NT, CB, GTW>(s, stw, p, two_p);
+            ct_round<TB, CB, 5, true, NT, CB, GTW>(s, stw, p, two_p);
         }
     } else if constexpr (U == 8) {      // two radix-16 rounds
         if (!DIF) {
-            ct_round<TB, CB, 4, false, NT, CB>(s, stw, p, two_p);
-            ct_round<TB, CB + 4, 4, false, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB, 4, false, NT, CB, GTW>(s, stw, p, two_p);
+            ct_round<TB, CB + 4, 4, false, NT, CB, GTW>(s, stw, p, two_p);
         } else {
-            ct_round<TB, CB + 4, 4, true, NT, CB>(s, stw, p, two_p);
-            ct_round<TB, CB, 4, true, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB + 4, 4, true, NT, CB, GTW>(s, stw, p, two_p);
+            ct_round<TB, CB, 4, true, NT, CB, GTW>(s, stw, p, two_p);
         }
     } else {
 #else
     if constexpr (U == 10) {
         if (!DIF) {
-            ct_round<TB, CB, 4, false, NT, CB>(s, stw, p, two_p);
-            ct_round<TB, CB + 4, 3, false, NT, CB>(s, stw, p, two_p);
-            ct_round<TB, CB + 7, 3, false, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB, 4, false, NT, CB, GTW>(s, stw, p, two_p);
+            ct_round<TB, CB + 4, 3, false, NT, CB, GTW>(s, stw, p, two_p);
+            ct_round<TB, CB + 7, 3, false, NT, CB, GTW>(s, stw, p, two_p);
         } else {
-            ct_round<TB, CB + 7, 3, true, NT, CB>(s, stw, p, two_p);
-            ct_round<TB, CB + 4, 3, true, NT, CB>(s, stw, p, two_p);
-            ct_round<TB, CB, 4, true, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB + 7, 3, true, NT, CB, GTW>(s, stw, p, two_p);
+            ct_round<TB, CB + 4, 3, true, NT, CB, GTW>(s, stw, p, two_p);
+            ct_round<TB, CB, 4, true, NT, CB, GTW>(s, stw, p, two_p);
         }
     } else if constexpr (U == 9) {
         if (!DIF) {
-            ct_round<TB, CB, 3, false, NT, CB>(s, stw, p, two_p);
-            ct_round<TB, CB + 3, 3, false, NT, CB>(s, stw, p, two_p);
-            ct_round<TB, CB + 6, 3, false, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB, 3, false, NT, CB, GTW>(s, stw, p, two_p);
+            ct_round<TB, CB + 3, 3, false, NT, CB, GTW>(s, stw, p, two_p);
+            ct_round<TB, CB + 6, 3, false, NT, CB, GTW>(s, stw, p, two_p);
         } else {
-            ct_round<TB, CB + 6, 3, true, NT, CB>(s, stw, p, two_p);
-            ct_round<TB, CB + 3, 3, true, NT, CB>(s, stw, p, two_p);
-            ct_round<TB, CB, 3, true, NT, CB>(s, stw, p, two_p);
+            ct_round<TB, CB + 6, 3, true, NT, CB, GTW>(s, stw, p, two_p);
+            ct_round<TB, CB + 3, 3, true, NT, CB, GTW>(s, stw, p, two_p);
+            ct_round<TB, CB, 3, true, NT, CB, GTW>(s, stw, p, two_p);
         }
     } else {
 #endif
         static_assert(U == 4, "unsupported compile-time pass");
-        ct_round<TB, CB, 4, DIF, NT, CB>(s, stw, p, two_p);
+        ct_round<TB, CB, 4, DIF, NT, CB, GTW>(s, stw, p, two_p);
     }
 }
 
 __host__ __device__ constexpr uint32_t ct_tw_offset_words(uint32_t n) { return (padded_words(n) + 1) & ~1u; }
 
-template <int MODE, int NT, int U, int CB = 4>
+template <int MODE, int NT, int U, int CB = 4, bool GTW = false>
 __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (CB == 3 ? 4 : (NT <= 256 ? TC_HIGH_MINB : 2))) k_high_ct(HighArgs A) {
     constexpr int TB = U + CB;
     constexpr uint32_t n = 1u << TB, ntw = 1u << U;
@@ -1407,8 +1415,9 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (CB == 3 ? 4 : (NT <= 256 ?
     for (uint32_t e = threadIdx.x; e < n; e += NT) cp_async4(s + padi(e), g + hidx(e));   // all in flight
     cp_async_commit();
 #endif
-    // CTA twiddles (requires lgL >= CB: the row bits below u0 come from mid only)
-    {
+    // CTA twiddles (requires lgL >= CB: the row bits below u0 come from mid only;
+    // narrow rows (GTW) read them through L1 instead)
+    if (!GTW) {
         const uint32_t rb = mid >> (A.lgL - CB);
         const uint2* twf = A.twf + (int64_t)q * A.tw_stride;
         const uint2* twi = A.twi + (int64_t)q * A.tw_stride;
@@ -1426,7 +1435,8 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (CB == 3 ? 4 : (NT <= 256 ?
     tile_load<TC_HIGH_BATCH>(s, g, n, hidx);
 #endif
     __syncthreads();
-    if (MODE == MODE_FWD || MODE == MODE_MID) ct_pass<U, false, NT, CB>(s, stw_f, pc.p, pc.two_p);
+    const CtTw tf{stw_f, A.twf + (int64_t)q * A.tw_stride, mid << CB, A.lgL, A.u0};
+    if (MODE == MODE_FWD || MODE == MODE_MID) ct_pass<U, false, NT, CB, GTW>(s, tf, pc.p, pc.two_p);
     if (MODE == MODE_MID) {
         const uint32_t* ga = A.other + (int64_t)q * qstride;
         constexpr uint32_t nv = n >> 2;
@@ -1456,7 +1466,8 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (CB == 3 ? 4 : (NT <= 256 ?
         }
         __syncthreads();
     }
-    if (MODE == MODE_INV || MODE == MODE_MID) ct_pass<U, true, NT, CB>(s, stw_i, pc.p, pc.two_p);
+    const CtTw ti{stw_i, A.twi + (int64_t)q * A.tw_stride, mid << CB, A.lgL, A.u0};
+    if (MODE == MODE_INV || MODE == MODE_MID) ct_pass<U, true, NT, CB, GTW>(s, ti, pc.p, pc.two_p);
     tile_store(g, s, n, hidx);
 }
 
