@@ -7,8 +7,10 @@ two all-to-all transposes (the north_star's "x/y transpose done as an NCCL
 all-to-all").  All P primes live on every rank.  Phases are C-ABI calls
 (include/tc_api.h, tc_shard_*); exchanges are pluggable:
 
-* TorchExchange -- torch.distributed all_to_all_single per prime (NCCL over
-  NVLink when the process group is "nccl"), one process per GPU;
+* torch.distributed, one process per GPU: with NCCL every exchange of a
+  phase (all primes, both operands) is ONE group of point-to-point transfers
+  over NVLink (torch_exchange_grouped); otherwise (gloo) all_to_all_single
+  per prime (torch_all_to_all);
 * LocalExchange -- `world` virtual ranks inside one process on one GPU (each
   with its own library context), exchanging by device-to-device copies.  Used
   by the single-GPU parity tests; the kernels never wait on one another.
@@ -206,6 +208,36 @@ def torch_all_to_all(send, recv, world: int):
         recv.copy_(r_)
 
 
+def torch_exchange_grouped(pairs, world: int):
+    """Several exchanges at once as ONE group of point-to-point transfers
+    (torch batch_isend_irecv: a single NCCL group launch over NVLink instead
+    of one all_to_all_single per prime and operand).  `pairs` are (send, recv)
+    (P, shard_words) tensors with the layout of torch_all_to_all; this rank's
+    own peer block is a local copy."""
+    import torch.distributed as dist
+    rank = dist.get_rank()
+    ops = []
+    for send, recv in pairs:
+        P, sw = send.shape
+        pw = sw // world
+        for q in range(P):
+            for t in range(world):
+                if t == rank:
+                    recv[q, rank * pw:(rank + 1) * pw].copy_(send[q, rank * pw:(rank + 1) * pw])
+                    continue
+                ops.append(dist.P2POp(dist.isend, send[q, t * pw:(t + 1) * pw], t))
+                ops.append(dist.P2POp(dist.irecv, recv[q, t * pw:(t + 1) * pw], t))
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+
+
+def _grouped_ok() -> bool:
+    import os
+    import torch.distributed as dist
+    return dist.get_backend() == "nccl" and os.environ.get("TC_SHARD_GROUPED", "1") != "0"
+
+
 def torch_gather(t, out_list, dst: int = 0):
     import torch.distributed as dist
     if t.is_cuda and _host_staged():
@@ -289,13 +321,19 @@ class DistributedMultiplier:
         _lib.check(lib.tc_shard_low(h, tp, rank, world, 0, a.bit_width, self.send_a.data_ptr()), "shard_low")
         _lib.check(lib.tc_shard_low(h, tp, rank, world, 1, b.bit_width, self.send_b.data_ptr()), "shard_low")
         self._sync()
-        torch_all_to_all(self.send_a, self.mid_a, world)
-        torch_all_to_all(self.send_b, self.mid_b, world)
+        if _grouped_ok():
+            torch_exchange_grouped([(self.send_a, self.mid_a), (self.send_b, self.mid_b)], world)
+        else:
+            torch_all_to_all(self.send_a, self.mid_a, world)
+            torch_all_to_all(self.send_b, self.mid_b, world)
         t.cuda.synchronize(self.device)
         _lib.check(lib.tc_shard_high(h, tp, rank, world, self.mid_a.data_ptr(), self.mid_b.data_ptr()),
                    "shard_high")
         self._sync()
-        torch_all_to_all(self.mid_b, self.recv_b, world)
+        if _grouped_ok():
+            torch_exchange_grouped([(self.mid_b, self.recv_b)], world)
+        else:
+            torch_all_to_all(self.mid_b, self.recv_b, world)
         t.cuda.synchronize(self.device)
         err = ctypes.c_int64(-1)
         rc = lib.tc_shard_final(h, tp, rank, world, self.recv_b.data_ptr(), rows, out_cw,

@@ -33,28 +33,36 @@ def _tags(rank, primes, shard_words):
     return [[(rank << 24) | (q << 20) | i for i in range(shard_words)] for q in range(primes)]
 
 
-def _worker(rank, world, port, primes, shard_words, out):
+def _worker(rank, world, port, primes, shard_words, grouped, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_1612_05778_b200.shard import torch_all_to_all
+    from paper_1612_05778_b200.shard import torch_all_to_all, torch_exchange_grouped
     send = torch.tensor(_tags(rank, primes, shard_words), dtype=torch.int32)
     recv = torch.empty_like(send)
-    torch_all_to_all(send, recv, world)
-    out[rank] = recv.numpy().copy()
+    if grouped:        # the NCCL path's grouped point-to-point exchange (two at once, as after k_low)
+        send2 = send + 7
+        recv2 = torch.empty_like(send)
+        torch_exchange_grouped([(send, recv), (send2, recv2)], world)
+        out[rank] = (recv.numpy().copy(), (recv2 - 7).numpy().copy())
+    else:
+        torch_all_to_all(send, recv, world)
+        out[rank] = (recv.numpy().copy(),)
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,primes,shard_words", [(2, 3, 64), (2, 1, 16)])
-def test_torch_exchange_matches_layout_contract(world, primes, shard_words):
+@pytest.mark.parametrize("world,primes,shard_words,grouped",
+                         [(2, 3, 64, False), (2, 1, 16, False), (2, 3, 64, True), (3, 2, 48, True)])
+def test_torch_exchange_matches_layout_contract(world, primes, shard_words, grouped):
     from paper_1612_05778_b200.shard import exchange_slices
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), primes, shard_words, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), primes, shard_words, grouped, out), nprocs=world, join=True)
     info = _Info(primes, shard_words, world)
     sends = [np.array(_tags(r, primes, shard_words), dtype=np.int32).reshape(-1) for r in range(world)]
     exp = [np.zeros(primes * shard_words, dtype=np.int32) for _ in range(world)]
     for s, t, q, so, do, w in exchange_slices(world, info):
         exp[t][do:do + w] = sends[s][so:so + w]
     for r in range(world):
-        assert np.array_equal(out[r].reshape(-1), exp[r])
+        for got in out[r]:
+            assert np.array_equal(got.reshape(-1), exp[r])
