@@ -110,6 +110,22 @@ def test_gpu_plan_invariants():
         assert pl.s_y >= 2 * d - 1 and pl.s_y & (pl.s_y - 1) == 0
 
 
+def test_gpu_plans_of_the_baseline_configs():
+    # the plans DESIGN.md section 2 documents (each measured against the
+    # alternatives on the B200): two-word digits where the grid is large
+    exp = {(1024, 1025): (32, 33, 3), (8192, 8193): (128, 65, 5), (65536, 65537): (1024, 65, 6),
+           (1 << 20, 64): (1, 64, 5), (256, 262145): (4096, 65, 5)}
+    for (d, n_in), (K, M, P) in exp.items():
+        pl = params.plan_gpu(d, d, n_in)
+        assert (pl.K, pl.M, pl.P) == (K, M, P), pl.describe()
+    # the C2 two-word plan is feasible with exactly five 30-bit primes
+    pl = params.plan_gpu(8192, 8192, 8193)
+    prod = 1
+    for s in pl.primes:
+        prod *= s.p
+    assert prod > 2 * pl.coefficient_bound() and prod // pl.primes[-1].p <= 2 * pl.coefficient_bound()
+
+
 def test_workload_generators_match_recorded_hashes():
     cfg = json.load(open(os.path.join(GOLDEN, "configs.json")))
     for name in ("C1", "C2", "C5", "C4"):
