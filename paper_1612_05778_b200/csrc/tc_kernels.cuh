@@ -1581,6 +1581,7 @@ struct FinalArgs {
     int co_aw;                     // > 0: grouped ConvertOut with M = 32 co_aw + {0, 1} (host-checked)
     int co_fused;                  // grouped ConvertOut lifts the residues itself (no in-place CRT pass)
     int dual_ok;                   // allow two primes' transforms side by side (small tiles)
+    int co_stage;                  // grouped ConvertOut stages product words after the tiles (coalesced stores)
 };
 
 // ---------------------------------------------------------------------------
@@ -1630,15 +1631,23 @@ __device__ __forceinline__ void static_for(F&& f) {
     if constexpr (K < N) { f(std::integral_constant<int, K>{}); static_for<K + 1, N>(f); }
 }
 
-template <int P, int AW, bool FUSED>
+template <int P>
+__host__ __device__ constexpr int co_stage_words() { return 32 * (2 * 4 + 1) + 2 * 3 + P + 1; }   // max over AW <= 2
+
+// ost: per-warp staging of the product words (coalesced stores), or nullptr
+template <int P, int AW, bool FUSED, int NTH>
 __device__ __forceinline__ void crt_convert_grouped(const FinalArgs& A, const CrtConst& cc, const uint32_t* sm,
-                                                    uint32_t stride, int R, uint32_t pos0, bool sharded) {
+                                                    uint32_t stride, int R, uint32_t pos0, bool sharded,
+                                                    uint32_t* ost) {
     constexpr int G = 4, NA = AW * (G - 1) + P + 1, NT = NA - AW * G;
     static_assert(NT >= 1 && AW * G - 1 >= NT, "tail must not reach the sender's last owned word");
     static_assert(NT <= 8, "tail carry counts are packed in one register");
     __shared__ uint32_t stail[2][32][NT + 1];
     __shared__ uint32_t shi[2][32];
     __shared__ uint32_t gwtf[32], gwcin[32], gcarry;
+    // a warp's product words are staged in ost (its slice: co_stage_words) so
+    // that its global stores are coalesced (a warp's 32 groups share one row
+    // when a row has >= 32 groups; lanes own <= AW G + 1 words, a row's last NA)
     const int L = 1 << A.lgL, lgng = A.lgL - 2, ngr = L >> 2;
     const int M = A.M, W32 = A.W32;
     const bool bodd = (M & 31) != 0;
@@ -1779,10 +1788,26 @@ __device__ __forceinline__ void crt_convert_grouped(const FinalArgs& A, const Cr
         uint32_t c = (uint32_t)(((A1 + B1 + gwcin[warp]) ^ A1 ^ B1) >> lane) & 1u;
         uint32_t* orow = sharded ? A.out + ((int64_t)blockIdx.x * R + r) * W32 : A.out + (int64_t)prow * W32;
         const bool store = sharded || prow < A.rows_out;
+        if (ost != nullptr && ngr >= 32) {
+            const int wb0 = __shfl_sync(0xffffffffu, ub, 0);
+            uint32_t* st = ost + warp * co_stage_words<P>();
 #pragma unroll
-        for (int k = 0; k < NA; ++k) {
-            if (((om >> k) & 1u) && store) orow[ub + k] = tw[k] + c;
-            c = ((gm >> k) & 1u) | (((pm >> k) & 1u) & c);
+            for (int k = 0; k < NA; ++k) {
+                if ((om >> k) & 1u) st[ub + k - wb0] = tw[k] + c;
+                c = ((gm >> k) & 1u) | (((pm >> k) & 1u) & c);
+            }
+            const int myend = om ? ub + 32 - __clz(om) - wb0 : 0;   // owned words are contiguous from ub
+            const int nwd = (int)__reduce_max_sync(0xffffffffu, (unsigned)myend);
+            __syncwarp();
+            if (store)
+                for (int i = lane; i < nwd; i += 32) orow[wb0 + i] = st[i];
+            __syncwarp();
+        } else {
+#pragma unroll
+            for (int k = 0; k < NA; ++k) {
+                if (((om >> k) & 1u) && store) orow[ub + k] = tw[k] + c;
+                c = ((gm >> k) & 1u) | (((pm >> k) & 1u) & c);
+            }
         }
     }
 }
@@ -1855,15 +1880,17 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
             x_transform<false>(t, A.lgL, tile_bits, tw.twx, pc.p, pc.two_p, cta_span());      // x: DIT
         }
     }
+    // grouped ConvertOut staging: a dynamic region after the P tiles (host-sized)
+    uint32_t* co_ost = A.co_stage ? sm + P * stride : nullptr;
 #ifndef TC_CO_FUSED_BUILD
 #define TC_CO_FUSED_BUILD 0     // fused CRT in the grouped path: spills at 64 registers (P >= 5)
 #endif
     if constexpr (!DUMP && P <= 8 && TC_CO_FUSED_BUILD) {
         if (A.co_fused) {
             if constexpr (P >= 2)
-                if (A.co_aw == 2) { crt_convert_grouped<P, 2, true>(A, cc, sm, stride, R, pos0, sharded); return; }
+                if (A.co_aw == 2) { crt_convert_grouped<P, 2, true, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }
             if constexpr (P <= 3)
-                if (A.co_aw == 1) { crt_convert_grouped<P, 1, true>(A, cc, sm, stride, R, pos0, sharded); return; }
+                if (A.co_aw == 1) { crt_convert_grouped<P, 1, true, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }
         }
     }
     // CRT in place
@@ -1892,9 +1919,9 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
     __syncthreads();
     if constexpr (P <= 8) {
         if constexpr (P >= 2)
-            if (A.co_aw == 2) { crt_convert_grouped<P, 2, false>(A, cc, sm, stride, R, pos0, sharded); return; }
+            if (A.co_aw == 2) { crt_convert_grouped<P, 2, false, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }
         if constexpr (P <= 3)
-            if (A.co_aw == 1) { crt_convert_grouped<P, 1, false>(A, cc, sm, stride, R, pos0, sharded); return; }
+            if (A.co_aw == 1) { crt_convert_grouped<P, 1, false, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }
     }
 
     // ConvertOut over the tile's rows, kW words per thread (rows padded to a
