@@ -21,14 +21,18 @@ cudaError_t launch_final_t(bool dump, FinalArgs A, const CrtConst& cc, unsigned 
         if (e != cudaSuccess) return e;                                                           \
         k_final<P, DUMP, NT><<<grid, NT, smem, st>>>(A, cc);                                     \
     } while (0)
+    static const int stage_env = [] { const char* v = getenv("TC_CO_STAGE"); return v && *v ? atoi(v) : 1; }();
     if (dump) { if (big) TC_LAUNCH(true, 1024); else TC_LAUNCH(true, 512); }
-    else if (big) TC_LAUNCH(false, 1024);
+    else if (big) {
+        const size_t stage = (size_t)(1024 / 32) * co_stage_words<P>() * 4;    // one CTA per SM anyway
+        if (stage_env && P <= 8 && A.co_aw > 0 && smem + stage <= 224 * 1024) { A.co_stage = 1; smem += stage; }
+        TC_LAUNCH(false, 1024);
+    }
     // 256 threads when >= 3 CTAs fit an SM (C3: 22.7 -> 19.2 ms), 512 at 2 per SM (C2)
     else if (ft == 256 || (ft == 0 && smem <= 76 * 1024)) TC_LAUNCH(false, 256);
     else {
         // 512 threads: the grouped ConvertOut's per-warp staging of product words
         // (coalesced stores) when it still leaves two CTAs per SM
-        static const int stage_env = [] { const char* v = getenv("TC_CO_STAGE"); return v && *v ? atoi(v) : 1; }();
         const size_t stage = (size_t)(512 / 32) * co_stage_words<P>() * 4;
         if (stage_env && P <= 8 && A.co_aw > 0 && smem + stage <= 112 * 1024) { A.co_stage = 1; smem += stage; }
         TC_LAUNCH(false, 512);
