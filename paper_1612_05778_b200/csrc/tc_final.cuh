@@ -11,9 +11,9 @@ template <int P>
 cudaError_t launch_final_t(bool dump, FinalArgs A, const CrtConst& cc, unsigned grid, size_t smem,
                            cudaStream_t st) {
     // a tile too large for two CTAs per SM gets 32 warps in one CTA
-    const bool big = smem > 112 * 1024;
     const char* ev = getenv("TC_FINAL_THREADS");
     const int ft = ev && *ev ? atoi(ev) : 0;
+    const bool big = smem > 112 * 1024 || ft == 1024;
     cudaError_t e = cudaSuccess;
 #define TC_LAUNCH(DUMP, NT)                                                                       \
     do {                                                                                          \
