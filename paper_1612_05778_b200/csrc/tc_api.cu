@@ -536,6 +536,8 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
         A.co_fused = fused;
         static const int fdual = env_int("TC_FINAL_DUAL", 1);
         A.dual_ok = fdual;
+        static const int stage = env_int("TC_CO_STAGE", 1);
+        A.co_nostage = !stage;
     }
     const uint32_t n = 1u << (G.lgL + G.yl);
     const size_t smem = (size_t)G.P * padded_words(n) * 4;

@@ -31,8 +31,9 @@ cudaError_t launch_final_t(bool dump, FinalArgs A, const CrtConst& cc, unsigned 
     // 256 threads when >= 3 CTAs fit an SM (C3: 22.7 -> 19.2 ms), 512 at 2 per SM (C2)
     else if (ft == 256 || (ft == 0 && smem <= 76 * 1024)) TC_LAUNCH(false, 256);
     else {
-        // 512 threads: the grouped ConvertOut's per-warp staging of product words
-        // (coalesced stores) when it still leaves two CTAs per SM
+        // 512 threads: a dedicated region for the grouped ConvertOut's per-warp
+        // staging of product words when it still leaves two CTAs per SM (else
+        // the kernel stages in the warps' dead limb slots: C2 152 vs 156 us)
         const size_t stage = (size_t)(512 / 32) * co_stage_words<P>() * 4;
         if (stage_env && P <= 8 && A.co_aw > 0 && smem + stage <= 112 * 1024) { A.co_stage = 1; smem += stage; }
         TC_LAUNCH(false, 512);

@@ -1582,6 +1582,7 @@ struct FinalArgs {
     int co_fused;                  // grouped ConvertOut lifts the residues itself (no in-place CRT pass)
     int dual_ok;                   // allow two primes' transforms side by side (small tiles)
     int co_stage;                  // grouped ConvertOut stages product words after the tiles (coalesced stores)
+    int co_nostage;                // grouped ConvertOut stores straight from registers (A/B)
 };
 
 // ---------------------------------------------------------------------------
@@ -1788,19 +1789,29 @@ __device__ __forceinline__ void crt_convert_grouped(const FinalArgs& A, const Cr
         uint32_t c = (uint32_t)(((A1 + B1 + gwcin[warp]) ^ A1 ^ B1) >> lane) & 1u;
         uint32_t* orow = sharded ? A.out + ((int64_t)blockIdx.x * R + r) * W32 : A.out + (int64_t)prow * W32;
         const bool store = sharded || prow < A.rows_out;
-        if (ost != nullptr && ngr >= 32) {
+        // staging in the host-sized region after the tiles, or in place: the
+        // warp's own limb slots (terms [j0(lane 0), +128) of this row in tiles
+        // 0..2), dead once its accumulation is done
+        constexpr bool kInplace = AW == 1 ? P >= 2 : P >= 3;
+        if (ngr >= 32 && !A.co_nostage && (kInplace || ost != nullptr)) {
             const int wb0 = __shfl_sync(0xffffffffu, ub, 0);
+            const uint32_t sbase = rowbase + (uint32_t)__shfl_sync(0xffffffffu, j0, 0);
+            uint32_t* smw = const_cast<uint32_t*>(sm);
             uint32_t* st = ost + warp * co_stage_words<P>();
+            const bool inplace = ost == nullptr;                   // a dedicated region when the host gave one
+            auto sp = [&](int i) -> uint32_t* {
+                return inplace ? smw + (uint32_t)(i >> 7) * stride + padi(sbase + (uint32_t)(i & 127)) : st + i;
+            };
 #pragma unroll
             for (int k = 0; k < NA; ++k) {
-                if ((om >> k) & 1u) st[ub + k - wb0] = tw[k] + c;
+                if ((om >> k) & 1u) *sp(ub + k - wb0) = tw[k] + c;
                 c = ((gm >> k) & 1u) | (((pm >> k) & 1u) & c);
             }
             const int myend = om ? ub + 32 - __clz(om) - wb0 : 0;   // owned words are contiguous from ub
             const int nwd = (int)__reduce_max_sync(0xffffffffu, (unsigned)myend);
             __syncwarp();
             if (store)
-                for (int i = lane; i < nwd; i += 32) orow[wb0 + i] = st[i];
+                for (int i = lane; i < nwd; i += 32) orow[wb0 + i] = *sp(i);
             __syncwarp();
         } else {
 #pragma unroll
