@@ -959,7 +959,20 @@ static __device__ __noinline__ bool y_transform_expand(uint32_t* s, int lgL, int
     const int ny = tile_bits - lgL - 1;          // y levels after the duplication
     if (lgL < 5) return false;
     switch (ny) {
-        case 0: yct_expand_columns<0>(s, lgL, twy, p, two_p, gout, sp); return true;   // the duplication alone
+        case 0:                                  // the duplication alone
+            if (gout) {                          // 4 columns per thread, two 16-byte stores
+                const uint32_t L = 1u << lgL;
+                for (uint32_t c4 = sp.t0; c4 < (L >> 2); c4 += sp.nt) {
+                    const uint32_t* q = s + padi(c4 << 2);           // 4 slots inside one 32-slot run
+                    const uint4 v = make_uint4(q[0], q[1], q[2], q[3]);
+                    *reinterpret_cast<uint4*>(gout + (c4 << 2)) = v;
+                    *reinterpret_cast<uint4*>(gout + L + (c4 << 2)) = v;
+                }
+                __syncthreads();
+            } else {
+                yct_expand_columns<0>(s, lgL, twy, p, two_p, gout, sp);
+            }
+            return true;
         case 1: yct_expand_columns<1>(s, lgL, twy, p, two_p, gout, sp); return true;
         case 2: yct_expand_columns<2>(s, lgL, twy, p, two_p, gout, sp); return true;
         case 3: yct_expand_columns<3>(s, lgL, twy, p, two_p, gout, sp); return true;
