@@ -10,8 +10,11 @@ import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass",
-                      "--kernel-name", f"regex:{kern}"], capture_output=True, text=True).stdout
+if rep.endswith(".csv"):      # a source page already exported on the GPU box
+    out = open(rep).read()
+else:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass",
+                          "--kernel-name", f"regex:{kern}"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 fname, hdr, data = "", None, []
 for r in rows:
