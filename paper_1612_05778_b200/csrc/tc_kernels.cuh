@@ -1083,12 +1083,12 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
         }
         return;
     }
-    // coefficient words staged in the (not yet used) tile buffer when they fit,
-    // unless a thread's digits span >= 8 words (D >= 8 digits of M > 63 bits:
-    // the lanes' staged reads then hit the same banks 8 ways; reading the
-    // words through L1 instead measured C5 k_low 203 -> 190 us)
-    const bool staged = (int64_t)Rc * A.src.cw * 8 <= (int64_t)padded_words(n) * 4 &&
-                        !(wide && (int64_t)Rc * A.src.K >= 8 * (int64_t)blockDim.x);
+    // coefficient words staged in the (not yet used) tile buffer when they fit;
+    // two-word digits read them through L1 instead: a thread's D consecutive
+    // digits span ~D*M/64 words, so the lanes' staged 64-bit reads conflict
+    // D/2..D ways (measured unstaged: C2 k_low 166 -> 154 us, C3 8.98 -> 8.49
+    // ms, C5 203 -> 189 us)
+    const bool staged = !wide && (int64_t)Rc * A.src.cw * 8 <= (int64_t)padded_words(n) * 4;
     if (!wide) {
         if (staged) compute_digits_staged<int64_t>(A.src, Rc, coeff, dig, ds, reinterpret_cast<uint64_t*>(tile));
         else compute_digits<int64_t>(A.src, Rc, coeff, dig, ds);
