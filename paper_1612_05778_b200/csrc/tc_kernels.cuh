@@ -63,7 +63,8 @@ constexpr int kMaxPrimes = 16;
 #define TC_HIGH_ASYNC 0     // k_high_ct: whole-tile cp.async loads (all in flight) instead of LDG batches
 #endif
 #ifndef TC_HIGH_BATCH
-#define TC_HIGH_BATCH 4     // k_high_ct: 16-byte tile loads in flight per thread
+#define TC_HIGH_BATCH 0     // k_high_ct: 16-byte tile loads in flight per thread; 0: 8 for 256-thread
+                            // CTAs (C3 FWD 10.0 -> 9.1 ms, C5 FWD 59 -> 55 us), 4 for 512 (C2: 8 is +3 %)
 #endif
 #ifndef TC_MID_BATCH
 #define TC_MID_BATCH 8      // k_high_ct MID: 16-byte loads of A in flight per thread (8: C2 MID 168 -> 157 us)
@@ -1449,7 +1450,7 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (CB == 3 ? 4 : (NT <= 256 ?
 #if TC_HIGH_ASYNC
     cp_async_wait<0>();
 #else
-    tile_load<TC_HIGH_BATCH>(s, g, n, hidx);
+    tile_load<TC_HIGH_BATCH ? TC_HIGH_BATCH : (NT <= 256 ? 8 : 4)>(s, g, n, hidx);
 #endif
     __syncthreads();
     const CtTw tf{stw_f, A.twf + (int64_t)q * A.tw_stride, mid << CB, A.lgL, A.u0};
