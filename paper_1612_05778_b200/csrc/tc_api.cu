@@ -556,6 +556,10 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
         A.dual_ok = fdual;
         static const int stage = env_int("TC_CO_STAGE", 1);
         A.co_nostage = !stage;
+        // word-per-thread path: 2 words per thread on short rows (C4, 6 words:
+        // k_final -12 %; C2's 514-word rows: +2 %)
+        static const int kw2 = env_int("TC_CO_KW2_MAX", 16);
+        A.co_kw = W32 <= kw2 ? 2 : 4;
     }
     const uint32_t n = 1u << (G.lgL + G.yl);
     const size_t smem = (size_t)G.P * padded_words(n) * 4;

@@ -1609,6 +1609,7 @@ struct FinalArgs {
     int dual_ok;                   // allow two primes' transforms side by side (small tiles)
     int co_stage;                  // grouped ConvertOut stages product words after the tiles (coalesced stores)
     int co_nostage;                // grouped ConvertOut stores straight from registers (A/B)
+    int co_kw;                     // word-per-thread ConvertOut: words per thread (2, or TC_CO_KW)
 };
 
 // ---------------------------------------------------------------------------
@@ -1849,118 +1850,16 @@ __device__ __forceinline__ void crt_convert_grouped(const FinalArgs& A, const Cr
     }
 }
 
-template <int P, bool DUMP, int NT>
-__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_final(FinalArgs A, const __grid_constant__ CrtConst cc) {
-    extern __shared__ __align__(16) uint32_t sm[];
+// Word-per-thread ConvertOut (any M; the grouped path covers M = 32 AW + {0, 1}
+// with L >= 4), kW words per thread: 2 for short rows (C4: 6-word rows,
+// k_final -12 %), TC_CO_KW otherwise.
+template <int P, int kW>
+__device__ __forceinline__ void convert_out_words(const FinalArgs& A, const uint32_t* sm, uint32_t stride, int R,
+                                                  int L, uint32_t pos0, bool sharded) {
     __shared__ uint32_t wtf[32], wcin1[32];
     __shared__ int64_t whi[32];
     __shared__ uint32_t s_c1;
     __shared__ int64_t s_hi;
-    __shared__ int s_any;
-    const int R = 1 << A.yl;
-    const int L = 1 << A.lgL;
-    const int tile_bits = A.lgL + A.yl;
-    const uint32_t n = 1u << tile_bits;
-    const uint32_t stride = padded_words(n);
-    const bool sharded = A.sh.world > 1;
-    const uint32_t tile = sharded ? blockIdx.x + (uint32_t)A.sh.h0 : bitrev(A.x0 + blockIdx.x, A.lgT);
-    const uint32_t pos0 = tile * (uint32_t)R;
-    if (threadIdx.x == 0) s_any = 0;
-    __syncthreads();
-    for (int r = threadIdx.x; r < R; r += blockDim.x)
-        if (bitrev(pos0 + r, A.lgS) < A.rows_out) s_any = 1;
-    __syncthreads();
-    if (!s_any) return;      // every row of this tile is zero padding
-
-    // all P tiles stream in at once (one cp.async group per prime); prime q's
-    // transform waits only for its own tile, later primes' loads overlap it
-    for (int q = 0; q < P; ++q) {
-        uint32_t* t = sm + q * stride;
-        if (sharded) {
-            const uint32_t* g = A.g + (int64_t)q * (A.sh.Tl << A.sh.TB);
-            const XchgIdx xi{A.sh, blockIdx.x};
-            for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) cp_async4(t + padi(e), g + xi(e));
-        } else {
-            const uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)tile * n;
-            for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) cp_async4(t + padi(e), g + e);
-        }
-        cp_async_commit();
-    }
-    // A tile whose radix-16 rounds occupy at most half the threads (L = 256
-    // tiles of 512-thread CTAs): two primes side by side, one per half.
-    const uint32_t halfT = blockDim.x >> 1;
-    const bool dual = A.dual_ok && P >= 2 && A.lgL >= 5 && A.yl <= 12 && (n >> 4) <= halfT;
-    if (dual) {
-        const int hsel = threadIdx.x >= halfT ? 1 : 0;
-        for (int q0 = 0; q0 < P; q0 += 2) {
-            const int q = q0 + hsel;
-            cp_async_wait_dyn(P - 1 - min(q0 + 1, P - 1));
-            __syncthreads();
-            const bool act = q < P;
-            const int qq = act ? q : q0;
-            const PrimeC pc = A.pcs[qq];
-            uint32_t* t = sm + qq * stride;
-            const Span sp{act ? threadIdx.x - hsel * halfT : 0x7fffffffu, halfT};
-            const TwRows tw{A.twx + (int64_t)qq * L, A.twy + (int64_t)qq * A.twy_stride, A.lgL};
-            y_transform<true>(t, A.lgL, 0, tile_bits, tw.twy, pc.p, pc.two_p, sp);   // y low: DIF
-            x_transform<false>(t, A.lgL, tile_bits, tw.twx, pc.p, pc.two_p, sp);     // x: DIT
-        }
-    } else {
-        for (int q = 0; q < P; ++q) {
-            const PrimeC pc = A.pcs[q];
-            uint32_t* t = sm + q * stride;
-            cp_async_wait_dyn(P - 1 - q);
-            __syncthreads();
-            const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
-            if (!y_transform<true>(t, A.lgL, 0, tile_bits, tw.twy, pc.p, pc.two_p, cta_span()))   // y low: DIF
-                run_bits<true>(t, tile_bits, A.lgL, tile_bits, tw, pc.p, pc.two_p);
-            x_transform<false>(t, A.lgL, tile_bits, tw.twx, pc.p, pc.two_p, cta_span());      // x: DIT
-        }
-    }
-    // grouped ConvertOut staging: a dynamic region after the P tiles (host-sized)
-    uint32_t* co_ost = A.co_stage ? sm + P * stride : nullptr;
-#ifndef TC_CO_FUSED_BUILD
-#define TC_CO_FUSED_BUILD 0     // fused CRT in the grouped path: spills at 64 registers (P >= 5)
-#endif
-    if constexpr (!DUMP && P <= 8 && TC_CO_FUSED_BUILD) {
-        if (A.co_fused) {
-            if constexpr (P >= 2)
-                if (A.co_aw == 2) { crt_convert_grouped<P, 2, true, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }
-            if constexpr (P <= 3)
-                if (A.co_aw == 1) { crt_convert_grouped<P, 1, true, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }
-        }
-    }
-    // CRT in place
-    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
-        uint32_t r[P], x[P];
-        r[0] = canon(sm[padi(e)], cc.p[0]);
-#pragma unroll
-        for (int q = 1; q < P; ++q) r[q] = reduce_2p(sm[q * stride + padi(e)], 2 * cc.p[q]);
-        if (A.inject >= 0 && (int64_t)bitrev(pos0 + (e >> A.lgL), A.lgS) * L + (e & (L - 1)) == A.inject)
-            r[0] = r[0] ? r[0] - 1 : cc.p[0] - 1;     // fault injection (tests of the bound check)
-        const bool bad = crt_term<P>(r, cc, x);
-        const uint32_t row = bitrev(pos0 + (e >> A.lgL), A.lgS);
-        const uint32_t j = e & (L - 1);
-        if (row < A.rows_out) {
-            if (bad) atomicMin(&A.err[2], (int)min((int64_t)row * L + j, (int64_t)0x7fffffff));
-            if (DUMP) {
-#pragma unroll
-                for (int l = 0; l < P; ++l) A.out[((int64_t)row * L + j) * P + l] = x[l];
-            }
-        }
-#pragma unroll
-        for (int l = 0; l < P - 1; ++l) sm[l * stride + padi(e)] = x[l];
-        sm[(P - 1) * stride + padi(e)] = x[P - 1] ^ 0x80000000u;     // biased: c_ij + 2^(32P-1) >= 0
-    }
-    if (DUMP) return;
-    __syncthreads();
-    if constexpr (P <= 8) {
-        if constexpr (P >= 2)
-            if (A.co_aw == 2) { crt_convert_grouped<P, 2, false, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }
-        if constexpr (P <= 3)
-            if (A.co_aw == 1) { crt_convert_grouped<P, 1, false, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }
-    }
-
     // ConvertOut over the tile's rows, kW words per thread (rows padded to a
     // multiple of kW words).  Terms are stored biased (c_ij + 2^(32P-1), an
     // unsigned P-limb number) so every shifted piece is unsigned; the bias
@@ -1973,7 +1872,6 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
     // row's top word never generates or propagates (the mod 2^(32 W32) wrap),
     // so chains never cross rows.
     const int M = A.M, W32 = A.W32;
-    constexpr int kW = TC_CO_KW;
     const int Wp = (W32 + kW - 1) / kW * kW;
     const int64_t total = (int64_t)R * Wp;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -2087,6 +1985,118 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
             c = gg[k] | (pp[k] & c);
         }
     }
+}
+
+template <int P, bool DUMP, int NT>
+__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_final(FinalArgs A, const __grid_constant__ CrtConst cc) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    __shared__ int s_any;
+    const int R = 1 << A.yl;
+    const int L = 1 << A.lgL;
+    const int tile_bits = A.lgL + A.yl;
+    const uint32_t n = 1u << tile_bits;
+    const uint32_t stride = padded_words(n);
+    const bool sharded = A.sh.world > 1;
+    const uint32_t tile = sharded ? blockIdx.x + (uint32_t)A.sh.h0 : bitrev(A.x0 + blockIdx.x, A.lgT);
+    const uint32_t pos0 = tile * (uint32_t)R;
+    if (threadIdx.x == 0) s_any = 0;
+    __syncthreads();
+    for (int r = threadIdx.x; r < R; r += blockDim.x)
+        if (bitrev(pos0 + r, A.lgS) < A.rows_out) s_any = 1;
+    __syncthreads();
+    if (!s_any) return;      // every row of this tile is zero padding
+
+    // all P tiles stream in at once (one cp.async group per prime); prime q's
+    // transform waits only for its own tile, later primes' loads overlap it
+    for (int q = 0; q < P; ++q) {
+        uint32_t* t = sm + q * stride;
+        if (sharded) {
+            const uint32_t* g = A.g + (int64_t)q * (A.sh.Tl << A.sh.TB);
+            const XchgIdx xi{A.sh, blockIdx.x};
+            for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) cp_async4(t + padi(e), g + xi(e));
+        } else {
+            const uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)tile * n;
+            for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) cp_async4(t + padi(e), g + e);
+        }
+        cp_async_commit();
+    }
+    // A tile whose radix-16 rounds occupy at most half the threads (L = 256
+    // tiles of 512-thread CTAs): two primes side by side, one per half.
+    const uint32_t halfT = blockDim.x >> 1;
+    const bool dual = A.dual_ok && P >= 2 && A.lgL >= 5 && A.yl <= 12 && (n >> 4) <= halfT;
+    if (dual) {
+        const int hsel = threadIdx.x >= halfT ? 1 : 0;
+        for (int q0 = 0; q0 < P; q0 += 2) {
+            const int q = q0 + hsel;
+            cp_async_wait_dyn(P - 1 - min(q0 + 1, P - 1));
+            __syncthreads();
+            const bool act = q < P;
+            const int qq = act ? q : q0;
+            const PrimeC pc = A.pcs[qq];
+            uint32_t* t = sm + qq * stride;
+            const Span sp{act ? threadIdx.x - hsel * halfT : 0x7fffffffu, halfT};
+            const TwRows tw{A.twx + (int64_t)qq * L, A.twy + (int64_t)qq * A.twy_stride, A.lgL};
+            y_transform<true>(t, A.lgL, 0, tile_bits, tw.twy, pc.p, pc.two_p, sp);   // y low: DIF
+            x_transform<false>(t, A.lgL, tile_bits, tw.twx, pc.p, pc.two_p, sp);     // x: DIT
+        }
+    } else {
+        for (int q = 0; q < P; ++q) {
+            const PrimeC pc = A.pcs[q];
+            uint32_t* t = sm + q * stride;
+            cp_async_wait_dyn(P - 1 - q);
+            __syncthreads();
+            const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
+            if (!y_transform<true>(t, A.lgL, 0, tile_bits, tw.twy, pc.p, pc.two_p, cta_span()))   // y low: DIF
+                run_bits<true>(t, tile_bits, A.lgL, tile_bits, tw, pc.p, pc.two_p);
+            x_transform<false>(t, A.lgL, tile_bits, tw.twx, pc.p, pc.two_p, cta_span());      // x: DIT
+        }
+    }
+    // grouped ConvertOut staging: a dynamic region after the P tiles (host-sized)
+    uint32_t* co_ost = A.co_stage ? sm + P * stride : nullptr;
+#ifndef TC_CO_FUSED_BUILD
+#define TC_CO_FUSED_BUILD 0     // fused CRT in the grouped path: spills at 64 registers (P >= 5)
+#endif
+    if constexpr (!DUMP && P <= 8 && TC_CO_FUSED_BUILD) {
+        if (A.co_fused) {
+            if constexpr (P >= 2)
+                if (A.co_aw == 2) { crt_convert_grouped<P, 2, true, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }
+            if constexpr (P <= 3)
+                if (A.co_aw == 1) { crt_convert_grouped<P, 1, true, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }
+        }
+    }
+    // CRT in place
+    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
+        uint32_t r[P], x[P];
+        r[0] = canon(sm[padi(e)], cc.p[0]);
+#pragma unroll
+        for (int q = 1; q < P; ++q) r[q] = reduce_2p(sm[q * stride + padi(e)], 2 * cc.p[q]);
+        if (A.inject >= 0 && (int64_t)bitrev(pos0 + (e >> A.lgL), A.lgS) * L + (e & (L - 1)) == A.inject)
+            r[0] = r[0] ? r[0] - 1 : cc.p[0] - 1;     // fault injection (tests of the bound check)
+        const bool bad = crt_term<P>(r, cc, x);
+        const uint32_t row = bitrev(pos0 + (e >> A.lgL), A.lgS);
+        const uint32_t j = e & (L - 1);
+        if (row < A.rows_out) {
+            if (bad) atomicMin(&A.err[2], (int)min((int64_t)row * L + j, (int64_t)0x7fffffff));
+            if (DUMP) {
+#pragma unroll
+                for (int l = 0; l < P; ++l) A.out[((int64_t)row * L + j) * P + l] = x[l];
+            }
+        }
+#pragma unroll
+        for (int l = 0; l < P - 1; ++l) sm[l * stride + padi(e)] = x[l];
+        sm[(P - 1) * stride + padi(e)] = x[P - 1] ^ 0x80000000u;     // biased: c_ij + 2^(32P-1) >= 0
+    }
+    if (DUMP) return;
+    __syncthreads();
+    if constexpr (P <= 8) {
+        if constexpr (P >= 2)
+            if (A.co_aw == 2) { crt_convert_grouped<P, 2, false, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }
+        if constexpr (P <= 3)
+            if (A.co_aw == 1) { crt_convert_grouped<P, 1, false, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }
+    }
+
+    if (A.co_kw == 2) convert_out_words<P, 2>(A, sm, stride, R, L, pos0, sharded);
+    else convert_out_words<P, TC_CO_KW>(A, sm, stride, R, L, pos0, sharded);
 }
 
 // Gathered compact rows (position order, world x rows-per-rank) -> product
