@@ -44,6 +44,8 @@ extern "C" {
 
 #define TC_MAX_PRIMES 16
 #define TC_MAX_DIGIT_BITS 126   /* M > 63: two-word digits (the paper allows 1-3 words) */
+#define TC_SPLIT_COEF 1
+#define TC_SPLIT_POLY 2
 
 /*
  * One multiplication plan, produced by the host planner
@@ -54,16 +56,28 @@ extern "C" {
  * tc/ntt2d.py:128-135.
  */
 typedef struct {
-    int64_t d;        /* max(da, db)                                          */
+    int64_t d;        /* max(da, db) of the transform (the inner product when split_kind != 0) */
     int64_t N;        /* padded coefficient width, N = K*M                    */
-    int64_t K;        /* digits per coefficient, power of two, 1 <= K <= 2^14 */
+    int64_t K;        /* digits per coefficient, power of two, 1 <= K <= 2^13 */
     int64_t M;        /* digit width in bits, 2 <= M <= TC_MAX_DIGIT_BITS      */
     int64_t s_y;      /* least power of two >= 2d-1                           */
     int32_t P;        /* number of word primes, 1..TC_MAX_PRIMES              */
-    int32_t flags;    /* 0; bit 0 = fault injection for tests: the residue of product
-                         slot (row flags>>16, column 1) is corrupted before the CRT */
+    int32_t flags;    /* 0; test fault injection, row = flags>>16: bit 0 corrupts the
+                         residue of product slot (row, column 1) before the CRT (bound
+                         check); bit 1 adds 1 to every residue of slot (row, 2K-1)
+                         (the odd-combination check, TC_ERR_PARITY) */
     uint32_t p[TC_MAX_PRIMES];  /* primes p < 2^30, 2^k | p-1, 2^k >= max(s_y, 2K) */
     uint32_t g[TC_MAX_PRIMES];  /* a primitive root of each p                       */
+    /* Kronecker reduction (csrc/tc_split.cuh; params.SplitSpec), 0 = none:
+       TC_SPLIT_COEF: coefficients as split_n super-digits of split_bits bits,
+                      placed split_block = da+db-1 rows apart;
+       TC_SPLIT_POLY: the polynomials as blocks of split_block coefficients,
+                      block t weighted by 2^(t*split_bits).
+       K, M, s_y, d and the primes then describe the inner product.          */
+    int32_t split_kind;
+    int32_t split_n;
+    int64_t split_bits;   /* multiple of 64 */
+    int64_t split_block;
 } tc_plan_t;
 
 /* StageTimings (tc/multiplier.py:41-56), seconds, measured with CUDA events. */
@@ -205,6 +219,8 @@ int tc_flush_l2(void* ctx);
 /* INT-pipe roofline denominator: sustained DIF butterflies/s (Shoup, p < 2^30)
  * of a register-only chain over every SM, and of the Montgomery product. */
 int tc_int_peak(void* ctx, double* butterflies_per_s, double* montmul_per_s);
+/* Free and total device memory of the context's GPU (plan feasibility). */
+int tc_mem_info(void* ctx, int64_t* free_bytes, int64_t* total_bytes);
 
 /* Launch counter: kernels this context launched since creation. */
 int64_t tc_kernel_launches(void* ctx);

@@ -34,7 +34,7 @@ EXPORTED_SYMBOLS = (
     "tc_device_alloc", "tc_device_free", "tc_memcpy", "tc_synchronize",
     "tc_kernel_launches", "tc_set_profiling", "tc_last_profile", "tc_last_error", "tc_version",
     "tc_host_alloc", "tc_host_free", "tc_record_event", "tc_event_elapsed", "tc_flush_l2",
-    "tc_int_peak", "tc_shard_info", "tc_shard_low", "tc_shard_high", "tc_shard_final", "tc_unshard",
+    "tc_int_peak", "tc_mem_info", "tc_shard_info", "tc_shard_low", "tc_shard_high", "tc_shard_final", "tc_unshard",
 )
 
 
@@ -42,7 +42,9 @@ class TcPlan(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int64), ("N", ctypes.c_int64), ("K", ctypes.c_int64),
                 ("M", ctypes.c_int64), ("s_y", ctypes.c_int64), ("P", ctypes.c_int32),
                 ("flags", ctypes.c_int32), ("p", ctypes.c_uint32 * TC_MAX_PRIMES),
-                ("g", ctypes.c_uint32 * TC_MAX_PRIMES)]
+                ("g", ctypes.c_uint32 * TC_MAX_PRIMES),
+                ("split_kind", ctypes.c_int32), ("split_n", ctypes.c_int32),
+                ("split_bits", ctypes.c_int64), ("split_block", ctypes.c_int64)]
 
 
 class TcTimes(ctypes.Structure):
@@ -103,6 +105,7 @@ def load(path: str = LIB_PATH):
             "tc_event_elapsed": (i32, [vp, i32, i32, P(ctypes.c_float)]),
             "tc_flush_l2": (i32, [vp]),
             "tc_int_peak": (i32, [vp, P(ctypes.c_double), P(ctypes.c_double)]),
+            "tc_mem_info": (i32, [vp, P(i64), P(i64)]),
             "tc_last_error": (ctypes.c_char_p, []),
             "tc_version": (ctypes.c_char_p, []),
         }
@@ -137,6 +140,9 @@ def make_plan(gp, flags: int = 0) -> TcPlan:
     for i, s in enumerate(gp.primes):
         pl.p[i] = s.p
         pl.g[i] = s.generator
+    sp = getattr(gp, "split", None)
+    if sp is not None:
+        pl.split_kind, pl.split_n, pl.split_bits, pl.split_block = sp.kind, sp.n, sp.bits, sp.block
     return pl
 
 
@@ -162,6 +168,12 @@ class Context:
 
     def launches(self) -> int:
         return int(self.lib.tc_kernel_launches(self.handle))
+
+    def mem_info(self):
+        """(free, total) bytes of the context's device."""
+        free, total = ctypes.c_int64(), ctypes.c_int64()
+        check(self.lib.tc_mem_info(self.handle, ctypes.byref(free), ctypes.byref(total)), "tc_mem_info")
+        return free.value, total.value
 
 
 class PinnedPool:

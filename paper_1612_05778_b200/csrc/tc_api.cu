@@ -19,6 +19,7 @@
 
 #include "../../include/tc_api.h"
 #include "tc_kernels.cuh"
+#include "tc_split.cuh"
 
 using namespace tc;
 
@@ -83,6 +84,7 @@ struct Ctx {
     int device = 0;
     cudaStream_t st = nullptr;
     DevBuf in_a, in_b, grids, twx_f, twx_i, twy_f, twy_i, pcs, flags, outbuf, dbg, nbias;
+    DevBuf sp_a, sp_b, sp_out;          // Kronecker reductions: packed operands, inner product (tc_split.cuh)
     int64_t nb_key[4] = {-1, -1, -1, -1};  // (M, P, L, W32) of nbias
     std::vector<uint32_t> pcs_key; int64_t pcs_S = -1;   // primes and S of pcs
     cudaGraphExec_t gexec = nullptr;                     // captured product pipeline (run_pipeline)
@@ -273,6 +275,7 @@ struct Geometry {
     int hthreads = 512;                        // threads per k_high CTA
     int htile = 14;
     int64_t inject = -1;                       // fault injection slot (plan.flags & 1)
+    int64_t inject_par = -1;                   // parity fault injection slot (plan.flags & 2)
 };
 
 // Pass layout: k_final keeps P tiles of 2^(lgL+yl) words in shared memory
@@ -284,6 +287,7 @@ int make_geometry(const tc_plan_t* pl, Geometry& G, int world = 1) {
     // flags bit 0: corrupt one residue of product slot (row = flags >> 16, col 1) before the CRT,
     // so the CorruptedConvolutionError path of tc/multiplier.py:59-63 can be exercised
     G.inject = (pl->flags & 1) ? (int64_t)((uint32_t)pl->flags >> 16) * G.L + 1 : -1;
+    G.inject_par = (pl->flags & 2) ? (int64_t)((uint32_t)pl->flags >> 16) * G.L + G.L - 1 : -1;
     if (G.lgL + G.lgS > 31) return set_err(TC_ERR_BAD_ARG, "grid of 2^%d slots exceeds 2^31", G.lgL + G.lgS);
     const int64_t budget = 96 * 1024;
     int tb = 0;
@@ -530,6 +534,7 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
     A.sh = sh;
     A.x0 = (uint32_t)x0; A.lgT = G.lgL + G.lgS - (G.lgL + G.yl);
     A.inject = G.inject;
+    A.inject_par = G.inject_par;
     A.g = grids; A.S = G.S; A.lgL = G.lgL; A.lgS = G.lgS; A.yl = G.yl;
     A.twx = c->twx_i.as<uint2>(); A.twy = c->twy_i.as<uint2>();
     A.twy_stride = G.s_y;
@@ -736,9 +741,124 @@ int run_pipeline(Ctx* c, const tc_plan_t* pl, int a_bits, int b_bits, int64_t ro
     return TC_OK;
 }
 
+// ---- Kronecker reductions (tc_split.cuh) ----
+struct SplitDims {
+    int64_t da2, db2, rows2;   // inner operand lengths, inner product rows
+    int bits2, cw2, ocw2;      // inner declared width, words per inner input / output row
+    int nza, nzb;              // SPLIT_POLY: blocks per operand
+};
+
+int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int bitlen64(int64_t x) { int l = 0; while (l < 63 && (1ll << l) <= x) ++l; return l; }
+
+// Inner shapes of a split plan (params.split_inner_shape mirrors this).
+int split_dims(const tc_plan_t* pl, int64_t da, int64_t db, int a_bits, int b_bits, SplitDims& s) {
+    if (pl->split_bits < 64 || pl->split_bits % 64 || pl->split_n < 1 || pl->split_block < 1)
+        return set_err(TC_ERR_BAD_ARG, "bad split (n=%d bits=%lld block=%lld)", pl->split_n,
+                       (long long)pl->split_bits, (long long)pl->split_block);
+    const int64_t n_in = a_bits > b_bits ? a_bits : b_bits;
+    if (pl->split_kind == TC_SPLIT_COEF) {
+        const int64_t D = da + db - 1;
+        if (pl->split_block != D) return set_err(TC_ERR_BAD_ARG, "coef split stride %lld != da+db-1", (long long)pl->split_block);
+        if ((int64_t)pl->split_n * pl->split_bits < n_in)
+            return set_err(TC_ERR_BAD_ARG, "coef split covers %lld bits < %lld", (long long)pl->split_n * pl->split_bits, (long long)n_in);
+        s.da2 = da + (int64_t)(pl->split_n - 1) * D;
+        s.db2 = db + (int64_t)(pl->split_n - 1) * D;
+        s.bits2 = (int)pl->split_bits + 1;
+        s.nza = s.nzb = 0;
+    } else if (pl->split_kind == TC_SPLIT_POLY) {
+        const int64_t B = pl->split_block;
+        s.nza = (int)ceil_div64(da, B); s.nzb = (int)ceil_div64(db, B);
+        const int nz = s.nza > s.nzb ? s.nza : s.nzb;
+        if (nz > pl->split_n) return set_err(TC_ERR_BAD_ARG, "poly split has %d blocks > %d", nz, pl->split_n);
+        const int64_t dmin = da < db ? da : db;
+        if (pl->split_bits < bitlen64(dmin) + 2 * n_in)
+            return set_err(TC_ERR_BAD_ARG, "poly split chunks of %lld bits are too narrow", (long long)pl->split_bits);
+        s.da2 = da < B ? da : B;
+        s.db2 = db < B ? db : B;
+        const int64_t b2 = (int64_t)(pl->split_n - 1) * pl->split_bits + n_in + 1;
+        if (b2 > INT_MAX / 2) return set_err(TC_ERR_BAD_ARG, "poly split inner width too large");
+        s.bits2 = (int)b2;
+    } else {
+        return set_err(TC_ERR_BAD_ARG, "unknown split kind %d", pl->split_kind);
+    }
+    s.rows2 = s.da2 + s.db2 - 1;
+    s.cw2 = (s.bits2 + 63) / 64;
+    const int64_t d2 = s.da2 > s.db2 ? s.da2 : s.db2;
+    s.ocw2 = (int)ceil_div64(bitlen64(d2) + 2ll * s.bits2 - 2 + 1, 64);
+    return TC_OK;
+}
+
+// One split product on the staged inputs (c->a_dev, c->b_dev): pack both
+// operands, run the transform pipeline on the inner product, unpack into
+// dout (rows x out_cw words).  Everything on c->st.
+int split_execute(Ctx* c, const tc_plan_t* pl, int a_bits, int b_bits, uint64_t* dout, int64_t rows, int out_cw,
+                  bool stage_events) {
+    int rc;
+    SplitDims s;
+    const int64_t da = c->da, db = c->db;
+    if ((rc = split_dims(pl, da, db, a_bits, b_bits, s))) return rc;
+    tc_plan_t in = *pl;
+    in.split_kind = 0; in.split_n = 0; in.split_bits = 0; in.split_block = 0;
+    if ((rc = validate_plan(&in, s.da2, s.db2))) return rc;
+    CrtConst cc;
+    if ((rc = make_crt_const(&in, s.da2 < s.db2 ? s.da2 : s.db2, &cc))) return rc;
+    if ((rc = c->sp_a.ensure((size_t)s.da2 * s.cw2 * 8))) return rc;
+    if ((rc = c->sp_b.ensure((size_t)s.db2 * s.cw2 * 8))) return rc;
+    if ((rc = c->sp_out.ensure((size_t)s.rows2 * s.ocw2 * 8))) return rc;
+    const uint64_t* srcs[2] = {c->a_dev, c->b_dev};
+    const int64_t ds[2] = {da, db}, d2s[2] = {s.da2, s.db2};
+    const int cws[2] = {c->a_cw, c->b_cw}, nzs[2] = {s.nza, s.nzb};
+    uint64_t* dsts[2] = {c->sp_a.as<uint64_t>(), c->sp_b.as<uint64_t>()};
+    const unsigned gs = (unsigned)(c->sms * 8);
+    for (int o = 0; o < 2; ++o) {
+        if (pl->split_kind == TC_SPLIT_COEF) {
+            k_pack_coef<<<gs, 256, 0, c->st>>>(srcs[o], ds[o], cws[o], dsts[o], d2s[o], s.cw2, pl->split_n,
+                                               (int)(pl->split_bits / 64), pl->split_block);
+        } else {
+            ShiftAddArgs A{srcs[o], ds[o], cws[o], pl->split_block, nzs[o], (int)(pl->split_bits / 64),
+                           dsts[o], d2s[o], s.cw2};
+            k_shift_add<<<(unsigned)(d2s[o] < (int64_t)gs ? d2s[o] : gs), 256, 0, c->st>>>(A);
+        }
+        c->launches++;
+        CKL();
+    }
+    // the inner product over the packed operands
+    const uint64_t* sa = c->a_dev; const uint64_t* sb = c->b_dev;
+    const int scw_a = c->a_cw, scw_b = c->b_cw;
+    c->a_dev = c->sp_a.as<uint64_t>(); c->b_dev = c->sp_b.as<uint64_t>();
+    c->da = s.da2; c->db = s.db2; c->a_cw = s.cw2; c->b_cw = s.cw2;
+    rc = run_pipeline(c, &in, s.bits2, s.bits2, s.rows2, 2 * s.ocw2, c->sp_out.as<uint32_t>(), false, cc, stage_events);
+    c->a_dev = sa; c->b_dev = sb; c->da = da; c->db = db; c->a_cw = scw_a; c->b_cw = scw_b;
+    if (rc) return rc;
+    if (pl->split_kind == TC_SPLIT_COEF) {
+        ShiftAddArgs A{c->sp_out.as<uint64_t>(), s.rows2, s.ocw2, pl->split_block, 2 * pl->split_n - 1,
+                       (int)(pl->split_bits / 64), dout, rows, out_cw};
+        k_shift_add<<<(unsigned)(rows < (int64_t)gs ? rows : gs), 256, 0, c->st>>>(A);
+    } else {
+        k_unpack_poly<<<gs, 128, 0, c->st>>>(c->sp_out.as<uint64_t>(), s.rows2, s.ocw2, pl->split_block,
+                                             (int)(pl->split_bits / 64), dout, rows, out_cw);
+    }
+    c->launches++;
+    CKL();
+    return TC_OK;
+}
+
 int read_flags(Ctx* c, int* f) {
     CK(cudaMemcpyAsync(f, c->flags.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
+    return TC_OK;
+}
+
+// Error flags of a product, in the order the reference raises them:
+// ConvertIn (range, then digit capacity, tc/codec.py:78-98), the CRT bound
+// (tc/multiplier.py:59-63), then the odd combination (tc/multiplier.py:156-160).
+int flag_status(const int* f, int64_t* err_index) {
+    const int none = 0x7f7f7f7f;
+    if (f[1] != none) { if (err_index) *err_index = f[1]; return set_err(TC_ERR_RANGE, "coefficient %d outside the plan's range", f[1]); }
+    if (f[0] != none) { if (err_index) *err_index = f[0]; return set_err(TC_ERR_ENCODING, "coefficient %d exceeds the digit capacity", f[0]); }
+    if (f[2] != none) { if (err_index) *err_index = f[2]; return set_err(TC_ERR_BOUND, "coefficient bound exceeded at flat index %d", f[2]); }
+    if (f[3] != none) { if (err_index) *err_index = f[3]; return set_err(TC_ERR_PARITY, "odd combination (non-zero term 2K-1) at row %d", f[3]); }
     return TC_OK;
 }
 
@@ -766,11 +886,18 @@ int tc_ctx_create(int device, void** out) {
     cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device);
     cudaError_t e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
     if (e != cudaSuccess) { delete c; return set_err(TC_ERR_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e)); }
-    for (auto& ev : c->ev) cudaEventCreate(&ev);
-    for (auto& ev : c->xev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    for (auto& ev : c->fev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking);
-    cudaHostAlloc((void**)&c->hinfo, 64, cudaHostAllocDefault);
+    bool ok = true;
+    for (auto& ev : c->ev) ok = ok && cudaEventCreate(&ev) == cudaSuccess;
+    for (auto& ev : c->xev) ok = ok && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
+    for (auto& ev : c->fev) ok = ok && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) == cudaSuccess;
+    ok = ok && cudaHostAlloc((void**)&c->hinfo, 64, cudaHostAllocDefault) == cudaSuccess;
+    if (!ok) {
+        const cudaError_t e2 = cudaGetLastError();
+        tc_ctx_destroy(c);
+        return set_err(TC_ERR_CUDA, "context setup (events / aux stream / pinned flags) failed: %s",
+                       cudaGetErrorString(e2));
+    }
     *out = c;
     return TC_OK;
 }
@@ -781,7 +908,7 @@ int tc_ctx_destroy(void* ctx) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->st);
     for (DevBuf* b : {&c->in_a, &c->in_b, &c->grids, &c->twx_f, &c->twx_i, &c->twy_f, &c->twy_i,
-                      &c->pcs, &c->flags, &c->outbuf, &c->dbg, &c->nbias}) b->release();
+                      &c->pcs, &c->flags, &c->outbuf, &c->dbg, &c->nbias, &c->sp_a, &c->sp_b, &c->sp_out}) b->release();
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (auto& ev : c->ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : c->user_ev) if (ev) cudaEventDestroy(ev);
@@ -838,12 +965,14 @@ int tc_execute(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32_t b_bits,
     if (err_index) *err_index = -1;
     CK(cudaSetDevice(c->device));
     int rc;
-    if ((rc = validate_plan(plan, c->da, c->db))) return rc;
+    if (!plan) return set_err(TC_ERR_BAD_ARG, "plan is NULL");
+    const bool split = plan->split_kind != 0;
+    if (!split && (rc = validate_plan(plan, c->da, c->db))) return rc;
     if (rows != c->da + c->db - 1) return set_err(TC_ERR_BAD_ARG, "rows must be da+db-1");
     if (out_cw < 1 || !out) return set_err(TC_ERR_BAD_ARG, "bad output buffer");
     CrtConst cc;
     const int64_t dmin = c->da < c->db ? c->da : c->db;
-    if ((rc = make_crt_const(plan, dmin, &cc))) return rc;
+    if (!split && (rc = make_crt_const(plan, dmin, &cc))) return rc;
     uint32_t* dout;
     if (out_on_device) {
         dout = reinterpret_cast<uint32_t*>(out);
@@ -852,7 +981,9 @@ int tc_execute(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32_t b_bits,
         dout = c->outbuf.as<uint32_t>();
     }
     const bool stage_events = times != nullptr || c->profiling;
-    if ((rc = run_pipeline(c, plan, a_bits, b_bits, rows, 2 * out_cw, dout, false, cc, stage_events))) return rc;
+    rc = split ? split_execute(c, plan, a_bits, b_bits, reinterpret_cast<uint64_t*>(dout), rows, out_cw, stage_events)
+               : run_pipeline(c, plan, a_bits, b_bits, rows, 2 * out_cw, dout, false, cc, stage_events);
+    if (rc) { cudaStreamSynchronize(c->st); return rc; }
     if (!out_on_device)
         CK(cudaMemcpyAsync(out, dout, (size_t)rows * out_cw * 8, cudaMemcpyDeviceToHost, c->st));
     if (stage_events) CK(cudaEventRecord(c->ev[6], c->st));
@@ -874,10 +1005,7 @@ int tc_execute(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32_t b_bits,
         times->total = now_s() - t_begin;
         times->gpus = 1;
     }
-    if (f[1] != 0x7f7f7f7f) { if (err_index) *err_index = f[1]; return set_err(TC_ERR_RANGE, "coefficient outside the plan's %lld-bit range", (long long)plan->N); }
-    if (f[0] != 0x7f7f7f7f) { if (err_index) *err_index = f[0]; return set_err(TC_ERR_ENCODING, "coefficient %d exceeds the digit capacity", f[0]); }
-    if (f[2] != 0x7f7f7f7f) { if (err_index) *err_index = f[2]; return set_err(TC_ERR_BOUND, "coefficient bound exceeded at flat index %d", f[2]); }
-    return TC_OK;
+    return flag_status(f, err_index);
 }
 
 int tc_multiply(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int32_t a_bits,
@@ -893,16 +1021,110 @@ int tc_multiply(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int32_t 
     return rc;
 }
 
+namespace {
+
+// out_bits / out_cw of the product from the device width scans (wf -> hinfo),
+// tc/zpoly.py:103-114; TC_ERR_EMPTY for a zero operand (tc/params.py:288-289).
+int product_shape(Ctx* c, int64_t d, int64_t rows, int64_t cap_words, tc_product_info_t* pinfo, int& out_cw) {
+    const int n_in = c->hinfo[0] > c->hinfo[2] ? c->hinfo[0] : c->hinfo[2];
+    int bl = 0; while ((1ll << bl) <= d) ++bl;                       // bit length of d
+    const int out_bits = bl + (2 * n_in - 2 > 0 ? 2 * n_in - 2 : 0) + 1;
+    out_cw = (out_bits + 63) / 64;
+    if (pinfo) { pinfo->n_in = n_in; pinfo->out_bits = out_bits; pinfo->out_cw = out_cw;
+                 pinfo->nonzero = (c->hinfo[1] && c->hinfo[3]) ? 1 : 0; }
+    if (!(c->hinfo[1] && c->hinfo[3])) return set_err(TC_ERR_EMPTY, "empty input: zero polynomial");
+    if (rows * out_cw > cap_words)
+        return set_err(TC_ERR_BAD_ARG, "output capacity %lld words < %lld", (long long)cap_words, (long long)(rows * out_cw));
+    return TC_OK;
+}
+
+// A Kronecker-split product from host buffers: uploads, width scans, the
+// split pipeline (tc_split.cuh) and the product download, on one stream.
+int multiply_host_split(Ctx* c, const uint64_t* a, int64_t da, int32_t a_cw, int32_t a_bits,
+                        const uint64_t* b, int64_t db, int32_t b_cw, int32_t b_bits,
+                        const tc_plan_t* plan, uint64_t* out, int64_t cap_words,
+                        tc_product_info_t* pinfo, tc_times_t* times, int64_t* err_index, double t_begin) {
+    int rc;
+    const int64_t rows = da + db - 1;
+    if ((rc = c->in_a.ensure((size_t)da * a_cw * 8))) return rc;
+    if ((rc = c->in_b.ensure((size_t)db * b_cw * 8))) return rc;
+    if ((rc = c->dbg.ensure(64))) return rc;
+    c->a_dev = c->in_a.as<uint64_t>(); c->b_dev = c->in_b.as<uint64_t>();
+    c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true;
+    int* wf = c->dbg.as<int>();
+    CK(cudaEventRecord(c->ev[0], c->st));
+    CK(cudaMemsetAsync(wf, 0, 16, c->st));
+    CK(cudaMemcpyAsync(c->in_a.p, a, (size_t)da * a_cw * 8, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->in_b.p, b, (size_t)db * b_cw * 8, cudaMemcpyHostToDevice, c->st));
+    k_width<<<(unsigned)((da + 255) / 256), 256, 0, c->st>>>(c->a_dev, da, a_cw, wf);
+    k_width<<<(unsigned)((db + 255) / 256), 256, 0, c->st>>>(c->b_dev, db, b_cw, wf + 2);
+    c->launches += 2;
+    CKL();
+    CK(cudaMemcpyAsync(c->hinfo, wf, 16, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    int out_cw;
+    if ((rc = product_shape(c, da > db ? da : db, rows, cap_words, pinfo, out_cw))) return rc;
+    if ((rc = c->outbuf.ensure((size_t)rows * out_cw * 8))) return rc;
+    CK(cudaEventRecord(c->ev[1], c->st));
+    if ((rc = split_execute(c, plan, a_bits, b_bits, c->outbuf.as<uint64_t>(), rows, out_cw, false))) return rc;
+    CK(cudaEventRecord(c->ev[5], c->st));
+    CK(cudaMemcpyAsync(out, c->outbuf.p, (size_t)rows * out_cw * 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaEventRecord(c->ev[6], c->st));
+    int f[4];
+    if ((rc = read_flags(c, f))) return rc;
+    if (times) {
+        float up = 0, mid = 0, down = 0;
+        cudaEventElapsedTime(&up, c->ev[0], c->ev[1]);
+        cudaEventElapsedTime(&mid, c->ev[1], c->ev[5]);
+        cudaEventElapsedTime(&down, c->ev[5], c->ev[6]);
+        (void)cudaGetLastError();
+        memset(times, 0, sizeof *times);
+        times->convert = up * 1e-3;
+        times->ntt_forward = mid * 1e-3;
+        times->recover = down * 1e-3;
+        times->total = now_s() - t_begin;
+        times->gpus = 1;
+    }
+    return flag_status(f, err_index);
+}
+
+int multiply_host_impl(Ctx* c, const uint64_t* a, int64_t da, int32_t a_cw, int32_t a_bits,
+                       const uint64_t* b, int64_t db, int32_t b_cw, int32_t b_bits,
+                       const tc_plan_t* plan, uint64_t* out, int64_t out_capacity_words,
+                       tc_product_info_t* pinfo, tc_times_t* times, int64_t* err_index, double t_begin);
+
+}  // namespace
+
 int tc_multiply_host(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int32_t a_bits,
                      const uint64_t* b, int64_t db, int32_t b_cw, int32_t b_bits,
                      const tc_plan_t* plan, uint64_t* out, int64_t out_capacity_words,
                      tc_product_info_t* pinfo, tc_times_t* times, int64_t* err_index) {
     Ctx* c = static_cast<Ctx*>(ctx);
     const double t_begin = now_s();
-    if (!c || !a || !b || !out || da < 1 || db < 1 || a_cw < 1 || b_cw < 1)
+    if (!c || !a || !b || !out || !plan || da < 1 || db < 1 || a_cw < 1 || b_cw < 1)
         return set_err(TC_ERR_BAD_ARG, "bad operand arguments");
     if (err_index) *err_index = -1;
     CK(cudaSetDevice(c->device));
+    const int rc = plan->split_kind
+        ? multiply_host_split(c, a, da, a_cw, a_bits, b, db, b_cw, b_bits, plan, out, out_capacity_words,
+                              pinfo, times, err_index, t_begin)
+        : multiply_host_impl(c, a, da, a_cw, a_bits, b, db, b_cw, b_bits, plan, out, out_capacity_words,
+                             pinfo, times, err_index, t_begin);
+    if (rc) {
+        // queued copies read the caller's inputs and write its output buffer:
+        // none may outlive the call
+        cudaStreamSynchronize(c->st);
+        cudaStreamSynchronize(c->aux);
+    }
+    return rc;
+}
+
+namespace {
+
+int multiply_host_impl(Ctx* c, const uint64_t* a, int64_t da, int32_t a_cw, int32_t a_bits,
+                       const uint64_t* b, int64_t db, int32_t b_cw, int32_t b_bits,
+                       const tc_plan_t* plan, uint64_t* out, int64_t out_capacity_words,
+                       tc_product_info_t* pinfo, tc_times_t* times, int64_t* err_index, double t_begin) {
     int rc;
     if ((rc = validate_plan(plan, da, db))) return rc;
     const int64_t rows = da + db - 1;
@@ -924,11 +1146,7 @@ int tc_multiply_host(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int
     CK(cudaMemcpyAsync(c->in_b.p, b, (size_t)db * b_cw * 8, cudaMemcpyHostToDevice, c->aux));
     CK(cudaEventRecord(c->xev[20], c->aux));
     Geometry G;
-    if ((rc = prepare(c, plan, G, true)) || (rc = c->grids.ensure((size_t)2 * G.P * G.S * 4))) {
-        cudaStreamSynchronize(c->st);        // the uploads read the caller's buffers: finish them first
-        cudaStreamSynchronize(c->aux);
-        return rc;
-    }
+    if ((rc = prepare(c, plan, G, true)) || (rc = c->grids.ensure((size_t)2 * G.P * G.S * 4))) return rc;
     uint32_t* GA = c->grids.as<uint32_t>();
     uint32_t* GB = GA + (size_t)G.P * G.S;
     const ShardArgs one = single_gpu();
@@ -964,22 +1182,8 @@ int tc_multiply_host(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int
     CK(cudaEventRecord(c->ev[4], c->st));
     // the true widths (back long ago) fix the product's row length: only k_final needs them
     CK(cudaEventSynchronize(c->xev[1]));
-    const int n_in = c->hinfo[0] > c->hinfo[2] ? c->hinfo[0] : c->hinfo[2];
-    const int64_t d = da > db ? da : db;
-    int bl = 0; while ((1ll << bl) <= d) ++bl;                       // bit length of d
-    const int out_bits = bl + (2 * n_in - 2 > 0 ? 2 * n_in - 2 : 0) + 1;   // tc/zpoly.py:103-114
-    const int out_cw = (out_bits + 63) / 64;
-    if (pinfo) { pinfo->n_in = n_in; pinfo->out_bits = out_bits; pinfo->out_cw = out_cw;
-                 pinfo->nonzero = (c->hinfo[1] && c->hinfo[3]) ? 1 : 0; }
-    if (!(c->hinfo[1] && c->hinfo[3])) {
-        CK(cudaStreamSynchronize(c->st));
-        return set_err(TC_ERR_EMPTY, "empty input: zero polynomial");
-    }
-    if ((int64_t)rows * out_cw > out_capacity_words) {
-        CK(cudaStreamSynchronize(c->st));
-        return set_err(TC_ERR_BAD_ARG, "output capacity %lld words < %lld", (long long)out_capacity_words,
-                       (long long)rows * out_cw);
-    }
+    int out_cw;
+    if ((rc = product_shape(c, da > db ? da : db, rows, out_capacity_words, pinfo, out_cw))) return rc;
     // k_final in chunks; chunk j's rows (k*T + x, x in the chunk) go to the host while later chunks run
     const int W32 = 2 * out_cw;
     if ((rc = c->outbuf.ensure((size_t)rows * out_cw * 8))) return rc;
@@ -1027,11 +1231,10 @@ int tc_multiply_host(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int
         times->total = now_s() - t_begin;
         times->gpus = 1;
     }
-    if (f[1] != 0x7f7f7f7f) { if (err_index) *err_index = f[1]; return set_err(TC_ERR_RANGE, "coefficient outside the plan's %lld-bit range", (long long)plan->N); }
-    if (f[0] != 0x7f7f7f7f) { if (err_index) *err_index = f[0]; return set_err(TC_ERR_ENCODING, "coefficient %d exceeds the digit capacity", f[0]); }
-    if (f[2] != 0x7f7f7f7f) { if (err_index) *err_index = f[2]; return set_err(TC_ERR_BOUND, "coefficient bound exceeded at flat index %d", f[2]); }
-    return TC_OK;
+    return flag_status(f, err_index);
 }
+
+}  // namespace
 
 int tc_digits(void* ctx, int32_t which, int64_t K, int64_t M, int64_t N, int32_t in_bits,
               int64_t* digits_out, int64_t* err_index) {
@@ -1061,9 +1264,7 @@ int tc_digits(void* ctx, int32_t which, int64_t K, int64_t M, int64_t N, int32_t
     CK(cudaMemcpyAsync(digits_out, dd, (size_t)d * K * 8, cudaMemcpyDeviceToHost, c->st));
     int f[4];
     if ((rc = read_flags(c, f))) return rc;
-    if (f[1] != 0x7f7f7f7f) { if (err_index) *err_index = f[1]; return set_err(TC_ERR_RANGE, "coefficient outside the plan's %lld-bit range", (long long)N); }
-    if (f[0] != 0x7f7f7f7f) { if (err_index) *err_index = f[0]; return set_err(TC_ERR_ENCODING, "coefficient %d exceeds the digit capacity", f[0]); }
-    return TC_OK;
+    return flag_status(f, err_index);
 }
 
 int tc_bivariate_product(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32_t b_bits,
@@ -1084,10 +1285,7 @@ int tc_bivariate_product(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32
     CK(cudaMemcpyAsync(coeffs_out, c->outbuf.p, bytes, cudaMemcpyDeviceToHost, c->st));
     int f[4];
     if ((rc = read_flags(c, f))) return rc;
-    if (f[1] != 0x7f7f7f7f) { if (err_index) *err_index = f[1]; return set_err(TC_ERR_RANGE, "coefficient outside the plan's range"); }
-    if (f[0] != 0x7f7f7f7f) { if (err_index) *err_index = f[0]; return set_err(TC_ERR_ENCODING, "coefficient %d exceeds the digit capacity", f[0]); }
-    if (f[2] != 0x7f7f7f7f) { if (err_index) *err_index = f[2]; return set_err(TC_ERR_BOUND, "coefficient bound exceeded at flat index %d", f[2]); }
-    return TC_OK;
+    return flag_status(f, err_index);
 }
 
 int tc_shard_info(const tc_plan_t* plan, int32_t world, tc_shard_info_t* info) {
@@ -1162,10 +1360,7 @@ int tc_shard_final(void* ctx, const tc_plan_t* plan, int32_t rank, int32_t world
     if ((rc = launch_final(c, G, recvB, rows, (int)plan->M, 2 * out_cw, out_rows, cc, false, sh))) return rc;
     int f[4];
     if ((rc = read_flags(c, f))) return rc;
-    if (f[1] != 0x7f7f7f7f) { if (err_index) *err_index = f[1]; return set_err(TC_ERR_RANGE, "coefficient outside the plan's range"); }
-    if (f[0] != 0x7f7f7f7f) { if (err_index) *err_index = f[0]; return set_err(TC_ERR_ENCODING, "coefficient %d exceeds the digit capacity", f[0]); }
-    if (f[2] != 0x7f7f7f7f) { if (err_index) *err_index = f[2]; return set_err(TC_ERR_BOUND, "coefficient bound exceeded at flat index %d", f[2]); }
-    return TC_OK;
+    return flag_status(f, err_index);
 }
 
 int tc_unshard(void* ctx, const tc_plan_t* plan, const uint32_t* gathered, int64_t rows, int32_t out_cw, uint64_t* out) {
@@ -1322,6 +1517,16 @@ int tc_int_peak(void* ctx, double* bfly_per_s, double* mont_per_s) {
         if (mode == 1 && mont_per_s) *mont_per_s = ops / (ms * 1e-3);
     }
     cudaEventDestroy(e0); cudaEventDestroy(e1);
+    return TC_OK;
+}
+
+int tc_mem_info(void* ctx, int64_t* free_bytes, int64_t* total_bytes) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || !free_bytes || !total_bytes) return set_err(TC_ERR_BAD_ARG, "NULL argument");
+    CK(cudaSetDevice(c->device));
+    size_t f = 0, t = 0;
+    CK(cudaMemGetInfo(&f, &t));
+    *free_bytes = (int64_t)f; *total_bytes = (int64_t)t;
     return TC_OK;
 }
 

@@ -1604,6 +1604,7 @@ struct FinalArgs {
     // (rows k*T + x): the host copies it while later chunks compute.
     uint32_t x0; int lgT;
     int64_t inject;                // >= 0: corrupt the residue of flat slot row*L + j (plan.flags)
+    int64_t inject_par;            // >= 0: add 1 to every residue of flat slot row*L + L-1 (plan.flags bit 1)
     int co_aw;                     // > 0: grouped ConvertOut with M = 32 co_aw + {0, 1} (host-checked)
     int co_fused;                  // grouped ConvertOut lifts the residues itself (no in-place CRT pass)
     int dual_ok;                   // allow two primes' transforms side by side (small tiles)
@@ -2070,13 +2071,26 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
         r[0] = canon(sm[padi(e)], cc.p[0]);
 #pragma unroll
         for (int q = 1; q < P; ++q) r[q] = reduce_2p(sm[q * stride + padi(e)], 2 * cc.p[q]);
-        if (A.inject >= 0 && (int64_t)bitrev(pos0 + (e >> A.lgL), A.lgS) * L + (e & (L - 1)) == A.inject)
-            r[0] = r[0] ? r[0] - 1 : cc.p[0] - 1;     // fault injection (tests of the bound check)
-        const bool bad = crt_term<P>(r, cc, x);
         const uint32_t row = bitrev(pos0 + (e >> A.lgL), A.lgS);
         const uint32_t j = e & (L - 1);
+        if (A.inject >= 0 && (int64_t)row * L + j == A.inject)
+            r[0] = r[0] ? r[0] - 1 : cc.p[0] - 1;     // fault injection (tests of the bound check)
+        if (A.inject_par >= 0 && (int64_t)row * L + j == A.inject_par) {
+#pragma unroll
+            for (int q = 0; q < P; ++q) r[q] = (r[q] + 1) % cc.p[q];   // c_(i,2K-1) = 1 (parity test)
+        }
+        const bool bad = crt_term<P>(r, cc, x);
         if (row < A.rows_out) {
             if (bad) atomicMin(&A.err[2], (int)min((int64_t)row * L + j, (int64_t)0x7fffffff));
+            // the acyclic product of two K-digit rows has no term 2K-1: a
+            // non-zero one is the odd combination of tc/_kernels.py:416-417
+            // (u + v odd, tc/multiplier.py:156-160) in this formulation
+            if (j == (uint32_t)(L - 1) && !bad) {
+                uint32_t nz = 0;
+#pragma unroll
+                for (int l = 0; l < P; ++l) nz |= x[l];
+                if (nz) atomicMin(&A.err[3], (int)row);
+            }
             if (DUMP) {
 #pragma unroll
                 for (int l = 0; l < P; ++l) A.out[((int64_t)row * L + j) * P + l] = x[l];

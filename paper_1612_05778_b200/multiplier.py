@@ -25,9 +25,10 @@ from time import perf_counter
 import numpy as np
 
 from . import _lib
-from .errors import (CorruptedConvolutionError, EmptyInputError, EncodingError,
+from .errors import (CorruptedConvolutionError, DeviceError, EmptyInputError, EncodingError,
                      TransformLengthError)
-from .params import GpuPlan, _finish_plan, _choose_split, extreme_coefficients, plan_gpu, s_y_for
+from .params import (GpuPlan, _finish_plan, _choose_split, extreme_coefficients, plan_device_bytes,
+                     plan_gpu, plan_with_split, s_y_for)
 from .zpoly import IntPolynomial, output_bit_width, twos_complement_width
 
 WORD_BITS = 64
@@ -122,7 +123,15 @@ def _run_pipeline(req: MulRequest, plan_override: dict | None = None, device: in
     _check_reference_planning(req, d)
     n_decl = max(a.bit_width, b.bit_width)
     po = plan_override or {}
-    plan = plan_gpu(d, min(da, db), max(n_decl, po.get("n_min", 1)), K=po.get("K"), M=po.get("M"))
+    if po.get("split") is not None:
+        plan = plan_with_split(d, min(da, db), n_decl, po["split"])
+    else:
+        plan = plan_gpu(d, min(da, db), max(n_decl, po.get("n_min", 1)), K=po.get("K"), M=po.get("M"))
+    need = plan_device_bytes(plan, da, db)
+    free, total = ctx.mem_info()
+    if need > total:
+        raise DeviceError(f"the product needs {need / 2**30:.1f} GiB of device memory; "
+                          f"the device has {total / 2**30:.1f} GiB ({plan.describe()})")
     cap_cw = -(-output_bit_width(d, n_decl) // WORD_BITS)
     buf = _lib.pinned.empty((rows * cap_cw,), np.uint64)     # pinned: DMA at full PCIe rate
     info = _lib.TcProductInfo()
@@ -163,7 +172,8 @@ def multiply_with_stats(req: MulRequest) -> tuple:
     return result, stats
 
 
-def multiply_with_plan(req: MulRequest, K: int | None = None, M: int | None = None):
-    """multiply under an explicit digit split (experiments / parity tests);
-    returns (product, stats, GpuPlan)."""
-    return _run_pipeline(req, plan_override={"K": K, "M": M})
+def multiply_with_plan(req: MulRequest, K: int | None = None, M: int | None = None, split=None):
+    """multiply under an explicit digit split or Kronecker reduction
+    (params.SplitSpec; experiments / parity tests); returns (product, stats,
+    GpuPlan)."""
+    return _run_pipeline(req, plan_override={"K": K, "M": M, "split": split})

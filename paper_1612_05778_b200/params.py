@@ -137,19 +137,18 @@ def is_primitive_root(g: int, spec: PrimeSpec) -> bool:   # tc/params.py:123-127
 
 @lru_cache(maxsize=1)
 def gpu_prime_table() -> tuple:
-    """Primes p = q*2^k + 1 (q odd) in (2^29, 2^30) with k >= 20, each with its
-    smallest primitive root, by descending p.  p < 2^30 keeps the lazy
-    butterflies' [0, 4p) range inside 32 bits."""
+    """Primes p = q*2^k + 1 (q odd, k >= 20) below 2^30, each with its smallest
+    primitive root, by descending p.  p < 2^30 keeps the lazy butterflies'
+    [0, 4p) range inside 32 bits.  Most are in (2^29, 2^30); the few with a
+    larger 2-adic valuation (k = 23..26: 998244353, 754974721, 469762049,
+    167772161, ...) sit lower and set how long a y transform can get
+    (2^26 slots)."""
     out = []
-    for c in range((1 << 30) >> 20, ((1 << 29) >> 20), -1):
-        p = (c << 20) + 1
-        if p >= (1 << 30) or p <= (1 << 29) or not is_prime_u64(p):
-            continue
-        q, k = p - 1, 0
-        while q % 2 == 0:
-            q //= 2
-            k += 1
-        out.append(PrimeSpec(p, q, k, _smallest_primitive_root(p, q)))
+    for k in range(20, 30):
+        for q in range(1, (1 << 30) >> k, 2):
+            p = (q << k) + 1
+            if p < (1 << 30) and is_prime_u64(p):
+                out.append(PrimeSpec(p, q, k, _smallest_primitive_root(p, q)))
     return tuple(sorted(out, key=lambda s: s.p, reverse=True))
 
 
@@ -175,19 +174,54 @@ def s_y_for(d: int) -> int:                             # tc/params.py:164-168
 
 
 def min_digit_bits(K: int, n_in: int) -> int:
-    """Smallest M >= 2 whose balanced capacity covers every n_in-bit value."""
-    lo, hi = -(1 << (n_in - 1)), (1 << (n_in - 1)) - 1 if n_in > 1 else 0
-    M = max(2, _ceil_div(n_in, K))
-    while True:
-        cl, ch = balanced_capacity(K, M)
-        if cl <= lo and hi <= ch:
-            return M
-        M += 1
+    """Smallest M >= 2 whose balanced capacity (balanced_capacity) covers
+    every n_in-bit value.  Closed form: with U = (2^(MK) - 1)/(2^M - 1) the
+    low end -2^(M-1) U reaches -2^(n-1) iff MK >= n, and the high end
+    (2^(M-1) - 1) U reaches 2^(n-1) - 1 iff K = 1 or MK >= n + 1
+    (tests/test_host.py checks it against the big-integer capacities)."""
+    if K == 1:
+        return max(2, n_in)
+    return max(2, _ceil_div(n_in + 1, K))
+
+
+def product_width_bits(d: int, n_in: int) -> int:
+    """bit_length(d << (2 n_in - 2)) + 1 without building the integer (tc/zpoly.py:103-114)."""
+    return d.bit_length() + max(2 * n_in - 2, 0) + 1
+
+
+SPLIT_NONE, SPLIT_COEF, SPLIT_POLY = 0, 1, 2
+MAX_GRID_BITS = 31                   # 32-bit slot indexing inside one prime's grid
+FINAL_SMEM_LIMIT = 220 * 1024        # k_final's P resident tiles (make_geometry, csrc/tc_api.cu)
+
+
+@dataclass(frozen=True)
+class SplitSpec:
+    """A Kronecker reduction that maps a product the 2-D transform cannot hold
+    onto one it can (csrc/tc_split.cuh packs and unpacks on the device).
+
+    SPLIT_COEF (coefficients wider than K <= 2^13 digits of <= 126 bits hold):
+      every coefficient becomes `n` super-digits of `bits` bits (unsigned, the
+      top one signed) placed `block` = da+db-1 rows apart, so the inner product
+      c~ has c~[i + s*block] = sum_{t+u=s} a_t b_u at row i and
+      c_i = sum_s c~[i + s*block] * 2^(s*bits).
+    SPLIT_POLY (degree beyond the y-transform lengths of the prime table):
+      the polynomial becomes blocks of `block` = B coefficients, block t
+      weighted by 2^(t*bits) (Kronecker substitution y^B -> 2^bits), so the
+      inner product has degree < 2B and c_{sB+i} = C(s, i) + C(s-1, i+B) with
+      C(s, i) the balanced `bits`-bit chunk s of c~_i."""
+
+    kind: int
+    n: int         # super-digits per coefficient (COEF) / blocks of the longer operand (POLY)
+    bits: int      # chunk width, a multiple of 64
+    block: int     # row stride D = da+db-1 (COEF) / coefficients per block B (POLY)
 
 
 @dataclass(frozen=True)
 class GpuPlan:
-    """The plan tc_execute runs (tc_plan_t, include/tc_api.h)."""
+    """The plan tc_execute runs (tc_plan_t, include/tc_api.h).  d, dmin, n_in,
+    K, M, s_y and the primes describe the transform actually executed; with a
+    `split` that is the inner product of the Kronecker reduction and `outer`
+    holds the caller's (d, dmin, n_in)."""
 
     d: int              # max(da, db)
     dmin: int           # min(da, db): the bound uses it
@@ -197,6 +231,8 @@ class GpuPlan:
     M: int
     s_y: int
     primes: tuple       # PrimeSpec, p < 2^30
+    split: SplitSpec | None = None
+    outer: tuple | None = None
 
     @property
     def L(self) -> int:
@@ -219,8 +255,13 @@ class GpuPlan:
         return self.dmin * self.K << (2 * self.M - 2)
 
     def describe(self) -> str:
-        return (f"K={self.K} M={self.M} N={self.N} s_y={self.s_y} L={self.L} "
-                f"P={self.P} primes={[s.p for s in self.primes]}")
+        s = (f"K={self.K} M={self.M} N={self.N} s_y={self.s_y} L={self.L} "
+             f"P={self.P} primes={[s.p for s in self.primes]}")
+        if self.split:
+            kind = "coef" if self.split.kind == SPLIT_COEF else "poly"
+            s += (f" split={kind}(n={self.split.n}, bits={self.split.bits}, block={self.split.block}; "
+                  f"outer d={self.outer[0]} n_in={self.outer[2]})")
+        return s
 
 
 def _primes_for_bound(bound2: int, need_len: int):
@@ -299,38 +340,143 @@ def plan_cost(d: int, dmin: int, K: int, M: int, P: int, out_words: int) -> floa
     return bfly / 2.5e12 + mem / 5.5e12 + crt / 3.0e13 + out / 3.0e13
 
 
-@lru_cache(maxsize=256)
-def plan_gpu(d: int, dmin: int, n_in: int, K: int | None = None, M: int | None = None) -> GpuPlan:
-    """Choose (K, M, primes) for d coefficients of width <= n_in."""
-    if d < 1 or dmin < 1 or n_in < 1:
-        raise ValueError("d, dmin and n_in must be positive")
+def final_tile_bytes(K: int, s_y: int, P: int) -> int:
+    """Shared memory of k_final's P resident tiles for this shape."""
+    lgL, lgS = (2 * K).bit_length() - 1, s_y.bit_length() - 1
+    yl, _ = pass_layout(lgL, lgS, P)
+    n = 1 << (lgL + yl)
+    return 4 * P * (n + (n >> 5) + 1)
+
+
+def _plan_direct(d: int, dmin: int, n_in: int, K: int | None, M: int | None):
+    """(cost, GpuPlan) of the cheapest one-transform plan, or None.
+
+    Feasible = K <= 2^13, M <= 126, a prime set of <= 16 primes with
+    2^k >= max(s_y, 2K) whose product exceeds twice the bound, at most 2^31
+    slots per prime, and k_final's P tiles within shared memory."""
     s_y = s_y_for(d)
-    out_words = _ceil_div((d << max(2 * n_in - 2, 0)).bit_length() + 1, WORD_BITS)
+    out_words = _ceil_div(product_width_bits(d, n_in), WORD_BITS)
     cands = [K] if K else [1 << k for k in range(0, 14)]
     best = None
-    for k in cands:
-        m = M if M else min_digit_bits(k, n_in)
-        if K is None and (m > MAX_GPU_DIGIT_BITS or k > MAX_K):
+    # two-word digits trade primes for per-slot CRT / ConvertIn work; they
+    # pay on grids of >= 2^20 slots per prime (B200: C2 -8 %, C3 -6 %,
+    # C4 -9 %, C5 -5 %) but not on latency-bound small ones (C1 +8 %) --
+    # unless no single-word plan exists at all
+    for prefer in (True, False):
+        for k in cands:
+            m = M if M else min_digit_bits(k, n_in)
+            if K is None and (m > MAX_GPU_DIGIT_BITS or k > MAX_K):
+                continue
+            if prefer and K is None and M is None and m > MAX_DIGIT_BITS and s_y * 2 * k < (1 << 20):
+                continue
+            if m > MAX_GPU_DIGIT_BITS or m < 2 or k > MAX_K:
+                raise ValueError(f"unsupported digit split K={k} M={m}")
+            if (s_y * 2 * k).bit_length() - 1 > MAX_GRID_BITS:
+                continue
+            primes = _primes_for_bound(2 * (dmin * k << (2 * m - 2)), max(s_y, 2 * k))
+            if primes is None:
+                continue
+            if final_tile_bytes(k, s_y, len(primes)) > FINAL_SMEM_LIMIT:
+                continue
+            cost = plan_cost(d, dmin, k, m, len(primes), out_words)
+            if best is None or cost < best[0]:
+                best = (cost, GpuPlan(d=d, dmin=dmin, n_in=n_in, N=k * m, K=k, M=m, s_y=s_y, primes=primes))
+        if best is not None:
+            break
+    return best
+
+
+def split_inner_shape(split: SplitSpec, d: int, dmin: int, n_in: int):
+    """(d', dmin', n_in') of the inner product of a Kronecker reduction
+    (mirrors split_dims in csrc/tc_api.cu)."""
+    if split.kind == SPLIT_COEF:
+        D = split.block
+        return d + (split.n - 1) * D, dmin + (split.n - 1) * D, split.bits + 1
+    B = split.block
+    return min(d, B), min(dmin, B), (split.n - 1) * split.bits + n_in + 1
+
+
+def _plan_split(d: int, dmin: int, n_in: int):
+    """Cheapest Kronecker reduction onto a feasible one-transform plan."""
+    best = None
+    # wide coefficients: super-digits of 2^12 .. 2^19 bits
+    for lg in range(12, 20):
+        bits = 1 << lg
+        if bits >= n_in:
+            break
+        sp = SplitSpec(SPLIT_COEF, _ceil_div(n_in, bits), bits, d + dmin - 1)
+        d2, m2, n2 = split_inner_shape(sp, d, dmin, n_in)
+        if s_y_for(d2) > (1 << 26):
             continue
-        # two-word digits trade primes for per-slot CRT / ConvertIn work; they
-        # pay on grids of >= 2^20 slots per prime (B200: C2 -8 %, C3 -6 %,
-        # C4 -9 %, C5 -5 %) but not on latency-bound small ones (C1 +8 %)
-        if K is None and M is None and m > MAX_DIGIT_BITS and s_y * 2 * k < (1 << 20):
-            continue
-        if m > MAX_GPU_DIGIT_BITS or m < 2 or k > MAX_K:
-            raise ValueError(f"unsupported digit split K={k} M={m}")
-        primes = _primes_for_bound(2 * (dmin * k << (2 * m - 2)), max(s_y, 2 * k))
-        if primes is None:
-            if K is not None:
-                raise PrimeCapacityError(f"no prime set of <= {MAX_PRIMES} 30-bit primes covers K={k} M={m}")
-            continue
-        cost = plan_cost(d, dmin, k, m, len(primes), out_words)
-        if best is None or cost < best[0]:
-            best = (cost, k, m, primes)
+        r = _plan_direct(d2, m2, n2, None, None)
+        if r and (best is None or r[0] < best[0]):
+            best = (r[0], r[1], sp)
+    # long polynomials: blocks of B coefficients, chunks wide enough for the
+    # block products' coefficients (|C| <= dmin 2^(2 n_in - 2) < 2^(bits-1))
+    bits = WORD_BITS * _ceil_div(dmin.bit_length() + 2 * n_in, WORD_BITS)
+    for lg in range(6, 26):
+        B = 1 << lg
+        if B >= d:
+            break
+        sp = SplitSpec(SPLIT_POLY, _ceil_div(d, B), bits, B)
+        d2, m2, n2 = split_inner_shape(sp, d, dmin, n_in)
+        r = _plan_direct(d2, m2, n2, None, None)
+        if r and (best is None or r[0] < best[0]):
+            best = (r[0], r[1], sp)
     if best is None:
-        raise PrimeCapacityError(f"no feasible GPU plan for d={d} n_in={n_in}")
-    _, k, m, primes = best
-    return GpuPlan(d=d, dmin=dmin, n_in=n_in, N=k * m, K=k, M=m, s_y=s_y, primes=primes)
+        return None
+    cost, inner, sp = best
+    return cost, GpuPlan(**{**inner.__dict__, "split": sp, "outer": (d, dmin, n_in)})
+
+
+def plan_with_split(d: int, dmin: int, n_in: int, split: SplitSpec) -> GpuPlan:
+    """A plan under an explicit Kronecker reduction (tests, experiments)."""
+    if split.kind == SPLIT_COEF and split.block != d + dmin - 1:
+        raise ValueError("a coefficient split's block must be da + db - 1")
+    d2, m2, n2 = split_inner_shape(split, d, dmin, n_in)
+    r = _plan_direct(d2, m2, n2, None, None)
+    if r is None:
+        raise PrimeCapacityError(f"no inner plan for the split {split}")
+    return GpuPlan(**{**r[1].__dict__, "split": split, "outer": (d, dmin, n_in)})
+
+
+@lru_cache(maxsize=256)
+def plan_gpu(d: int, dmin: int, n_in: int, K: int | None = None, M: int | None = None) -> GpuPlan:
+    """Choose (K, M, primes) for d coefficients of width <= n_in.
+
+    When no single transform holds the product (coefficients beyond ~1 Mbit,
+    or a degree whose y transform is longer than the prime table's 2-adic
+    valuations allow), the product is reduced by Kronecker substitution onto
+    one that does (SplitSpec), so every shape the reference plans
+    (tc/params.py:225-267) gets a GPU plan, memory permitting."""
+    if d < 1 or dmin < 1 or n_in < 1:
+        raise ValueError("d, dmin and n_in must be positive")
+    r = _plan_direct(d, dmin, n_in, K, M)
+    if r is None and K is None and M is None:
+        r = _plan_split(d, dmin, n_in)
+    if r is None:
+        if K is not None:
+            raise PrimeCapacityError(f"no prime set of <= {MAX_PRIMES} 30-bit primes covers K={K} M={M}")
+        raise PrimeCapacityError(
+            f"no feasible GPU plan for d={d} n_in={n_in}: its transform grids alone would need "
+            f"~{2.5 * (d + dmin) * n_in / 1e9:.0f} GB (one B200 holds 180 GB) or 2^31+ slots per prime")
+    return r[1]
+
+
+def plan_device_bytes(plan: GpuPlan, da: int, db: int) -> int:
+    """Device memory one product of this plan holds at its peak (grids,
+    staged operands, product words, Kronecker scratch)."""
+    d, dmin, n_in = plan.outer if plan.split else (plan.d, plan.dmin, plan.n_in)
+    rows = da + db - 1
+    out_cw = _ceil_div(product_width_bits(d, n_in), WORD_BITS)
+    cw = _ceil_div(n_in, WORD_BITS)
+    total = 2 * plan.P * plan.S * 4 + (da + db) * cw * 8 + rows * out_cw * 8
+    if plan.split:
+        d2, m2, n2 = split_inner_shape(plan.split, d, dmin, n_in)
+        cw2 = _ceil_div(n2, WORD_BITS)
+        ocw2 = _ceil_div(product_width_bits(d2, n2), WORD_BITS)
+        total += (d2 + m2) * cw2 * 8 + (d2 + m2 - 1) * ocw2 * 8
+    return total
 
 
 # ---------------------------------------------------------------------------

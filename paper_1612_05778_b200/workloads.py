@@ -101,4 +101,4 @@ def words_sha256(words: np.ndarray) -> str:
 
 def output_bits(d: int, n_in: int) -> int:
     """product_bit_width (tc/zpoly.py:103-114) from the max input width."""
-    return (d << max(2 * n_in - 2, 0)).bit_length() + 1
+    return d.bit_length() + max(2 * n_in - 2, 0) + 1      # bit_length(d << (2 n_in - 2)) + 1

@@ -145,7 +145,7 @@ class IntPolynomial:
 
 def output_bit_width(d: int, n_in: int) -> int:
     """Width of the product from the tight bound |c_i| <= d 2^(2 n_in - 2)."""
-    return (d << max(2 * n_in - 2, 0)).bit_length() + 1
+    return d.bit_length() + max(2 * n_in - 2, 0) + 1      # bit_length(d << (2 n_in - 2)) + 1
 
 
 def product_bit_width(a: IntPolynomial, b: IntPolynomial) -> int:

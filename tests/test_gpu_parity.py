@@ -342,6 +342,23 @@ def test_corruption_is_detected():
     assert tc.multiply(tc.MulRequest(a, b)) == tc.multiply(tc.MulRequest(b, a))   # no fault: fine
 
 
+def test_odd_combination_is_detected():
+    # tc/_kernels.py:416-417 -> tc/multiplier.py:156-160: the reference's u + v
+    # parity check; here the acyclic product's term 2K-1 of a row must be 0.
+    # plan.flags bit 1 adds 1 to every residue of slot (row, 2K-1): a value
+    # inside the CRT bound, so only this check can catch it
+    from paper_1612_05778_b200.multiplier import _run_pipeline
+    rng = random.Random(78)
+    a = _random_poly(rng, 40, 300)
+    b = _random_poly(rng, 33, 300)
+    for row in (0, 7, 71):
+        with pytest.raises(tc.CorruptedConvolutionError, match=rf"odd combination at coefficient {row}$"):
+            _run_pipeline(tc.MulRequest(a, b), plan_override={"flags": 2 | (row << 16)})
+    # a padding row past the product is never checked
+    out, _, _ = _run_pipeline(tc.MulRequest(a, b), plan_override={"flags": 2 | (200 << 16)})
+    assert out == tc.multiply(tc.MulRequest(a, b))
+
+
 def test_extreme_plans(oracle):
     # K = 1 (no digit split), one prime, and the widest prime sets the planner
     # reaches with single-word digits; every plan gives the same product

@@ -85,9 +85,10 @@ def test_reference_build_plan_matches_golden():
 
 def test_gpu_prime_table():
     tab = params.gpu_prime_table()
-    assert len(tab) >= 40
+    assert len(tab) >= 100
+    assert max(s.k for s in tab) == 26 and sorted(s.p for s in tab if s.k >= 24) == [167772161, 469762049, 754974721]
     for s in tab:
-        assert (1 << 29) < s.p < (1 << 30) and s.p == s.q * (1 << s.k) + 1 and s.q % 2 == 1
+        assert s.p < (1 << 30) and s.k >= 20 and s.p == s.q * (1 << s.k) + 1 and s.q % 2 == 1
         assert params.is_prime_u64(s.p) and params.is_primitive_root(s.generator, s)
 
 
