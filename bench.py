@@ -1,32 +1,37 @@
 #!/usr/bin/env python3
 """Benchmark: product time and output Gbit/s of the dense Z[y] multiply on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--extra C1,C2,C4,C5]
+                    [--impl ours|reference]
 
 Metric (BASELINE.json): "product time (ms) & output Gbit/s, dxN-bit Z[x]
 multiply"; `value` is output Gbit/s = rows*out_bits/1e9 per product / time.
-Workload: BASELINE config C2 (d=8192, N=8192-bit signed; configs[1]), seeded
-synthetic inputs (paper_1612_05778_b200/workloads.py), the same arrays the
-reference hashes in tests/golden/configs.json.
+Workload: BASELINE config C3 (d=65536, N=65536-bit, half all-ones), the
+largest configuration that fits one GPU (BASELINE.json's metric names no
+single config); C1, C2, C4, C5 are measured beside it (`other_configs`).
+Seeded synthetic inputs (paper_1612_05778_b200/workloads.py), the same arrays
+the reference hashes in tests/golden/configs.json; every config's product is
+checked against the reference's SHA-256 before it is timed.
 
 * value      device-resident: inputs already in HBM, output left in HBM; each
-             step = device width scan + host plan + every kernel, timed with
-             CUDA events on the library's stream, L2 flushed (256 MiB memset)
-             before every step outside the timed region.
-* e2e        the public API `multiply(MulRequest(a, b))` on pinned host arrays:
-             H2D of both operands, all kernels and D2H of the product inside the
-             timed region (wall clock around the synchronous call).
-* roofline   the dominant stage of the device-resident step: algorithmic bytes
-             (HBM) and radix-2 butterflies (INT pipe) per launch / its event
-             time, against MEASURED_PEAKS.json's HBM copy bandwidth and the
-             butterfly peak measured live by tc_int_peak.
-* cpu_baseline  the CPU oracle (oracle/, a C restatement of the reference's
-             numba kernels) on this host, all cores, one full C2 product.
+             step = device width scan + every kernel, timed with CUDA events on
+             the library's stream, L2 flushed (256 MiB memset) before every step
+             outside the timed region.
+* e2e        the public API `multiply(MulRequest(a, b))` on plain (pageable)
+             numpy arrays, as a drop-in caller holds them: H2D of both operands,
+             all kernels and D2H of the product inside the timed region (wall
+             clock around the synchronous call).  `e2e_pinned`: page-locked inputs.
+* roofline   every stage of the device-resident step: algorithmic bytes (HBM)
+             and radix-2 butterflies (INT pipe) / its event time, against
+             MEASURED_PEAKS.json's HBM copy bandwidth and the butterfly peak
+             measured live by tc_int_peak; the longest stage is the headline.
+* cpu_baseline  the reference's algorithm (oracle/, a C restatement of its numba
+             kernels, 63-bit primes, its own plan) on this host: one full product
+             on all cores with the stage split, and a one-thread sample.
 
 `--impl reference` times that same CPU restatement as the reference arm.
-N > 1 (torchrun): ONE product sharded over the N GPUs (shard.py: row tiles <->
-column groups, two NCCL all-to-all transposes per product, gather to rank 0);
-"scaling": "strong", time = max over ranks of CUDA-event time on each rank.
+N > 1 (torchrun): ONE product sharded over the N GPUs (shard.py); "scaling":
+"strong", time = max over ranks of CUDA-event time on each rank.
 """
 from __future__ import annotations
 
@@ -43,6 +48,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_1612_05778_b200 import workloads  # noqa: E402
+
+REF_SAMPLE_D = 16384        # reference-arm sample (see run_reference)
 METRIC = "product time (ms) & output Gbit/s, dxN-bit Z[x] multiply, at 1/2/4/8 B200"
 
 
@@ -193,126 +201,214 @@ def stage_model(plan, da, db, a_cw, b_cw, out_cw):
     return st
 
 
-def run_ours(args, rank, world, local):
-    import ctypes
-    import paper_1612_05778_b200 as tc
-    from paper_1612_05778_b200 import _lib, workloads
-    from paper_1612_05778_b200.params import plan_gpu
-    from paper_1612_05778_b200.zpoly import output_bit_width
+def _cpu_info():
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        import psutil
+        phys = psutil.cpu_count(logical=False)
+    except Exception:  # noqa: BLE001
+        phys = None
+    return {"model": model, "logical_cpus": os.cpu_count(), "physical_cores": phys}
 
-    ctx = _lib.context(local)
-    lib, h = ctx.lib, ctx.handle
-    (aw, ab), (bw, bb) = workloads.make_inputs(args.config)
-    da, db = aw.shape[0], bw.shape[0]
-    rows = da + db - 1
 
-    # device-resident copies
-    def dalloc(nbytes):
+class Resident:
+    """One config's device-resident product (inputs already in HBM, output
+    left in HBM) through tc_stage_inputs + tc_execute."""
+
+    def __init__(self, ctx, config):
+        import ctypes
+        from paper_1612_05778_b200 import _lib
+        from paper_1612_05778_b200.params import plan_gpu
+        from paper_1612_05778_b200.zpoly import output_bit_width
+        self.ctx, self.lib, self.h = ctx, ctx.lib, ctx.handle
+        self.config = config
+        (aw, ab), (bw, bb) = workloads.make_inputs(config)
+        self.aw, self.ab, self.bw, self.bb = aw, ab, bw, bb
+        self.da, self.db = aw.shape[0], bw.shape[0]
+        self.rows = self.da + self.db - 1
+        lib, h = self.lib, self.h
+        self.d_a, self.d_b = self._alloc(aw.nbytes), self._alloc(bw.nbytes)
+        _lib.check(lib.tc_memcpy(h, self.d_a, _lib.ptr(aw), aw.nbytes, 1), "H2D")
+        _lib.check(lib.tc_memcpy(h, self.d_b, _lib.ptr(bw), bw.nbytes, 1), "H2D")
+        info = _lib.TcInputInfo()
+        _lib.check(lib.tc_stage_inputs(h, self.d_a, self.da, aw.shape[1], self.d_b, self.db, bw.shape[1], 1,
+                                       ctypes.byref(info)), "stage")
+        self.n_in = max(info.n_in_a, info.n_in_b)
+        self.out_bits = output_bit_width(max(self.da, self.db), self.n_in)
+        self.out_cw = -(-self.out_bits // 64)
+        self.d_out = self._alloc(self.rows * self.out_cw * 8)
+        # the plan of these shapes, made once from the measured widths (as a
+        # resident caller re-running one shape would); every timed step still
+        # runs the device width scans, the whole product and the error checks
+        self.plan = plan_gpu(max(self.da, self.db), min(self.da, self.db), self.n_in)
+        self.c_plan = _lib.make_plan(self.plan)
+        self.out_gbit = self.rows * self.out_bits / 1e9
+
+    def _alloc(self, nbytes):
+        import ctypes
+        from paper_1612_05778_b200 import _lib
         p = ctypes.c_void_p()
-        _lib.check(lib.tc_device_alloc(h, nbytes, ctypes.byref(p)), "tc_device_alloc")
+        _lib.check(self.lib.tc_device_alloc(self.h, nbytes, ctypes.byref(p)), "tc_device_alloc")
         return p
 
-    d_a, d_b = dalloc(aw.nbytes), dalloc(bw.nbytes)
-    _lib.check(lib.tc_memcpy(h, d_a, _lib.ptr(aw), aw.nbytes, 1), "H2D")
-    _lib.check(lib.tc_memcpy(h, d_b, _lib.ptr(bw), bw.nbytes, 1), "H2D")
-    info = _lib.TcInputInfo()
-    _lib.check(lib.tc_stage_inputs(h, d_a, da, aw.shape[1], d_b, db, bw.shape[1], 1,
-                                   ctypes.byref(info)), "stage")
-    n_in = max(info.n_in_a, info.n_in_b)
-    out_bits = output_bit_width(max(da, db), n_in)
-    out_cw = -(-out_bits // 64)
-    d_out = dalloc(rows * out_cw * 8)
+    def free(self):
+        for p in (self.d_a, self.d_b, self.d_out):
+            self.lib.tc_device_free(self.h, p)
 
-    # the plan of these shapes, made once from the measured widths (as a
-    # resident caller re-running one shape would); every timed step still
-    # runs the device width scans, the whole product and the error checks
-    plan = plan_gpu(max(da, db), min(da, db), n_in)
-    c_plan = _lib.make_plan(plan)
-
-    def resident_step():
-        _lib.check(lib.tc_stage_inputs(h, d_a, da, aw.shape[1], d_b, db, bw.shape[1], 1, None), "stage")
+    def step(self):
+        import ctypes
+        from paper_1612_05778_b200 import _lib
+        lib, h = self.lib, self.h
+        _lib.check(lib.tc_stage_inputs(h, self.d_a, self.da, self.aw.shape[1], self.d_b, self.db,
+                                       self.bw.shape[1], 1, None), "stage")
         err = ctypes.c_int64(-1)
-        rc = lib.tc_execute(h, ctypes.byref(c_plan), ab, bb, d_out, rows, out_cw, 1,
+        rc = lib.tc_execute(h, ctypes.byref(self.c_plan), self.ab, self.bb, self.d_out, self.rows, self.out_cw, 1,
                             None, ctypes.byref(err))
         _lib.check(rc, "tc_execute")
         if err.value >= 0:
             raise SystemExit(f"bench: corrupted convolution reported at {err.value}")
-        return plan
 
-    # correctness gate (like tc/bench.py:110-125): no timing without parity
-    resident_step()
-    host_out = np.empty((rows, out_cw), dtype=np.uint64)
-    _lib.check(lib.tc_memcpy(h, _lib.ptr(host_out), d_out, host_out.nbytes, 2), "D2H")
-    golden = json.load(open(os.path.join(ROOT, "tests", "golden", "configs.json"))).get(args.config)
-    verified = None
-    if golden:
-        verified = (workloads.words_sha256(host_out) == golden["out_sha256"]
-                    and out_bits == golden["out_bits"])
-        if not verified:
-            raise SystemExit(f"bench: product mismatch vs the reference hash for {args.config}")
+    def verify(self):
+        """Correctness gate (like tc/bench.py:110-125): no timing without parity."""
+        from paper_1612_05778_b200 import _lib
+        self.step()
+        host_out = np.empty((self.rows, self.out_cw), dtype=np.uint64)
+        _lib.check(self.lib.tc_memcpy(self.h, _lib.ptr(host_out), self.d_out, host_out.nbytes, 2), "D2H")
+        golden = json.load(open(os.path.join(ROOT, "tests", "golden", "configs.json"))).get(self.config)
+        if not golden:
+            return None
+        ok = workloads.words_sha256(host_out) == golden["out_sha256"] and self.out_bits == golden["out_bits"]
+        if not ok:
+            raise SystemExit(f"bench: product mismatch vs the reference hash for {self.config}")
+        return True
 
-    def step_timed(fn):
+    def timed(self):
+        """CUDA-event time (ms) of one step on the library's stream, L2 flushed before."""
+        import ctypes
+        from paper_1612_05778_b200 import _lib
+        lib, h = self.lib, self.h
         _lib.check(lib.tc_flush_l2(h), "flush")
         _lib.check(lib.tc_record_event(h, 0), "event")
-        fn()
+        self.step()
         _lib.check(lib.tc_record_event(h, 1), "event")
         ms = ctypes.c_float()
         _lib.check(lib.tc_event_elapsed(h, 0, 1, ctypes.byref(ms)), "elapsed")
         return ms.value
 
-    clocks = ClockSampler(local)
-    clocks.start()
-    for _ in range(args.warmup):
-        step_timed(resident_step)
-    _barrier(world)
-    l0 = ctx.launches()
-    times = [step_timed(resident_step) for _ in range(args.steps)]
-    launches = ctx.launches() - l0
-    # per-stage profile of one more step (same kernels, enqueued directly with
-    # stage events instead of the captured graph) for the roofline
-    _lib.check(lib.tc_set_profiling(h, 1), "profiling")
-    step_timed(resident_step)
-    _lib.check(lib.tc_set_profiling(h, 0), "profiling")
-    prof = (ctypes.c_double * 8)()
-    lib.tc_last_profile(h, prof, None)
-    dev_ms = float(np.sum(times))
-    dev_ms_max = _max_over_ranks(dev_ms, world)
+    def stage_profile(self):
+        """Per-stage event times of one more step (same kernels, enqueued
+        directly with stage events instead of the captured graph)."""
+        import ctypes
+        from paper_1612_05778_b200 import _lib
+        _lib.check(self.lib.tc_set_profiling(self.h, 1), "profiling")
+        self.timed()
+        _lib.check(self.lib.tc_set_profiling(self.h, 0), "profiling")
+        prof = (ctypes.c_double * 8)()
+        self.lib.tc_last_profile(self.h, prof, None)
+        return list(prof)[:5]
 
-    # end to end through the public API from pinned host memory
-    pa = _lib.pinned.empty(aw.shape, np.uint64)
-    pb = _lib.pinned.empty(bw.shape, np.uint64)
-    pa[...] = aw
-    pb[...] = bw
+
+def e2e_loop(ctx, aw, ab, bw, bb, steps, warmup, pinned):
+    """multiply(MulRequest(a, b)) end to end from host arrays: H2D of both
+    operands, every kernel and the D2H of the product inside the timed region
+    (wall clock around the synchronous call).  pinned=False: the plain
+    (pageable) numpy arrays a drop-in caller holds."""
+    import paper_1612_05778_b200 as tc
+    from paper_1612_05778_b200 import _lib
+    if pinned:
+        pa = _lib.pinned.empty(aw.shape, np.uint64)
+        pb = _lib.pinned.empty(bw.shape, np.uint64)
+        pa[...] = aw
+        pb[...] = bw
+    else:
+        pa, pb = aw, bw
     A = tc.IntPolynomial._trusted(pa, ab)
     B = tc.IntPolynomial._trusted(pb, bb)
-    for _ in range(args.warmup):
+    lib, h = ctx.lib, ctx.handle
+    for _ in range(warmup):
         _lib.check(lib.tc_flush_l2(h), "flush")
         lib.tc_synchronize(h)
         tc.multiply(tc.MulRequest(A, B))
-    e2e = []
-    for _ in range(args.steps):
+    ts = []
+    for _ in range(steps):
         _lib.check(lib.tc_flush_l2(h), "flush")
         lib.tc_synchronize(h)
         t0 = time.perf_counter()
         prod = tc.multiply(tc.MulRequest(A, B))
-        e2e.append(time.perf_counter() - t0)
+        ts.append(time.perf_counter() - t0)
         del prod
-    clock_info = clocks.stop()
-    clock_info["window"] = "the warm-up, timed and e2e loops"
-    e2e_s = _max_over_ranks(float(np.sum(e2e)), world)
+    return float(np.sum(ts))
 
-    out_gbit = rows * out_bits / 1e9
+
+def run_ours(args, rank, world, local):
+    import ctypes
+    from paper_1612_05778_b200 import _lib
+    from paper_1612_05778_b200.params import pass_layout
+
+    ctx = _lib.context(local)
+    lib, h = ctx.lib, ctx.handle
+    R = Resident(ctx, args.config)
+    verified = R.verify()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(args.warmup):
+        R.timed()
+    _barrier(world)
+    l0 = ctx.launches()
+    times = [R.timed() for _ in range(args.steps)]
+    launches = ctx.launches() - l0
+    prof = R.stage_profile()
+    dev_ms_max = _max_over_ranks(float(np.sum(times)), world)
+
+    # end to end through the public API: plain numpy inputs (the headline)
+    # and pinned ones
+    e2e_s = _max_over_ranks(e2e_loop(ctx, R.aw, R.ab, R.bw, R.bb, args.steps, args.warmup, pinned=False), world)
+    e2e_pin_s = _max_over_ranks(e2e_loop(ctx, R.aw, R.ab, R.bw, R.bb, args.steps, args.warmup, pinned=True), world)
+
+    out_gbit = R.out_gbit
     value = world * args.steps * out_gbit / (dev_ms_max / 1e3)
     e2e_value = world * args.steps * out_gbit / e2e_s
+    e2e_pin_value = world * args.steps * out_gbit / e2e_pin_s
 
-    # roofline of the dominant stage
+    # the other BASELINE configs: device-resident and end-to-end figures
+    extras = {}
+    plan = R.plan
+    aw_nbytes, bw_nbytes, rows, out_cw = R.aw.nbytes, R.bw.nbytes, R.rows, R.out_cw
+    R.free()
+    for cfg in [c for c in args.extra.split(",") if c and c != args.config]:
+        X = Resident(ctx, cfg)
+        xv = X.verify()
+        for _ in range(3):
+            X.timed()
+        xs = [X.timed() for _ in range(args.steps)]
+        xe = e2e_loop(ctx, X.aw, X.ab, X.bw, X.bb, args.steps, 2, pinned=False)
+        xp = e2e_loop(ctx, X.aw, X.ab, X.bw, X.bb, args.steps, 2, pinned=True)
+        extras[cfg] = {"value": round(args.steps * X.out_gbit / (float(np.sum(xs)) / 1e3), 3), "unit": "Gbit/s",
+                       "ms_per_step": round(float(np.mean(xs)), 4),
+                       "e2e": {"value": round(args.steps * X.out_gbit / xe, 3), "ms_per_step": round(1e3 * xe / args.steps, 4)},
+                       "e2e_pinned": {"value": round(args.steps * X.out_gbit / xp, 3),
+                                      "ms_per_step": round(1e3 * xp / args.steps, 4)},
+                       "plan": X.plan.describe(), "verified_vs_reference_sha256": xv}
+        X.free()
+    clock_info = clocks.stop()
+    clock_info["window"] = "the warm-up, timed and e2e loops of every config"
+
+    # roofline: every stage's fractions, the longest stage named
     peaks = _peaks()
     bfly_peak = ctypes.c_double()
     mont_peak = ctypes.c_double()
     lib.tc_int_peak(h, ctypes.byref(bfly_peak), ctypes.byref(mont_peak))
-    model = stage_model(plan, da, db, aw.shape[1], bw.shape[1], out_cw)
+    model = stage_model(plan, R.da, R.db, R.aw.shape[1], R.bw.shape[1], out_cw)
     names = ["convert", "ntt_forward", "pointwise", "ntt_inverse", "recover"]
-    stage_ms = dict(zip(names, list(prof)[:5]))
+    stage_ms = dict(zip(names, prof))
     stages = {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     for n in names:
@@ -322,7 +418,8 @@ def run_ours(args, rank, world, local):
         gbf = m["bfly"] / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
         stages[n] = dict(ms=round(ms, 4), GBps=round(gbs, 1), hbm_frac=round(gbs / hbm_peak, 3),
                          Gbfly_s=round(gbf, 1),
-                         int_frac=round(gbf / (bfly_peak.value / 1e9), 3) if bfly_peak.value else None)
+                         int_frac=round(gbf / (bfly_peak.value / 1e9), 3) if bfly_peak.value else None,
+                         share_of_step=round(ms / max(sum(stage_ms.values()), 1e-9), 3))
     dom = max(names, key=lambda n: stage_ms[n])
     ds = stages[dom]
     if (ds["int_frac"] or 0) >= ds["hbm_frac"]:
@@ -332,32 +429,39 @@ def run_ours(args, rank, world, local):
         roof = {"bound": "hbm", "achieved": ds["GBps"], "peak": hbm_peak, "unit": "GB/s",
                 "frac": ds["hbm_frac"]}
     # DRAM traffic per launch of the dominant stage's kernel, from the committed
-    # ncu --set full capture of this config (profiles/r1_traffic.json)
+    # ncu --set full capture of this config
     traffic, tsrc = None, None
-    try:
-        tj = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json"))).get(args.config)
-        if tj and dom in tj["stages"]:
-            ls = tj["stages"][dom]
-            traffic = round(sum(x["dram_bytes"] for x in ls) / len(ls))
-            tsrc = f"{tj['source']}: {ls[0]['kernel']}, {len(ls)} launch(es) per product"
-    except (OSError, ValueError, KeyError):
-        pass
-    from paper_1612_05778_b200.params import pass_layout
+    for tf in ("r2_traffic.json", "r1_traffic.json"):
+        try:
+            tj = json.load(open(os.path.join(ROOT, "profiles", tf))).get(args.config)
+            if tj and dom in tj["stages"]:
+                ls = tj["stages"][dom]
+                traffic = round(sum(x["dram_bytes"] for x in ls) / len(ls))
+                tsrc = f"{tj['source']}: {ls[0]['kernel']}, {len(ls)} launch(es) per product"
+                break
+        except (OSError, ValueError, KeyError):
+            pass
     nh = len(pass_layout(plan.L.bit_length() - 1, plan.s_y.bit_length() - 1, plan.P)[1])
     nlaunch = {"convert": 2, "ntt_forward": max(1, 2 * nh - 1), "ntt_inverse": max(1, nh - 1)}.get(dom, 1)
-    # the same capture's pipe counters per stage kernel (north_star: each kernel
-    # justified by ncu counters -- HBM GB/s and integer-pipe utilisation)
     ncu = None
-    try:
-        nj = json.load(open(os.path.join(ROOT, "profiles", "r1_ncu_metrics.json"))).get(args.config)
-        ncu = nj["kernels"] if nj else None
-    except (OSError, ValueError, KeyError):
-        pass
+    for nf in ("r2_ncu_metrics.json", "r1_ncu_metrics.json"):
+        try:
+            nj = json.load(open(os.path.join(ROOT, "profiles", nf))).get(args.config)
+            if nj:
+                ncu = nj["kernels"]
+                break
+        except (OSError, ValueError, KeyError):
+            pass
+    mm = canonical_modmuls(args.config)
     roof.update({"kernel": dom, "traffic": traffic, "traffic_source": tsrc, "ncu": ncu,
                  "algorithmic_bytes_per_launch": int(model[dom]["bytes"] // nlaunch),
                  "peak_source": "hbm: MEASURED_PEAKS.json hbm_gbs (measured); int: tc_int_peak "
                                 "register-only butterfly chain, measured live",
-                 "stages": stages})
+                 "stages": stages,
+                 "canonical": {"modmuls_per_product": mm, "unit": "64-bit modmul/s (SURVEY 8(d) MM, reference plan)",
+                               "effective_rate": round(mm / (dev_ms_max / args.steps / 1e3), 1),
+                               "note": "the reference's own work count at P = 2 over the device-resident time; "
+                                       "this build does different (32-bit, pruned, fewer-prime) work"}})
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Gbit/s", "n_gpus": world,
@@ -366,25 +470,29 @@ def run_ours(args, rank, world, local):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded PCG64, BASELINE.md section 4 recipe)",
         "config": {"workload": f"{args.config}: {workloads.CONFIGS[args.config].text}",
-                   "d": max(da, db), "N": workloads.CONFIGS[args.config].N,
-                   "rows": rows, "out_bits": out_bits,
+                   "d": max(R.da, R.db), "N": workloads.CONFIGS[args.config].N,
+                   "rows": rows, "out_bits": R.out_bits,
                    "plan": plan.describe(), "parallelism": f"replicas x{world}",
-                   "l2": "flushed (256 MiB memset) before every timed step",
+                   "l2": "flushed (256 MiB memset) before every timed step (device-resident and e2e)",
                    "timed_step": "device width scans + tc_execute (all kernels, error flags read back) "
                                  "with the plan made once for these shapes",
                    "verified_vs_reference_sha256": verified},
         "e2e": {"value": round(e2e_value, 3), "unit": "Gbit/s",
                 "ms_per_step": round(1e3 * e2e_s / args.steps, 4),
-                "h2d_bytes_per_step": int(aw.nbytes + bw.nbytes),
+                "h2d_bytes_per_step": int(aw_nbytes + bw_nbytes),
                 "d2h_bytes_per_step": int(rows * out_cw * 8),
-                "api": "paper_1612_05778_b200.multiply(MulRequest) on pinned host arrays"},
+                "api": "paper_1612_05778_b200.multiply(MulRequest) on plain (pageable) numpy arrays"},
+        "e2e_pinned": {"value": round(e2e_pin_value, 3), "unit": "Gbit/s",
+                       "ms_per_step": round(1e3 * e2e_pin_s / args.steps, 4),
+                       "api": "the same call on page-locked host arrays"},
         "roofline": roof,
         "gpu_launches": int(launches),
         "int_peak": {"butterflies_per_s": bfly_peak.value, "montmul_per_s": mont_peak.value},
         "clocks": clock_info,
+        "other_configs": extras,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.config, aw, ab, bw, bb, out_gbit, samples=1)
+        line["cpu_baseline"] = cpu_baseline(args.config, R.aw, R.ab, R.bw, R.bb, out_gbit)
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -470,21 +578,52 @@ def run_sharded(args, rank, world, local):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(config, aw, ab, bw, bb, out_gbit, samples=1):
-    """The oracle (C restatement of the reference kernels) on this host's cores."""
+def canonical_modmuls(config):
+    """MM = 2P [3 (S/2) log2 S + 2S] + 2P d K of the
+    reference plan (P = 2) of this config: the reference's own work count."""
+    from oracle import port   # noqa: F401  (planning only: the reference plan's shape)
+    c = workloads.CONFIGS[config]
+    n_in = 64 if c.kind == "int64" else c.N + 1
+    pl = port.plan_from_shape(c.d, n_in, 2)
+    P, S = len(pl.primes), pl.s_y * pl.K
+    return 2 * P * (3 * (S // 2) * (S.bit_length() - 1) + 2 * S) + 2 * P * c.d * pl.K
+
+
+def cpu_baseline(config, aw, ab, bw, bb, out_gbit):
+    """The reference's algorithm on this host's cores (oracle/, a C
+    restatement of the reference's numba kernels with its 63-bit primes and
+    its own plan; the Python reference cannot travel to this box): one full
+    product on every host thread with its stage split (the reference's
+    StageTimings layout), and a one-thread sample -- the first 4096
+    coefficients of each operand, coefficient width unchanged -- sized to
+    ~10 s (a full one-thread C3 product takes minutes)."""
     from oracle import port
     threads = os.cpu_count() or 1
     port.multiply_words(aw[:64], ab, bw[:64], bb, threads=threads)   # warm tables / pages
-    ts = []
-    for _ in range(samples):
-        t0 = time.perf_counter()
-        port.multiply_words(aw, ab, bw, bb, threads=threads)
-        ts.append(time.perf_counter() - t0)
-    t = float(np.median(ts))
+    t0 = time.perf_counter()
+    _, _, st = port.multiply_words(aw, ab, bw, bb, threads=threads, stats=True)
+    t = time.perf_counter() - t0
+    stages = {k: round(v * 1e3, 1) for k, v in st.items()}
+    rows = aw.shape[0] + bw.shape[0] - 1
+    sub = min(4096, aw.shape[0], bw.shape[0])
+    if sub < aw.shape[0]:
+        sa, sb = aw[:sub], bw[:sub]
+    else:
+        sa, sb = aw, bw
+    t1 = time.perf_counter()
+    _, sbits = port.multiply_words(sa, ab, sb, bb, threads=1)
+    t1 = time.perf_counter() - t1
+    sub_gbit = (2 * sa.shape[0] - 1) * sbits / 1e9
     return {"value": round(out_gbit / t, 4), "unit": "Gbit/s", "cores": threads, "kind": "port",
-            "ms_per_product": round(t * 1e3, 1),
-            "sample": f"{samples} full {config} product(s) (reference algorithm: 63-bit primes, P=2, "
-                      f"reference plan), OpenMP over all host threads"}
+            "ms_per_product": round(t * 1e3, 1), "stage_ms": stages,
+            "numeric_only_ms": round(t * 1e3, 1),
+            "numeric_only_note": "the C restatement has no Python-int scans (tc/params.py:290-293, "
+                                 "tc/zpoly.py:45-48,103-114), so total = numeric-only",
+            "cpu": _cpu_info(),
+            "sample": f"1 full {config} product (reference algorithm: 63-bit primes, P=2, reference plan), "
+                      f"OpenMP over all {threads} host threads",
+            "w1": {"value": round(sub_gbit / t1, 4), "unit": "Gbit/s", "cores": 1, "ms": round(t1 * 1e3, 1),
+                   "sample": f"first {sa.shape[0]} coefficients of each {config} operand (same width), 1 thread"}}
 
 
 def run_reference(args, rank, world):
@@ -494,11 +633,22 @@ def run_reference(args, rank, world):
     from paper_1612_05778_b200 import workloads
     (aw, ab), (bw, bb) = workloads.make_inputs(args.config)
     threads = os.cpu_count() or 1
+    # bounded sample: a full C3 product takes ~29 s on the box's 16 cores, so
+    # each step multiplies the first REF_SAMPLE_D coefficients of each operand
+    # (coefficient width unchanged; output Gbit/s of that product).  Per
+    # output bit the smaller product is slightly cheaper (log d in the NTT),
+    # so the sampled rate flatters the reference.
+    full_d = aw.shape[0]
+    if aw.shape[0] > REF_SAMPLE_D:
+        aw, bw = aw[:REF_SAMPLE_D], bw[:REF_SAMPLE_D]
     rows = aw.shape[0] + bw.shape[0] - 1
     out_bits = port.product_bit_width(aw, bw)
     out_gbit = rows * out_bits / 1e9
-    for _ in range(args.warmup):
-        port.multiply_words(aw, ab, bw, bb, threads=threads)
+    # warm-up: the C restatement has no JIT; one product of the first 1024
+    # coefficients pages in its code and tables (full warm-up products would
+    # only lengthen the run: a C3 product takes seconds)
+    if args.warmup:
+        port.multiply_words(aw[:1024], ab, bw[:1024], bb, threads=threads)
     ts = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
@@ -515,9 +665,12 @@ def run_reference(args, rank, world):
                    "parallelism": "CPU, all host threads"},
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 4), "unit": "Gbit/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} full {args.config} products, oracle/ C restatement "
+                         "sample": f"{args.steps} products of the first {aw.shape[0]} of the {full_d} coefficients "
+                                   f"of each {args.config} operand (width unchanged), oracle/ C restatement "
                                    f"of the reference kernels (the reference is pure Python/numba "
-                                   f"and is not present on the GPU box)"},
+                                   f"and is not present on the GPU box); warm-up: one product of "
+                                   f"the first 1024 coefficients",
+                         "cpu": _cpu_info()},
         "e2e": {"value": round(value, 4), "unit": "Gbit/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -560,7 +713,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--extra", default="C1,C2,C4,C5",
+                    help="other BASELINE configs measured beside the headline (other_configs)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

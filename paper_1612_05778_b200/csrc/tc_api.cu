@@ -16,6 +16,10 @@
 #include <vector>
 #include <algorithm>
 #include <chrono>
+#include <thread>
+#include <mutex>
+#include <condition_variable>
+#include <atomic>
 
 #include "../../include/tc_api.h"
 #include "tc_kernels.cuh"
@@ -85,6 +89,7 @@ struct Ctx {
     cudaStream_t st = nullptr;
     DevBuf in_a, in_b, grids, twx_f, twx_i, twy_f, twy_i, pcs, flags, outbuf, dbg, nbias;
     DevBuf sp_a, sp_b, sp_out;          // Kronecker reductions: packed operands, inner product (tc_split.cuh)
+    DevBuf nbtab; int64_t nbt_key[2] = {-1, -1};          // crt_convert_warp's bias tables, key (M, P)
     int64_t nb_key[4] = {-1, -1, -1, -1};  // (M, P, L, W32) of nbias
     std::vector<uint32_t> pcs_key; int64_t pcs_S = -1;   // primes and S of pcs
     cudaGraphExec_t gexec = nullptr;                     // captured product pipeline (run_pipeline)
@@ -106,7 +111,109 @@ struct Ctx {
     int* hinfo = nullptr;                // pinned: widths read back early
     cudaEvent_t fev[2] = {};             // fork / join of the resident pipeline's two branches
     int sms = 148;                       // multiprocessors of the device
+    // pageable uploads: a pinned ring of chunks filled by the copy pool while
+    // the copy engine drains the previous chunk (stage_upload)
+    char* ring = nullptr;
+    cudaEvent_t ring_ev[4] = {};
+    int64_t ring_next = 0;
 };
+
+// A small pool of host threads for the pageable -> pinned copies of
+// stage_upload: one chunk is split into equal pieces, the calling thread takes
+// a piece too.  Process-wide, created on first use.
+class CopyPool {
+public:
+    static CopyPool& get() { static CopyPool p; return p; }
+    void copy(char* dst, const char* src, size_t len) {
+        const int T = (int)workers_.size() + 1;
+        if (T == 1 || len < ((size_t)1 << 20)) { memcpy(dst, src, len); return; }
+        std::unique_lock<std::mutex> lk(mu_);
+        dst_ = dst; src_ = src; len_ = len; pieces_ = T;
+        next_.store(0); remaining_.store(T);
+        ++gen_;
+        lk.unlock();
+        cv_.notify_all();
+        work();
+        lk.lock();
+        done_cv_.wait(lk, [&] { return remaining_.load() == 0; });
+    }
+    ~CopyPool() {
+        { std::lock_guard<std::mutex> lk(mu_); stop_ = true; ++gen_; }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+private:
+    CopyPool() {
+        int n = (int)std::thread::hardware_concurrency();
+        const char* e = getenv("TC_COPY_THREADS");
+        n = e && *e ? atoi(e) : (n > 8 ? 8 : n);
+        for (int i = 1; i < n; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    void work() {
+        for (;;) {
+            const int k = next_.fetch_add(1);
+            if (k >= pieces_) break;
+            const size_t per = (len_ / pieces_ + 63) & ~(size_t)63;
+            const size_t a = (size_t)k * per;
+            if (a < len_) memcpy(dst_ + a, src_ + a, a + per < len_ ? per : len_ - a);
+            if (remaining_.fetch_sub(1) == 1) { std::lock_guard<std::mutex> lk(mu_); done_cv_.notify_all(); }
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+            lk.unlock();
+            work();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    char* dst_ = nullptr; const char* src_ = nullptr; size_t len_ = 0; int pieces_ = 0;
+    std::atomic<int> next_{0}, remaining_{0};
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+constexpr size_t kRingChunk = (size_t)16 << 20;   // bytes per ring slot
+constexpr int kRingSlots = 4;
+
+bool host_is_pinned(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { (void)cudaGetLastError(); return false; }
+    return at.type == cudaMemoryTypeHost;
+}
+
+// H2D of `bytes` from host memory on stream st.  Page-locked sources go
+// straight to the copy engine; pageable ones (a drop-in caller's numpy arrays)
+// are staged chunk by chunk through the pinned ring, the copy pool filling
+// chunk i+1 while the copy engine reads chunk i -- instead of the driver's
+// synchronous pageable path (measured ~13 GB/s on the box against ~55 GB/s).
+// Returns when the last chunk is queued.
+int stage_upload(Ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (bytes < ((size_t)4 << 20) || host_is_pinned(src) || getenv("TC_NO_STAGING")) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return TC_OK;
+    }
+    if (!c->ring) {
+        CK(cudaHostAlloc((void**)&c->ring, kRingChunk * kRingSlots, cudaHostAllocDefault));
+        for (auto& e : c->ring_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    for (size_t off = 0; off < bytes; off += kRingChunk) {
+        const int slot = (int)(c->ring_next++ % kRingSlots);
+        char* sp = c->ring + (size_t)slot * kRingChunk;
+        const size_t len = bytes - off < kRingChunk ? bytes - off : kRingChunk;
+        CK(cudaEventSynchronize(c->ring_ev[slot]));          // the copy that last read this slot is done
+        CopyPool::get().copy(sp, static_cast<const char*>(src) + off, len);
+        CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, sp, len, cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(c->ring_ev[slot], st));
+    }
+    return TC_OK;
+}
 
 int ilog2(int64_t x) { int l = 0; while ((1ll << l) < x) ++l; return l; }
 int env_int(const char* name, int dflt) {           // tuning knobs for experiments
@@ -527,6 +634,32 @@ int ensure_nbias(Ctx* c, int M, int P, int64_t L, int W32) {
     return TC_OK;
 }
 
+// crt_convert_warp's bias words: -(sum_j 2^(32P-1+Mj)) mod 2^(32w), per
+// group-relative word, for a row's first group and for the later groups (the
+// pattern repeats with the group of 32 terms, GW = 32 AW + B words; checked).
+int ensure_nbtab(Ctx* c, int M, int P) {
+    if (c->nbt_key[0] == M && c->nbt_key[1] == P && c->nbtab.p) return TC_OK;
+    const int GW = M;                          // 32 AW + B = M words per group of 32 terms
+    const int nwd = 3 * GW;
+    std::vector<uint32_t> b((size_t)nwd, 0u);
+    for (int64_t j = 0;; ++j) {
+        const int64_t bit = 32ll * P - 1 + (int64_t)M * j;
+        if (bit >= 32ll * nwd) break;
+        b[(size_t)(bit >> 5)] |= 1u << (bit & 31);
+    }
+    uint64_t carry = 1;                        // two's complement negation
+    for (auto& w : b) { const uint64_t t = (uint64_t)(uint32_t)~w + carry; w = (uint32_t)t; carry = t >> 32; }
+    for (int v = 0; v < GW; ++v)
+        if (b[(size_t)(GW + v)] != b[(size_t)(2 * GW + v)])
+            return set_err(TC_ERR_BAD_ARG, "bias pattern of M=%d P=%d is not periodic", M, P);
+    int rc;
+    if ((rc = c->nbtab.ensure(sizeof(uint32_t) * 2 * GW))) return rc;
+    CK(cudaMemcpyAsync(c->nbtab.p, b.data(), sizeof(uint32_t) * 2 * GW, cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));          // pageable source (never inside a graph capture: run_pipeline calls this first)
+    c->nbt_key[0] = M; c->nbt_key[1] = P;
+    return TC_OK;
+}
+
 int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows, int M, int W32,
                  uint32_t* out, const CrtConst& cc, bool dump, const ShardArgs& sh,
                  int64_t x0 = 0, int64_t nx = -1) {
@@ -565,6 +698,18 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
         // k_final -12 %; C2's 514-word rows: +2 %)
         static const int kw2 = env_int("TC_CO_KW2_MAX", 16);
         A.co_kw = W32 <= kw2 ? 2 : 4;
+        // warp-group CRT + ConvertOut: M = 32 AW + B, rows of >= 32 terms,
+        // every stored word inside the groups' span (+ the flush group)
+        static const int cwarp = env_int("TC_CO_WARP", 1);
+        const int waw = M >> 5, wb = M & 31;
+        if (cwarp && !dump && W32 > 0 && G.lgL >= 5 && wb <= 1 &&
+            ((waw == 2 && G.P >= 1 && G.P <= 8) || (waw == 1 && G.P <= 4)) &&
+            (int64_t)W32 <= (int64_t)M * ((G.L >> 5) + 1)) {
+            int rc = ensure_nbtab(c, M, G.P);
+            if (rc) return rc;
+            A.cw_aw = waw; A.cw_b = wb; A.nbtab = c->nbtab.as<uint32_t>();
+            A.co_aw = 0;
+        }
     }
     const uint32_t n = 1u << (G.lgL + G.yl);
     const size_t smem = (size_t)G.P * padded_words(n) * 4;
@@ -705,6 +850,8 @@ int run_pipeline(Ctx* c, const tc_plan_t* pl, int a_bits, int b_bits, int64_t ro
     if ((rc = ensure_pcs(c, pl, G.S))) return rc;
     if ((rc = c->flags.ensure(64))) return rc;
     if (!dump && W32 > 0 && (rc = ensure_nbias(c, (int)pl->M, G.P, G.L, W32))) return rc;
+    if (!dump && W32 > 0 && pl->M >= 32 && pl->M <= 65 && (pl->M & 31) <= 1 && (rc = ensure_nbtab(c, (int)pl->M, G.P)))
+        return rc;
     static const int use_graph = env_int("TC_GRAPH", 1);
     // stage events (per-stage times, profiling) go on the direct path: event
     // nodes inside the graph cost as much as the launches it saves
@@ -908,7 +1055,7 @@ int tc_ctx_destroy(void* ctx) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->st);
     for (DevBuf* b : {&c->in_a, &c->in_b, &c->grids, &c->twx_f, &c->twx_i, &c->twy_f, &c->twy_i,
-                      &c->pcs, &c->flags, &c->outbuf, &c->dbg, &c->nbias, &c->sp_a, &c->sp_b, &c->sp_out}) b->release();
+                      &c->pcs, &c->flags, &c->outbuf, &c->dbg, &c->nbias, &c->sp_a, &c->sp_b, &c->sp_out, &c->nbtab}) b->release();
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (auto& ev : c->ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : c->user_ev) if (ev) cudaEventDestroy(ev);
@@ -916,6 +1063,8 @@ int tc_ctx_destroy(void* ctx) {
     for (auto& ev : c->fev) if (ev) cudaEventDestroy(ev);
     if (c->aux) { cudaStreamSynchronize(c->aux); cudaStreamDestroy(c->aux); }
     if (c->hinfo) cudaFreeHost(c->hinfo);
+    for (auto& ev : c->ring_ev) if (ev) { cudaEventSynchronize(ev); cudaEventDestroy(ev); }
+    if (c->ring) cudaFreeHost(c->ring);
     c->flush.release();
     cudaStreamDestroy(c->st);
     delete c;
@@ -935,8 +1084,8 @@ int tc_stage_inputs(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw,
     } else {
         if ((rc = c->in_a.ensure((size_t)da * a_cw * 8))) return rc;
         if ((rc = c->in_b.ensure((size_t)db * b_cw * 8))) return rc;
-        CK(cudaMemcpyAsync(c->in_a.p, a, (size_t)da * a_cw * 8, cudaMemcpyHostToDevice, c->st));
-        CK(cudaMemcpyAsync(c->in_b.p, b, (size_t)db * b_cw * 8, cudaMemcpyHostToDevice, c->st));
+        if ((rc = stage_upload(c, c->in_a.p, a, (size_t)da * a_cw * 8, c->st))) return rc;
+        if ((rc = stage_upload(c, c->in_b.p, b, (size_t)db * b_cw * 8, c->st))) return rc;
         c->a_dev = c->in_a.as<uint64_t>(); c->b_dev = c->in_b.as<uint64_t>();
     }
     c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true;
@@ -1054,8 +1203,8 @@ int multiply_host_split(Ctx* c, const uint64_t* a, int64_t da, int32_t a_cw, int
     int* wf = c->dbg.as<int>();
     CK(cudaEventRecord(c->ev[0], c->st));
     CK(cudaMemsetAsync(wf, 0, 16, c->st));
-    CK(cudaMemcpyAsync(c->in_a.p, a, (size_t)da * a_cw * 8, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->in_b.p, b, (size_t)db * b_cw * 8, cudaMemcpyHostToDevice, c->st));
+    if ((rc = stage_upload(c, c->in_a.p, a, (size_t)da * a_cw * 8, c->st))) return rc;
+    if ((rc = stage_upload(c, c->in_b.p, b, (size_t)db * b_cw * 8, c->st))) return rc;
     k_width<<<(unsigned)((da + 255) / 256), 256, 0, c->st>>>(c->a_dev, da, a_cw, wf);
     k_width<<<(unsigned)((db + 255) / 256), 256, 0, c->st>>>(c->b_dev, db, b_cw, wf + 2);
     c->launches += 2;
@@ -1136,22 +1285,19 @@ int multiply_host_impl(Ctx* c, const uint64_t* a, int64_t da, int32_t a_cw, int3
     c->a_dev = c->in_a.as<uint64_t>(); c->b_dev = c->in_b.as<uint64_t>();
     c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true;
     int* wf = c->dbg.as<int>();
-    // both uploads first (A, then B behind it on the aux stream: A first over
-    // PCIe); the host preparation below runs while they are on the wire
-    CK(cudaEventRecord(c->ev[0], c->st));
-    CK(cudaMemsetAsync(wf, 0, 16, c->st));
-    CK(cudaMemcpyAsync(c->in_a.p, a, (size_t)da * a_cw * 8, cudaMemcpyHostToDevice, c->st));
-    CK(cudaEventRecord(c->xev[0], c->st));            // A uploaded (and the width flags cleared)
-    CK(cudaStreamWaitEvent(c->aux, c->xev[0], 0));
-    CK(cudaMemcpyAsync(c->in_b.p, b, (size_t)db * b_cw * 8, cudaMemcpyHostToDevice, c->aux));
-    CK(cudaEventRecord(c->xev[20], c->aux));
     Geometry G;
     if ((rc = prepare(c, plan, G, true)) || (rc = c->grids.ensure((size_t)2 * G.P * G.S * 4))) return rc;
     uint32_t* GA = c->grids.as<uint32_t>();
     uint32_t* GB = GA + (size_t)G.P * G.S;
     const ShardArgs one = single_gpu();
-    // main: A's width, its first pass and its forward high passes (A's whole
-    // forward transform: nothing of it waits for B)
+    // main: A's upload, width, first pass and forward high passes (A's whole
+    // forward transform: nothing of it waits for B); B's upload then goes out
+    // on the aux stream while A's kernels run (pageable sources are staged
+    // through the pinned ring by the host copy pool meanwhile)
+    CK(cudaEventRecord(c->ev[0], c->st));
+    CK(cudaMemsetAsync(wf, 0, 16, c->st));
+    if ((rc = stage_upload(c, c->in_a.p, a, (size_t)da * a_cw * 8, c->st))) return rc;
+    CK(cudaEventRecord(c->xev[0], c->st));            // A uploaded (and the width flags cleared)
     const int nh = (int)G.high.size();
     k_width<<<(unsigned)((da + 255) / 256), 256, 0, c->st>>>(c->a_dev, da, a_cw, wf);
     c->launches++;
@@ -1160,6 +1306,9 @@ int multiply_host_impl(Ctx* c, const uint64_t* a, int64_t da, int32_t a_cw, int3
     if ((rc = launch_low(c, G, plan, c->a_dev, da, a_cw, a_bits > plan->N, GA, one))) return rc;
     for (int i = 0; i < nh; ++i)
         if ((rc = launch_high(c, MODE_FWD, G, GA, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
+    CK(cudaStreamWaitEvent(c->aux, c->xev[0], 0));     // B's DMA behind A's on the copy engine
+    if ((rc = stage_upload(c, c->in_b.p, b, (size_t)db * b_cw * 8, c->aux))) return rc;
+    CK(cudaEventRecord(c->xev[20], c->aux));
     // aux: B's width, both widths back to the host
     k_width<<<(unsigned)((db + 255) / 256), 256, 0, c->aux>>>(c->b_dev, db, b_cw, wf + 2);
     c->launches++;

@@ -1611,6 +1611,8 @@ struct FinalArgs {
     int co_stage;                  // grouped ConvertOut stages product words after the tiles (coalesced stores)
     int co_nostage;                // grouped ConvertOut stores straight from registers (A/B)
     int co_kw;                     // word-per-thread ConvertOut: words per thread (2, or TC_CO_KW)
+    int cw_aw, cw_b;               // > 0: warp-group CRT + ConvertOut (crt_convert_warp), M = 32 cw_aw + cw_b
+    const uint32_t* nbtab;         // its bias tables: 2 x (32 cw_aw + cw_b) words (first group / later groups)
 };
 
 // ---------------------------------------------------------------------------
@@ -1851,6 +1853,228 @@ __device__ __forceinline__ void crt_convert_grouped(const FinalArgs& A, const Cr
     }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-group CRT + ConvertOut for M = 32 AW + B (AW in {1, 2}, B in {0, 1}:
+// every BASELINE plan with L >= 32).  A warp takes 32 consecutive terms of a
+// row at a time ("group" g: terms j = 32 g + lane).  Term j starts at word
+// u_j = GW g + AW lane (GW = 32 AW + B words per group) with shift B lane, so
+// lane i lifts its term by CRT in registers (no limb round trip through
+// shared memory) and cuts it into NPC = P + B pieces, piece k landing in
+// group word AW i + k.  Lane o owns group words AW o .. AW o + AW - 1 (lane
+// 31 also the B extra word 32 AW) and gathers their pieces by warp shuffles:
+// word AW o + s takes piece AW t + s of lane o - t, t = 0, 1, ... -- from the
+// previous group (same warp, previous iteration) when o < t, where that word
+// is piece AW t + s + B of lane o - t + 32.  Terms are biased (c_ij +
+// 2^(32P-1) >= 0) so every piece is unsigned; the bias comes back out through
+// the per-word constants nbtab (periodic with the group: one table for a
+// row's first group, one for the others).  The word sums S_w (64-bit) then
+// resolve by the binary carry chain over t_w = lo(S_w) + hi(S_(w-1)): lane
+// level generate / propagate, one ballot add per warp, a running carry across
+// the warp's groups.  Each warp works a contiguous segment of its row's groups
+// (plus one virtual all-zero group that flushes the last tail); a segment not
+// at a row start first recomputes the group before it (its tail pieces and its
+// last word's high half), and its binary carry-in comes from the segments
+// before it after a barrier (carry-out for carry-in 0 and 1 per segment, then
+// an increment of the segment's first words where the carry-in is 1).  Words
+// are stored straight to global memory (each warp store covers one group's
+// consecutive words).
+// ---------------------------------------------------------------------------
+template <int P, int AW, int B>
+struct WarpCoShape {
+    static constexpr int GW = 32 * AW + B;          // words per group of 32 terms
+    static constexpr int NPC = P + B;               // pieces per term
+    static constexpr int TMAX = (NPC - 1) / AW;     // farthest lane distance of a piece
+};
+
+// Pieces of lane's term j of the tile row at rowbase (virtual terms j >= L:
+// biased zeros).  Reports bound / parity errors of real product rows.
+template <int P, int B>
+__device__ __forceinline__ void warp_term_pieces(const FinalArgs& A, const CrtConst& cc, const uint32_t* sm,
+                                                 uint32_t stride, uint32_t rowbase, int j, int L, uint32_t prow,
+                                                 bool real_row, uint32_t (&pc)[P + B]) {
+    uint32_t x[P];
+    if (j < L) {
+        uint32_t rr[P];
+        const uint32_t e = padi(rowbase + (uint32_t)j);
+        rr[0] = canon(sm[e], cc.p[0]);
+#pragma unroll
+        for (int q = 1; q < P; ++q) rr[q] = reduce_2p(sm[q * stride + e], 2 * cc.p[q]);
+        const int64_t flat = (int64_t)prow * L + j;
+        if (A.inject >= 0 && flat == A.inject) rr[0] = rr[0] ? rr[0] - 1 : cc.p[0] - 1;   // fault injection (tests)
+        if (A.inject_par >= 0 && flat == A.inject_par) {
+#pragma unroll
+            for (int q = 0; q < P; ++q) rr[q] = (rr[q] + 1) % cc.p[q];
+        }
+        const bool bad = crt_term<P>(rr, cc, x);
+        if (real_row) {
+            if (bad) atomicMin(&A.err[2], (int)min(flat, (int64_t)0x7fffffff));
+            if (j == L - 1 && !bad) {      // the term 2K-1 must vanish (tc/_kernels.py:416-417)
+                uint32_t nz = 0;
+#pragma unroll
+                for (int l = 0; l < P; ++l) nz |= x[l];
+                if (nz) atomicMin(&A.err[3], (int)prow);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int l = 0; l < P; ++l) x[l] = 0u;
+    }
+    x[P - 1] ^= 0x80000000u;                              // biased: c_ij + 2^(32P-1) >= 0
+    const int r = B ? (j & 31) : 0;
+#pragma unroll
+    for (int k = 0; k < P + B; ++k) {
+        if (B) {
+            const uint32_t lo = k > 0 ? x[k > 0 ? k - 1 : 0] : 0u, hi = k < P ? x[k < P ? k : 0] : 0u;
+            pc[k] = __funnelshift_l(lo, hi, r);
+        } else {
+            pc[k] = x[k < P ? k : 0];
+        }
+    }
+}
+
+template <int P, int AW, int B>
+__device__ __forceinline__ void crt_convert_warp(const FinalArgs& A, const CrtConst& cc, const uint32_t* sm,
+                                                 uint32_t stride, int R, uint32_t pos0, bool sharded) {
+    using Sh = WarpCoShape<P, AW, B>;
+    constexpr int GW = Sh::GW, NPC = Sh::NPC, TMAX = Sh::TMAX;
+    constexpr int NOWN = AW + B;                          // words a lane may own (lane 31: AW + B)
+    __shared__ uint32_t nbt[2][GW];
+    __shared__ uint32_t segc[32];                         // per warp: carry-out for carry-in 0 (bit 0) / 1 (bit 1)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int L = 1 << A.lgL, ngr = L >> 5, ngo = ngr + 1;   // + the virtual flush group
+    const int W32 = A.W32;
+    for (int i = threadIdx.x; i < 2 * GW; i += blockDim.x) nbt[i / GW][i % GW] = __ldg(A.nbtab + i);
+    __syncthreads();
+    // work split: nseg segments per row (a warp per segment), or whole rows per warp
+    const int nseg = nw > R ? nw / R : 1;
+    const int rstride = nw > R ? R : nw;                  // one row per warp, or rows warp, warp + nw, ...
+    int r = nw > R ? warp / nseg : warp;
+    const int seg = nw > R ? warp % nseg : 0;
+    const int ga = (int)(((int64_t)ngo * seg) / nseg), gb = (int)(((int64_t)ngo * (seg + 1)) / nseg);
+    uint32_t segflags = 0;
+    int64_t seg_w0 = 0;
+    uint32_t* seg_row = nullptr;
+    for (; r < R; r += rstride) {
+        const uint32_t prow = bitrev(pos0 + (uint32_t)r, A.lgS);
+        const bool real_row = prow < A.rows_out;
+        if (!real_row && !sharded) continue;
+        const uint32_t rowbase = (uint32_t)r << A.lgL;
+        uint32_t* orow = sharded ? A.out + ((int64_t)blockIdx.x * R + r) * W32 : A.out + (int64_t)prow * W32;
+        uint32_t prv[NPC];
+        uint32_t hprev = 0;                               // hi of the previous group's last word
+        if (ga > 0) {
+            // warm-up: the group before the segment, for its tail pieces and last word
+            const int g = ga - 1;
+            warp_term_pieces<P, B>(A, cc, sm, stride, rowbase, 32 * g + lane, L, prow, false, prv);
+            // last word of group g: lane 31's word AW*31 + AW - 1 (B = 0) or 32 AW (B = 1)
+            uint64_t S = 0;
+#pragma unroll
+            for (int t = 0; t <= TMAX; ++t) {
+                // word GW - 1 takes piece k of lane 31 - t: k = AW t + AW - 1 (B = 0), AW (t + 1) (B = 1)
+                const int k = B ? AW * (t + 1) : AW * t + AW - 1;
+                if (k < NPC) S += __shfl_sync(0xffffffffu, prv[k < NPC ? k : 0], 31 - t);
+            }
+            S += nbt[g == 0 ? 0 : 1][GW - 1];
+            hprev = (uint32_t)(S >> 32);
+        } else {
+#pragma unroll
+            for (int k = 0; k < NPC; ++k) prv[k] = 0u;
+        }
+        uint32_t c0 = 0, c1 = 1;                          // running carry for segment carry-in 0 / 1
+        for (int g = ga; g < gb; ++g) {
+            uint32_t cur[NPC];
+            warp_term_pieces<P, B>(A, cc, sm, stride, rowbase, 32 * g + lane, L, prow, real_row, cur);
+            const uint32_t* nb = nbt[g == 0 ? 0 : 1];
+            // word sums of the owned words: slot s < AW, and (lane 31, B = 1) the extra word
+            uint64_t S[NOWN];
+#pragma unroll
+            for (int s = 0; s < AW; ++s) {
+                uint64_t acc = cur[s];
+#pragma unroll
+                for (int t = 1; t <= TMAX; ++t) {
+                    const int k = AW * t + s;
+                    if (k < NPC) {
+                        const uint32_t vc = __shfl_sync(0xffffffffu, cur[k < NPC ? k : 0], (lane - t) & 31);
+                        uint32_t vp = 0;
+                        if (k + B < NPC) vp = __shfl_sync(0xffffffffu, prv[k + B < NPC ? k + B : 0], (lane - t) & 31);
+                        acc += lane >= t ? vc : vp;
+                    }
+                }
+                S[s] = acc + nb[AW * lane + s];
+            }
+            if (B) {
+                // lane 31's extra word 32 AW: piece AW (t' + 1) of lane 31 - t'
+                uint64_t acc = 0;
+#pragma unroll
+                for (int tp = 0; tp <= TMAX; ++tp) {
+                    const int k = AW * (tp + 1);
+                    if (k < NPC) acc += __shfl_sync(0xffffffffu, cur[k < NPC ? k : 0], (lane - tp) & 31);
+                }
+                S[NOWN - 1] = acc + nb[GW - 1];
+            }
+            const int nown = (B && lane == 31) ? AW + 1 : AW;
+            // carry terms t_w = lo(S_w) + hi(S_(w-1))
+            const uint32_t hlast = (uint32_t)(S[nown == AW ? AW - 1 : NOWN - 1] >> 32);
+            uint32_t hin = __shfl_up_sync(0xffffffffu, hlast, 1);
+            if (lane == 0) hin = hprev;
+            hprev = __shfl_sync(0xffffffffu, hlast, 31);
+            const int64_t wbase = (int64_t)GW * g + AW * lane;
+            uint32_t tw[NOWN], gg[NOWN], pp[NOWN];
+            uint32_t gl = 0, pl = 1;                      // lane generate / all-propagate
+            uint32_t h = hin;
+#pragma unroll
+            for (int s = 0; s < NOWN; ++s) {
+                if (s < nown) {
+                    const uint64_t t = (S[s] & 0xffffffffull) + h;
+                    h = (uint32_t)(S[s] >> 32);
+                    tw[s] = (uint32_t)t;
+                    gg[s] = (uint32_t)(t >> 32);
+                    pp[s] = (uint32_t)t == 0xffffffffu;
+                    gl = gg[s] | (pp[s] & gl);
+                    pl &= pp[s];
+                }
+            }
+            // carry-out of the lane for carry-in 0 (gl) and 1 (gl | pl)
+            const unsigned G1 = __ballot_sync(0xffffffffu, gl);
+            const unsigned P1 = __ballot_sync(0xffffffffu, pl & !gl);
+            const uint64_t Am = (uint64_t)(G1 | P1), Bm = (uint64_t)G1;
+            uint32_t c = (uint32_t)(((Am + Bm + c0) ^ Am ^ Bm) >> lane) & 1u;
+            c0 = (uint32_t)((Am + Bm + c0) >> 32) & 1u;
+            c1 = (uint32_t)((Am + Bm + c1) >> 32) & 1u;
+#pragma unroll
+            for (int s = 0; s < NOWN; ++s) {
+                if (s < nown) {
+                    const int64_t w = wbase + s;
+                    if (w < W32) orow[w] = tw[s] + c;
+                    c = gg[s] | (pp[s] & c);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NPC; ++k) prv[k] = cur[k];
+        }
+        segflags = c0 | (c1 << 1);
+        seg_w0 = (int64_t)GW * ga;
+        seg_row = orow;
+    }
+    if (nseg > 1) {
+        // binary carries across the segments of a row (a row's first segment has carry-in 0)
+        if (lane == 0) segc[warp] = segflags;
+        __syncthreads();
+        if (lane == 0 && seg > 0 && seg_row != nullptr) {
+            uint32_t cin = 0;
+            for (int s = warp - seg; s < warp; ++s) cin = cin ? (segc[s] >> 1) & 1u : segc[s] & 1u;
+            if (cin) {
+                const int64_t w1 = min((int64_t)GW * gb, (int64_t)W32);
+                for (int64_t w = seg_w0; w < w1; ++w) {
+                    const uint32_t v = seg_row[w] + 1u;
+                    seg_row[w] = v;
+                    if (v != 0u) break;
+                }
+            }
+        }
+    }
+}
+
 // Word-per-thread ConvertOut (any M; the grouped path covers M = 32 AW + {0, 1}
 // with L >= 4), kW words per thread: 2 for short rows (C4: 6-word rows,
 // k_final -12 %), TC_CO_KW otherwise.
@@ -2063,6 +2287,21 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
                 if (A.co_aw == 2) { crt_convert_grouped<P, 2, true, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }
             if constexpr (P <= 3)
                 if (A.co_aw == 1) { crt_convert_grouped<P, 1, true, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }
+        }
+    }
+    // warp-group CRT + ConvertOut (M = 32 AW + {0, 1}, host-checked shape)
+    if constexpr (!DUMP && P <= 8) {
+        if (A.cw_aw == 2) {
+            if (A.cw_b) crt_convert_warp<P, 2, 1>(A, cc, sm, stride, R, pos0, sharded);
+            else crt_convert_warp<P, 2, 0>(A, cc, sm, stride, R, pos0, sharded);
+            return;
+        }
+        if constexpr (P <= 4) {
+            if (A.cw_aw == 1) {
+                if (A.cw_b) crt_convert_warp<P, 1, 1>(A, cc, sm, stride, R, pos0, sharded);
+                else crt_convert_warp<P, 1, 0>(A, cc, sm, stride, R, pos0, sharded);
+                return;
+            }
         }
     }
     // CRT in place

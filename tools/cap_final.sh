@@ -1,11 +1,9 @@
-# Source-level capture of k_final (C2) exported to CSV on the box + C3 launch list.
-mkdir -p gpurun_out/cap
-python bench.py --config C2 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/cap/pre.json 2>gpurun_out/cap/pre.err || exit 1
-ncu --set full --import-source on --clock-control none -k regex:"k_final" -c 1 -o /tmp/fin \
-    python bench.py --config C2 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/cap/ncu_f.log 2>&1
-ncu -i /tmp/fin.ncu-rep --page source --csv --print-source=cuda,sass > gpurun_out/cap/fin_src.csv 2>&1
-ncu -i /tmp/fin.ncu-rep --page source --csv --print-source=sass > gpurun_out/cap/fin_sass.csv 2>&1
-gzip gpurun_out/cap/fin_src.csv gpurun_out/cap/fin_sass.csv
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/cap/launches_C3.csv \
-    python bench.py --config C3 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/cap/ncu_l3.log 2>&1
-ls -la gpurun_out/cap
+# one --set full capture of k_final for a config, source page exported; usage: bash tools/cap_final.sh CFG TAG
+CFG=${1:-C3}; TAG=${2:-x}
+mkdir -p gpurun_out/fin_$TAG
+ncu --set full --import-source on --clock-control none -k regex:"k_final" -c 1 -o /tmp/fin_$TAG \
+    python bench.py --config $CFG --steps 1 --warmup 0 --no-cpu-baseline --extra "" > gpurun_out/fin_$TAG/ncu.log 2>&1
+python tools/ncu_summary.py /tmp/fin_$TAG.ncu-rep > gpurun_out/fin_$TAG/summary.txt 2>&1
+python tools/ncu_brief.py /tmp/fin_$TAG.ncu-rep >> gpurun_out/fin_$TAG/summary.txt 2>&1
+ncu -i /tmp/fin_$TAG.ncu-rep --page source --csv --print-source=cuda,sass --kernel-name regex:k_final > gpurun_out/fin_$TAG/src.csv 2>&1
+gzip -f gpurun_out/fin_$TAG/src.csv
