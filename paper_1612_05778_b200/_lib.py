@@ -178,30 +178,78 @@ class Context:
 
 class PinnedPool:
     """Pinned host blocks for product outputs and staged inputs, recycled when
-    the numpy array that views them is garbage-collected."""
+    the numpy array that views them is garbage-collected.
 
-    def __init__(self):
-        self.free: dict = {}
+    Block sizes are rounded up to eighths of a power of two (at least 64 KiB:
+    at most 12.5 % slack), so products of nearby sizes share blocks; free blocks above `cap_bytes` in total are
+    returned to the driver (least recently released first), and every free
+    block is released at interpreter exit."""
+
+    MIN_BLOCK = 1 << 16
+
+    def __init__(self, cap_bytes: int | None = None):
+        import collections
+        self.free = collections.OrderedDict()      # (size, addr) -> None, oldest release first
+        self.free_bytes = 0
+        self.cap = cap_bytes if cap_bytes is not None else int(os.environ.get("TC_PINNED_POOL_CAP", 8 << 30))
         self.lock = threading.Lock()
+        import atexit
+        atexit.register(self.release_all)
+
+    @classmethod
+    def bucket(cls, nbytes: int) -> int:
+        if nbytes <= cls.MIN_BLOCK:
+            return cls.MIN_BLOCK
+        step = 1 << max(nbytes.bit_length() - 4, 0)
+        return -(-nbytes // step) * step
 
     def empty(self, shape, dtype=np.uint64) -> np.ndarray:
-        nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        count = int(np.prod(shape))
+        nbytes = count * np.dtype(dtype).itemsize
+        size = self.bucket(nbytes)
+        addr = None
         with self.lock:
-            blocks = self.free.get(nbytes)
-            addr = blocks.pop() if blocks else None
+            for key in self.free:
+                if key[0] == size:
+                    addr = key[1]
+                    del self.free[key]
+                    self.free_bytes -= size
+                    break
         if addr is None:
             p = ctypes.c_void_p()
-            check(load().tc_host_alloc(nbytes, ctypes.byref(p)), "tc_host_alloc")
+            check(load().tc_host_alloc(size, ctypes.byref(p)), "tc_host_alloc")
             addr = p.value
         buf = (ctypes.c_char * max(nbytes, 1)).from_address(addr)
-        arr = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+        arr = np.frombuffer(buf, dtype=dtype, count=count).reshape(shape)
         import weakref
-        weakref.finalize(buf, self._release, nbytes, addr)
+        weakref.finalize(buf, self._release, size, addr)
         return arr
 
-    def _release(self, nbytes, addr):
+    def _release(self, size, addr):
+        drop = []
         with self.lock:
-            self.free.setdefault(nbytes, []).append(addr)
+            self.free[(size, addr)] = None
+            self.free_bytes += size
+            while self.free_bytes > self.cap and self.free:
+                (sz, ad), _ = self.free.popitem(last=False)
+                self.free_bytes -= sz
+                drop.append(ad)
+        for ad in drop:
+            load().tc_host_free(ctypes.c_void_p(ad))
+
+    def release_all(self):
+        with self.lock:
+            addrs = [ad for (_, ad) in self.free]
+            self.free.clear()
+            self.free_bytes = 0
+        lib = _lib
+        if lib is None:
+            return
+        for ad in addrs:
+            try:
+                lib.tc_host_free(ctypes.c_void_p(ad))
+            except Exception:  # noqa: BLE001 -- interpreter shutdown
+                pass
 
 
 pinned = PinnedPool()

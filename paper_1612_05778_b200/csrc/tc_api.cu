@@ -6,6 +6,8 @@
 //   passes -> inverse x-NTT -> fused CRT + ConvertOut -> product words.
 // Replaces _run_pipeline (tc/multiplier.py:131-166) after `build_plan`.
 #include <cuda_runtime.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdarg.h>
@@ -524,6 +526,49 @@ cudaError_t launch_high_ct(int mode, const HighArgs& A, dim3 grid, uint32_t n, c
     return launch_high_ct_mode<NT, U, MODE_MID, CB, GTW>(A, grid, n, st);
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            (void)cudaGetLastError();
+            return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+        }
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// The 3-D view of an operand's P grids that k_high_tma's tiles are boxes of:
+// {2^b0 (contiguous), 2^U (stride 2^b0), P S / 2^(b0+U)}, box {32, min(2^U, 256), 1}.
+int high_tile_map(const Geometry& G, const uint32_t* base, int b0, int U, TmaMap* out) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return set_err(TC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {1ull << b0, 1ull << U, (cuuint64_t)((G.P * G.S) >> (b0 + U))};
+    cuuint64_t strides[2] = {(1ull << b0) * 4, (1ull << (b0 + U)) * 4};
+    cuuint32_t box[3] = {32, (cuuint32_t)(U > 8 ? 256 : 1 << U), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    static_assert(sizeof(TmaMap) == sizeof(CUtensorMap), "tensor map size");
+    const CUresult r = enc(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_UINT32, 3,
+                           const_cast<uint32_t*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(TC_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return TC_OK;
+}
+
+template <int MODE, int U>
+cudaError_t launch_high_tma_mode(const HighArgs& A, const TmaMap& mg, const TmaMap& mo, dim3 grid, cudaStream_t st) {
+    constexpr uint32_t n = 1u << (U + 5);
+    const size_t smem = 128 + (size_t)(MODE == MODE_MID ? 2 : 1) * n * 4 + (MODE == MODE_MID ? 2 : 1) * ((size_t)8 << U);
+    cudaError_t e = ensure_smem((const void*)k_high_tma<MODE, U, 256>, smem);
+    if (e != cudaSuccess) return e;
+    k_high_tma<MODE, U, 256><<<grid, 256, smem, st>>>(A, mg, mo);
+    return cudaGetLastError();
+}
+
 int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint32_t* other, int u0, int U,
                 const ShardArgs& sh) {
     HighArgs A{};
@@ -564,6 +609,21 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
             CKL();
             return TC_OK;
         }
+    }
+    // cb = 5, 8 levels: TMA-staged dense tiles (k_high_tma)
+    static const int tma_env = env_int("TC_HIGH_TMA", 1);
+    if (A.cb == 5 && G.lgL >= 5 && U == 8 && sh.world == 1 && tma_env) {
+        TmaMap mg, mo;
+        int rc;
+        if ((rc = high_tile_map(G, grids, G.lgL + u0, U, &mg))) return rc;
+        if (mode == MODE_MID && (rc = high_tile_map(G, other, G.lgL + u0, U, &mo))) return rc;
+        if (mode != MODE_MID) mo = mg;
+        cudaError_t e = mode == MODE_FWD ? launch_high_tma_mode<MODE_FWD, 8>(A, mg, mo, grid, c->st)
+                      : mode == MODE_INV ? launch_high_tma_mode<MODE_INV, 8>(A, mg, mo, grid, c->st)
+                                         : launch_high_tma_mode<MODE_MID, 8>(A, mg, mo, grid, c->st);
+        c->launches++;
+        if (e != cudaSuccess) return set_err(TC_ERR_CUDA, "k_high_tma launch failed: %s", cudaGetErrorString(e));
+        return TC_OK;
     }
     // cb = 5: 128-byte row segments per tile column group (TC_HIGH_CB=5)
     if (A.cb == 5 && G.lgL >= 5 && ct_env) {

@@ -1490,6 +1490,170 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (CB == 3 ? 4 : (NT <= 256 ?
 }
 
 // ---------------------------------------------------------------------------
+// k_high_tma: the 32-column high pass (cb = 5) with its tiles moved by the
+// Tensor Memory Accelerator.  A tile (2^U rows at stride 2^b0, 32 contiguous
+// columns) is one box of a 3-D tensor map over the operand's P grids
+// ({2^b0, 2^U, P S / 2^(b0+U)}, box {32, min(2^U, 256), 1}); one thread arms
+// an mbarrier and issues cp.async.bulk.tensor, the block waits on the barrier
+// (the twiddle gather runs meanwhile), and the finished tile goes back with a
+// TMA store.  The shared tile is dense: rows are exactly 128 bytes, and every
+// round of the pass works on bits >= 5, so a warp's accesses are always one
+// row's 32 consecutive words (no bank conflicts, no padding).  MODE_MID also
+// pulls the A tile into a second buffer, started before B's forward rounds.
+// ---------------------------------------------------------------------------
+struct TmaMap { alignas(64) unsigned char b[128]; };
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" :: "r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const TmaMap* map, uint64_t* bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+        :: "r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const TmaMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n"
+                 :: "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src)) : "memory");
+}
+__device__ __forceinline__ void tma_store_commit_wait() {
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// one radix-2^NB round on dense tile bits [BL, BL + NB), BL >= 5
+template <int TB, int BL, int NB, bool DIF, int NT>
+__device__ __forceinline__ void dense_round(uint32_t* s, const uint2* stw, uint32_t p, uint32_t two_p) {
+    constexpr int R = 1 << NB, CB = 5;
+    constexpr uint32_t ngroups = 1u << (TB - NB);
+    constexpr uint32_t lowmask = (1u << BL) - 1;
+    static_assert(BL >= CB, "dense rounds start at the column bits");
+#pragma unroll 1
+    for (uint32_t g = threadIdx.x; g < ngroups; g += NT) {
+        const uint32_t lo = g & lowmask;
+        uint32_t* sp = s + (((g & ~lowmask) << NB) | lo);
+        const uint2* tq = stw + (lo >> CB);
+        uint32_t x[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) x[k] = sp[k << BL];
+#pragma unroll
+        for (int it = 0; it < NB; ++it) {
+            const int lv = DIF ? NB - 1 - it : it;
+            const int vp = BL + lv - CB;
+#pragma unroll
+            for (int m = 0; m < (1 << lv); ++m) {
+                const uint2 w = tq[(1 << vp) + (m << (BL - CB))];
+#pragma unroll
+                for (int jj = 0; jj < R / (2 << lv); ++jj) {
+                    const int k = m + jj * (2 << lv);
+                    if (DIF) bfly_dif(x[k], x[k + (1 << lv)], w.x, w.y, p, two_p);
+                    else bfly_dit(x[k], x[k + (1 << lv)], w.x, w.y, p, two_p);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) sp[k << BL] = x[k];
+    }
+    __syncthreads();
+}
+
+template <int U, bool DIF, int NT>
+__device__ __forceinline__ void dense_pass(uint32_t* s, const uint2* stw, uint32_t p, uint32_t two_p) {
+    constexpr int TB = U + 5;
+    static_assert(U == 8 || U == 9 || U == 10, "dense pass shapes");
+    constexpr int N1 = U == 8 ? 4 : 5;           // rounds of (4, 4) or (5, 4) or (5, 5) levels
+    constexpr int N2 = U - N1;
+    if (!DIF) {
+        dense_round<TB, 5, N1, false, NT>(s, stw, p, two_p);
+        dense_round<TB, 5 + N1, N2, false, NT>(s, stw, p, two_p);
+    } else {
+        dense_round<TB, 5 + N1, N2, true, NT>(s, stw, p, two_p);
+        dense_round<TB, 5, N1, true, NT>(s, stw, p, two_p);
+    }
+}
+
+template <int MODE, int U, int NT>
+__global__ void __launch_bounds__(NT, NT <= 256 ? 3 : 1)
+k_high_tma(HighArgs A, const __grid_constant__ TmaMap mg, const __grid_constant__ TmaMap mo) {
+    constexpr int CB = 5, TB = U + CB;
+    constexpr uint32_t n = 1u << TB, ntw = 1u << U;
+    constexpr int NBOX = U > 8 ? 1 << (U - 8) : 1, BOXR = U > 8 ? 256 : 1 << U;
+    extern __shared__ __align__(16) unsigned char tma_raw[];
+    // TMA tile destinations must be 128-byte aligned: round the dynamic base up
+    uint32_t* s = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(tma_raw) + 127) & ~(uintptr_t)127);
+    uint32_t* so = s + n;                                           // MID: A's tile
+    uint2* stw_f = reinterpret_cast<uint2*>(s + (MODE == MODE_MID ? 2 : 1) * n);
+    uint2* stw_i = MODE == MODE_MID ? stw_f + ntw : stw_f;
+    __shared__ __align__(8) uint64_t bar[2];
+    const int q = blockIdx.y;
+    const PrimeC pc = A.pcs[q];
+    const int b0 = A.lgL + A.u0;
+    const int nmid = b0 - CB;
+    const uint32_t cta = blockIdx.x;
+    const uint32_t mid = cta & ((1u << nmid) - 1);
+    const uint32_t hi = cta >> nmid;
+    const int c0 = (int)(mid << CB);
+    const int c2 = (int)(hi + ((uint32_t)q << (A.lgL + A.lgS - b0 - U)));
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        if (MODE == MODE_MID) mbar_init(&bar[1], 1);
+        fence_proxy_async();
+        mbar_expect_tx(&bar[0], n * 4);
+        for (int i = 0; i < NBOX; ++i) tma_load_3d(s + i * BOXR * 32, &mg, &bar[0], c0, i * BOXR, c2);
+        if (MODE == MODE_MID) {
+            mbar_expect_tx(&bar[1], n * 4);
+            for (int i = 0; i < NBOX; ++i) tma_load_3d(so + i * BOXR * 32, &mo, &bar[1], c0, i * BOXR, c2);
+        }
+    }
+    // the CTA's twiddles (rows below u0 fixed: lgL >= 5), while the tiles land
+    const uint32_t rb = mid >> (A.lgL - CB);
+    {
+        const uint2* twf = A.twf + (int64_t)q * A.tw_stride;
+        const uint2* twi = A.twi + (int64_t)q * A.tw_stride;
+        for (uint32_t i = threadIdx.x; i < ntw; i += NT) {
+            if (i == 0) continue;
+            const int v = 31 - __clz(i);
+            const uint32_t gi = (1u << (A.u0 + v)) + rb + ((i - (1u << v)) << A.u0);
+            if (MODE != MODE_INV) stw_f[i] = __ldg(twf + gi);
+            if (MODE != MODE_FWD) stw_i[i] = __ldg(twi + gi);
+        }
+    }
+    __syncthreads();
+    mbar_wait(&bar[0], 0);
+    if (MODE == MODE_FWD || MODE == MODE_MID) dense_pass<U, false, NT>(s, stw_f, pc.p, pc.two_p);
+    if (MODE == MODE_MID) {
+        mbar_wait(&bar[1], 0);
+#pragma unroll 4
+        for (uint32_t e = threadIdx.x; e < n; e += NT) {
+            const uint32_t x = reduce_2p(s[e], pc.two_p);
+            s[e] = shoup_mul(mont_mul(x, reduce_2p(so[e], pc.two_p), pc.p, pc.pinv_neg), pc.scale, pc.scale_sh, pc.p);
+        }
+        __syncthreads();
+    }
+    if (MODE == MODE_INV || MODE == MODE_MID) dense_pass<U, true, NT>(s, stw_i, pc.p, pc.two_p);
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NBOX; ++i) tma_store_3d(&mg, s + i * BOXR * 32, c0, i * BOXR, c2);
+        tma_store_commit_wait();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // CRT (Garner, mixed radix) of P residues into a signed P*32-bit value with
 // the symmetric lift of tc/_kernels.py:258-313 / tc/multiplier.py:103-128.
 // ---------------------------------------------------------------------------
