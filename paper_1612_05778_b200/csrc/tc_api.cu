@@ -559,13 +559,14 @@ int high_tile_map(const Geometry& G, const uint32_t* base, int b0, int U, TmaMap
     return TC_OK;
 }
 
-template <int MODE, int U>
+template <int MODE, int U, bool AG = false>
 cudaError_t launch_high_tma_mode(const HighArgs& A, const TmaMap& mg, const TmaMap& mo, dim3 grid, cudaStream_t st) {
     constexpr uint32_t n = 1u << (U + 5);
-    const size_t smem = 128 + (size_t)(MODE == MODE_MID ? 2 : 1) * n * 4 + (MODE == MODE_MID ? 2 : 1) * ((size_t)8 << U);
-    cudaError_t e = ensure_smem((const void*)k_high_tma<MODE, U, 256>, smem);
+    constexpr bool OBUF = MODE == MODE_MID && !AG;
+    const size_t smem = 128 + (size_t)(OBUF ? 2 : 1) * n * 4 + (MODE == MODE_MID ? 2 : 1) * ((size_t)8 << U);
+    cudaError_t e = ensure_smem((const void*)k_high_tma<MODE, U, 256, AG>, smem);
     if (e != cudaSuccess) return e;
-    k_high_tma<MODE, U, 256><<<grid, 256, smem, st>>>(A, mg, mo);
+    k_high_tma<MODE, U, 256, AG><<<grid, 256, smem, st>>>(A, mg, mo);
     return cudaGetLastError();
 }
 
@@ -618,8 +619,10 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
         if ((rc = high_tile_map(G, grids, G.lgL + u0, U, &mg))) return rc;
         if (mode == MODE_MID && (rc = high_tile_map(G, other, G.lgL + u0, U, &mo))) return rc;
         if (mode != MODE_MID) mo = mg;
+        static const int mid_ag = env_int("TC_MID_GLOBAL_A", 0);   // A via TMA: C3 MID 6.32 -> 6.10 ms
         cudaError_t e = mode == MODE_FWD ? launch_high_tma_mode<MODE_FWD, 8>(A, mg, mo, grid, c->st)
                       : mode == MODE_INV ? launch_high_tma_mode<MODE_INV, 8>(A, mg, mo, grid, c->st)
+                      : mid_ag           ? launch_high_tma_mode<MODE_MID, 8, true>(A, mg, mo, grid, c->st)
                                          : launch_high_tma_mode<MODE_MID, 8>(A, mg, mo, grid, c->st);
         c->launches++;
         if (e != cudaSuccess) return set_err(TC_ERR_CUDA, "k_high_tma launch failed: %s", cudaGetErrorString(e));
@@ -760,6 +763,8 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
         A.co_kw = W32 <= kw2 ? 2 : 4;
         // warp-group CRT + ConvertOut: M = 32 AW + B, rows of >= 32 terms,
         // every stored word inside the groups' span (+ the flush group)
+        static const int ld4 = env_int("TC_FINAL_LD4", 1);
+        A.ld4 = ld4;
         static const int cwarp = env_int("TC_CO_WARP", 1);
         const int waw = M >> 5, wb = M & 31;
         if (cwarp && !dump && W32 > 0 && G.lgL >= 5 && wb <= 1 &&

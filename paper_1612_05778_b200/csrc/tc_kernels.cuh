@@ -1586,17 +1586,20 @@ __device__ __forceinline__ void dense_pass(uint32_t* s, const uint2* stw, uint32
     }
 }
 
-template <int MODE, int U, int NT>
+template <int MODE, int U, int NT, bool AG = false>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 3 : 1)
 k_high_tma(HighArgs A, const __grid_constant__ TmaMap mg, const __grid_constant__ TmaMap mo) {
+    // AG (MODE_MID): A's tile read from global memory in the pointwise step
+    // (16-byte loads, 8 in flight per thread) instead of a second TMA buffer
     constexpr int CB = 5, TB = U + CB;
     constexpr uint32_t n = 1u << TB, ntw = 1u << U;
     constexpr int NBOX = U > 8 ? 1 << (U - 8) : 1, BOXR = U > 8 ? 256 : 1 << U;
     extern __shared__ __align__(16) unsigned char tma_raw[];
     // TMA tile destinations must be 128-byte aligned: round the dynamic base up
     uint32_t* s = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(tma_raw) + 127) & ~(uintptr_t)127);
+    constexpr bool OBUF = MODE == MODE_MID && !AG;
     uint32_t* so = s + n;                                           // MID: A's tile
-    uint2* stw_f = reinterpret_cast<uint2*>(s + (MODE == MODE_MID ? 2 : 1) * n);
+    uint2* stw_f = reinterpret_cast<uint2*>(s + (OBUF ? 2 : 1) * n);
     uint2* stw_i = MODE == MODE_MID ? stw_f + ntw : stw_f;
     __shared__ __align__(8) uint64_t bar[2];
     const int q = blockIdx.y;
@@ -1610,11 +1613,11 @@ k_high_tma(HighArgs A, const __grid_constant__ TmaMap mg, const __grid_constant_
     const int c2 = (int)(hi + ((uint32_t)q << (A.lgL + A.lgS - b0 - U)));
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
-        if (MODE == MODE_MID) mbar_init(&bar[1], 1);
+        if (OBUF) mbar_init(&bar[1], 1);
         fence_proxy_async();
         mbar_expect_tx(&bar[0], n * 4);
         for (int i = 0; i < NBOX; ++i) tma_load_3d(s + i * BOXR * 32, &mg, &bar[0], c0, i * BOXR, c2);
-        if (MODE == MODE_MID) {
+        if (OBUF) {
             mbar_expect_tx(&bar[1], n * 4);
             for (int i = 0; i < NBOX; ++i) tma_load_3d(so + i * BOXR * 32, &mo, &bar[1], c0, i * BOXR, c2);
         }
@@ -1635,12 +1638,43 @@ k_high_tma(HighArgs A, const __grid_constant__ TmaMap mg, const __grid_constant_
     __syncthreads();
     mbar_wait(&bar[0], 0);
     if (MODE == MODE_FWD || MODE == MODE_MID) dense_pass<U, false, NT>(s, stw_f, pc.p, pc.two_p);
-    if (MODE == MODE_MID) {
+    if (MODE == MODE_MID && !AG) {
         mbar_wait(&bar[1], 0);
 #pragma unroll 4
         for (uint32_t e = threadIdx.x; e < n; e += NT) {
             const uint32_t x = reduce_2p(s[e], pc.two_p);
             s[e] = shoup_mul(mont_mul(x, reduce_2p(so[e], pc.two_p), pc.p, pc.pinv_neg), pc.scale, pc.scale_sh, pc.p);
+        }
+        __syncthreads();
+    }
+    if (MODE == MODE_MID && AG) {
+        // A's tile: row a of the tile is 32 contiguous words at flat (hi, a, mid)
+        const uint32_t* ga = A.other + (int64_t)q * A.S + ((uint64_t)hi << (b0 + U)) + ((uint64_t)mid << CB);
+        constexpr uint32_t nv = n >> 2;
+        constexpr int MB = 8;
+#pragma unroll 1
+        for (uint32_t v0 = threadIdx.x; v0 < nv; v0 += MB * NT) {
+            uint4 y[MB];
+#pragma unroll
+            for (int k = 0; k < MB; ++k) {
+                const uint32_t vi = v0 + k * NT, e = vi << 2;
+                y[k] = vi < nv ? *reinterpret_cast<const uint4*>(ga + ((uint64_t)(e >> CB) << b0) + (e & 31))
+                               : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int k = 0; k < MB; ++k) {
+                const uint32_t vi = v0 + k * NT;
+                if (vi < nv) {
+                    uint32_t* d = s + (vi << 2);
+                    const uint32_t yy[4] = {y[k].x, y[k].y, y[k].z, y[k].w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t x = reduce_2p(d[j], pc.two_p);
+                        d[j] = shoup_mul(mont_mul(x, reduce_2p(yy[j], pc.two_p), pc.p, pc.pinv_neg),
+                                         pc.scale, pc.scale_sh, pc.p);
+                    }
+                }
+            }
         }
         __syncthreads();
     }
@@ -1777,6 +1811,7 @@ struct FinalArgs {
     int co_kw;                     // word-per-thread ConvertOut: words per thread (2, or TC_CO_KW)
     int cw_aw, cw_b;               // > 0: warp-group CRT + ConvertOut (crt_convert_warp), M = 32 cw_aw + cw_b
     const uint32_t* nbtab;         // its bias tables: 2 x (32 cw_aw + cw_b) words (first group / later groups)
+    int ld4;                       // tile loads: four cp.async per address computation
 };
 
 // ---------------------------------------------------------------------------
@@ -2403,6 +2438,14 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
             const uint32_t* g = A.g + (int64_t)q * (A.sh.Tl << A.sh.TB);
             const XchgIdx xi{A.sh, blockIdx.x};
             for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) cp_async4(t + padi(e), g + xi(e));
+        } else if (A.ld4 && n >= 4) {
+            // four consecutive slots per address computation (one padded 32-slot run)
+            const uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)tile * n;
+            for (uint32_t v = threadIdx.x; v < (n >> 2); v += blockDim.x) {
+                uint32_t* d = t + padi(v << 2);
+                const uint32_t* src = g + (v << 2);
+                cp_async4(d, src); cp_async4(d + 1, src + 1); cp_async4(d + 2, src + 2); cp_async4(d + 3, src + 3);
+            }
         } else {
             const uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)tile * n;
             for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) cp_async4(t + padi(e), g + e);
