@@ -80,16 +80,24 @@ typedef struct {
     int64_t split_block;
 } tc_plan_t;
 
-/* StageTimings (tc/multiplier.py:41-56), seconds, measured with CUDA events. */
+/* StageTimings (tc/multiplier.py:41-56), seconds, with the reference's
+ * meaning (tc/multiplier.py:131-166; tc/ntt2d.py:87-125).  Filled only when
+ * the caller asks for them (multiply_with_stats): the product then runs as one
+ * sequential stream with CUDA events between the kernels, and the fused
+ * kernels' time is split by in-kernel phase timers (globaltimer / clock64).
+ * Transfers have no reference counterpart and are reported apart.  */
 typedef struct {
-    double convert;      /* H2D of inputs + ConvertIn fused with the x-direction forward NTT */
-    double ntt_forward;  /* y-direction forward passes (operand A complete, B up to its last pass) */
-    double pointwise;    /* fused last forward pass of B + pointwise product + first inverse pass */
-    double ntt_inverse;  /* remaining inverse y passes + inverse x-direction NTT */
-    double crt;          /* 0: CRT is fused into ConvertOut (reported under `recover`) */
-    double recover;      /* fused CRT + ConvertOut carry scan + D2H of the product */
+    double convert;      /* ConvertIn: balanced digits (k_low's digit phase) + the width scans */
+    double ntt_forward;  /* residue embedding + theta twist + forward 2-D NTTs (rest of k_low, forward
+                            passes, MID's forward part) */
+    double pointwise;    /* MID's pointwise product (with the 1/S scale) */
+    double ntt_inverse;  /* MID's inverse part, inverse passes, k_final's transforms */
+    double crt;          /* k_final's CRT share */
+    double recover;      /* k_final's ConvertOut share (the host adds the result wrapping) */
     double total;        /* whole call, wall clock */
     int32_t gpus;        /* GPUs used by this call */
+    double h2d;          /* host -> device copies of both operands */
+    double d2h;          /* device -> host copy of the product */
 } tc_times_t;
 
 typedef struct {
@@ -210,8 +218,9 @@ int tc_synchronize(void* ctx);
 int tc_host_alloc(int64_t bytes, void** hptr);
 int tc_host_free(void* hptr);
 
-/* Device-side timing on the context's stream: record into slot 0..15, read
- * the elapsed milliseconds between two recorded slots (synchronises). */
+/* Device-side timing on the context's stream: record into slot 0..9 (10..15
+ * belong to the library's own stage timing), read the elapsed milliseconds
+ * between two recorded slots (synchronises). */
 int tc_record_event(void* ctx, int32_t slot);
 int tc_event_elapsed(void* ctx, int32_t s0, int32_t s1, float* ms);
 /* Overwrite a 256 MiB scratch buffer so the next step starts with a cold L2. */

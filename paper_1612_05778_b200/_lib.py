@@ -51,7 +51,8 @@ class TcTimes(ctypes.Structure):
     _fields_ = [("convert", ctypes.c_double), ("ntt_forward", ctypes.c_double),
                 ("pointwise", ctypes.c_double), ("ntt_inverse", ctypes.c_double),
                 ("crt", ctypes.c_double), ("recover", ctypes.c_double),
-                ("total", ctypes.c_double), ("gpus", ctypes.c_int32)]
+                ("total", ctypes.c_double), ("gpus", ctypes.c_int32),
+                ("h2d", ctypes.c_double), ("d2h", ctypes.c_double)]
 
 
 class TcProductInfo(ctypes.Structure):

@@ -92,6 +92,7 @@ struct Ctx {
     DevBuf in_a, in_b, grids, twx_f, twx_i, twy_f, twy_i, pcs, flags, outbuf, dbg, nbias;
     DevBuf sp_a, sp_b, sp_out;          // Kronecker reductions: packed operands, inner product (tc_split.cuh)
     DevBuf nbtab; int64_t nbt_key[2] = {-1, -1};          // crt_convert_warp's bias tables, key (M, P)
+    DevBuf profbuf; bool prof_on = false;                // in-kernel phase timers (multiply_with_stats)
     int64_t nb_key[4] = {-1, -1, -1, -1};  // (M, P, L, W32) of nbias
     std::vector<uint32_t> pcs_key; int64_t pcs_S = -1;   // primes and S of pcs
     cudaGraphExec_t gexec = nullptr;                     // captured product pipeline (run_pipeline)
@@ -475,6 +476,7 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     a.twx = c->twx_f.as<uint2>(); a.twy = c->twy_f.as<uint2>();
     a.twy_stride = G.s_y;
     a.pcs = c->pcs.as<PrimeC>(); a.P = G.P;
+    a.prof = c->prof_on ? c->profbuf.as<unsigned long long>() : nullptr;
     const int Rc = G.yl >= 1 ? 1 << (G.yl - 1) : 1;      // computed (even) rows, see k_low
     const uint32_t n = 1u << (G.lgL + G.yl);
     size_t smem = (size_t)Rc * G.K * (pl->M > 63 ? 16 : 8) + (size_t)Rc * 8 + (size_t)padded_words(n) * 4;
@@ -580,6 +582,7 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
     A.twf = c->twy_f.as<uint2>(); A.twi = c->twy_i.as<uint2>();
     A.tw_stride = G.s_y;
     A.pcs = c->pcs.as<PrimeC>();
+    A.prof = c->prof_on ? c->profbuf.as<unsigned long long>() : nullptr;
     // (L2 prefetch of MID's A tile / of the next wave's tiles measured slower: C2 MID 131 -> 139 us)
     const uint32_t n = 1u << (U + A.cb);
     const size_t smem = (size_t)padded_words(n) * 4;
@@ -737,6 +740,7 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
     A.pcs = c->pcs.as<PrimeC>();
     A.rows_out = rows; A.M = M; A.minv = (uint32_t)(0xffffffffu / (uint32_t)M); A.W32 = W32;
     A.out = out; A.err = c->flags.as<int>();
+    A.prof = c->prof_on ? c->profbuf.as<unsigned long long>() : nullptr;
     if (!dump && W32 > 0) {
         int rc = ensure_nbias(c, M, G.P, G.L, W32);
         if (rc) return rc;
@@ -953,6 +957,38 @@ int run_pipeline(Ctx* c, const tc_plan_t* pl, int a_bits, int b_bits, int64_t ro
     return TC_OK;
 }
 
+// StageTimings with the reference's meaning from the kernel-class times (ms)
+// and the fused kernels' phase timers (profbuf, see PROF_* in tc_kernels.cuh).
+void fill_stage_times(Ctx* c, float scan, float low, float fwd, float mid, float inv, float fin, float h2d,
+                      float d2h, tc_times_t* t) {
+    unsigned long long pr[PROF_SLOTS] = {0};
+    if (c->profbuf.p && cudaMemcpy(pr, c->profbuf.p, sizeof pr, cudaMemcpyDeviceToHost) != cudaSuccess)
+        (void)cudaGetLastError();
+    auto frac = [](unsigned long long x, unsigned long long y) { return x + y ? (double)x / (double)(x + y) : 0.0; };
+    const double f_dig = frac(pr[PROF_LOW_DIG], pr[PROF_LOW_REST]);
+    const unsigned long long mtot = pr[PROF_MID_FWD] + pr[PROF_MID_PW] + pr[PROF_MID_INV];
+    const double m_f = mtot ? (double)pr[PROF_MID_FWD] / mtot : 0.5, m_p = mtot ? (double)pr[PROF_MID_PW] / mtot : 0.0;
+    const double f_x = frac(pr[PROF_FIN_X], pr[PROF_FIN_POST]);
+    const double f_crt = frac(pr[PROF_FIN_CRT], pr[PROF_FIN_OUT]);
+    t->h2d = h2d * 1e-3;
+    t->d2h = d2h * 1e-3;
+    t->convert = (scan + low * f_dig) * 1e-3;
+    t->ntt_forward = (low * (1 - f_dig) + fwd + mid * m_f) * 1e-3;
+    t->pointwise = mid * m_p * 1e-3;
+    t->ntt_inverse = (mid * (1 - m_f - m_p) + inv + fin * f_x) * 1e-3;
+    t->crt = fin * (1 - f_x) * f_crt * 1e-3;
+    t->recover = fin * (1 - f_x) * (1 - f_crt) * 1e-3;
+    t->gpus = 1;
+}
+
+int prof_begin(Ctx* c) {
+    int rc;
+    if ((rc = c->profbuf.ensure(PROF_SLOTS * 8))) return rc;
+    CK(cudaMemsetAsync(c->profbuf.p, 0, PROF_SLOTS * 8, c->st));
+    c->prof_on = true;
+    return TC_OK;
+}
+
 // ---- Kronecker reductions (tc_split.cuh) ----
 struct SplitDims {
     int64_t da2, db2, rows2;   // inner operand lengths, inner product rows
@@ -1120,7 +1156,7 @@ int tc_ctx_destroy(void* ctx) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->st);
     for (DevBuf* b : {&c->in_a, &c->in_b, &c->grids, &c->twx_f, &c->twx_i, &c->twy_f, &c->twy_i,
-                      &c->pcs, &c->flags, &c->outbuf, &c->dbg, &c->nbias, &c->sp_a, &c->sp_b, &c->sp_out, &c->nbtab}) b->release();
+                      &c->pcs, &c->flags, &c->outbuf, &c->dbg, &c->nbias, &c->sp_a, &c->sp_b, &c->sp_out, &c->nbtab, &c->profbuf}) b->release();
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (auto& ev : c->ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : c->user_ev) if (ev) cudaEventDestroy(ev);
@@ -1195,8 +1231,10 @@ int tc_execute(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32_t b_bits,
         dout = c->outbuf.as<uint32_t>();
     }
     const bool stage_events = times != nullptr || c->profiling;
+    if (times && (rc = prof_begin(c))) return rc;
     rc = split ? split_execute(c, plan, a_bits, b_bits, reinterpret_cast<uint64_t*>(dout), rows, out_cw, stage_events)
                : run_pipeline(c, plan, a_bits, b_bits, rows, 2 * out_cw, dout, false, cc, stage_events);
+    c->prof_on = false;
     if (rc) { cudaStreamSynchronize(c->st); return rc; }
     if (!out_on_device)
         CK(cudaMemcpyAsync(out, dout, (size_t)rows * out_cw * 8, cudaMemcpyDeviceToHost, c->st));
@@ -1210,14 +1248,9 @@ int tc_execute(void* ctx, const tc_plan_t* plan, int32_t a_bits, int32_t b_bits,
         for (int i = 0; i < 6; ++i) c->stage_ms[i] = ms[i];
     }
     if (times) {
-        times->convert = ms[0] * 1e-3;
-        times->ntt_forward = ms[1] * 1e-3;
-        times->pointwise = ms[2] * 1e-3;
-        times->ntt_inverse = ms[3] * 1e-3;
-        times->crt = 0.0;
-        times->recover = (ms[4] + ms[5]) * 1e-3;
+        // enqueue_pipeline's stage events: k_low x2 | forward passes | MID | inverse passes | k_final | D2H
+        fill_stage_times(c, 0.f, ms[0], ms[1], ms[2], ms[3], ms[4], 0.f, out_on_device ? 0.f : ms[5], times);
         times->total = now_s() - t_begin;
-        times->gpus = 1;
     }
     return flag_status(f, err_index);
 }
@@ -1231,7 +1264,7 @@ int tc_multiply(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int32_t 
     if (rc) return rc;
     const double t1 = now_s();
     rc = tc_execute(ctx, plan, a_bits, b_bits, out, rows, out_cw, 0, times, err_index);
-    if (times && rc == TC_OK) { times->convert += t1 - t0; times->total = now_s() - t0; }
+    if (times && rc == TC_OK) { times->h2d += t1 - t0; times->total = now_s() - t0; }
     return rc;
 }
 
@@ -1266,7 +1299,8 @@ int multiply_host_split(Ctx* c, const uint64_t* a, int64_t da, int32_t a_cw, int
     c->a_dev = c->in_a.as<uint64_t>(); c->b_dev = c->in_b.as<uint64_t>();
     c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true;
     int* wf = c->dbg.as<int>();
-    CK(cudaEventRecord(c->ev[0], c->st));
+    if (!c->user_ev[10]) CK(cudaEventCreate(&c->user_ev[10]));
+    CK(cudaEventRecord(c->user_ev[10], c->st));
     CK(cudaMemsetAsync(wf, 0, 16, c->st));
     if ((rc = stage_upload(c, c->in_a.p, a, (size_t)da * a_cw * 8, c->st))) return rc;
     if ((rc = stage_upload(c, c->in_b.p, b, (size_t)db * b_cw * 8, c->st))) return rc;
@@ -1279,25 +1313,33 @@ int multiply_host_split(Ctx* c, const uint64_t* a, int64_t da, int32_t a_cw, int
     int out_cw;
     if ((rc = product_shape(c, da > db ? da : db, rows, cap_words, pinfo, out_cw))) return rc;
     if ((rc = c->outbuf.ensure((size_t)rows * out_cw * 8))) return rc;
-    CK(cudaEventRecord(c->ev[1], c->st));
-    if ((rc = split_execute(c, plan, a_bits, b_bits, c->outbuf.as<uint64_t>(), rows, out_cw, false))) return rc;
-    CK(cudaEventRecord(c->ev[5], c->st));
+    if (!c->user_ev[13]) CK(cudaEventCreate(&c->user_ev[13]));
+    if (!c->user_ev[12]) CK(cudaEventCreate(&c->user_ev[12]));
+    CK(cudaEventRecord(c->user_ev[12], c->st));
+    if (times && (rc = prof_begin(c))) return rc;
+    // stage events (inner pipeline, direct launches) only when stats are asked for
+    rc = split_execute(c, plan, a_bits, b_bits, c->outbuf.as<uint64_t>(), rows, out_cw, times != nullptr);
+    c->prof_on = false;
+    if (rc) return rc;
+    CK(cudaEventRecord(c->user_ev[13], c->st));
     CK(cudaMemcpyAsync(out, c->outbuf.p, (size_t)rows * out_cw * 8, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaEventRecord(c->ev[6], c->st));
+    if (!c->user_ev[11]) CK(cudaEventCreate(&c->user_ev[11]));
+    CK(cudaEventRecord(c->user_ev[11], c->st));
     int f[4];
     if ((rc = read_flags(c, f))) return rc;
     if (times) {
-        float up = 0, mid = 0, down = 0;
-        cudaEventElapsedTime(&up, c->ev[0], c->ev[1]);
-        cudaEventElapsedTime(&mid, c->ev[1], c->ev[5]);
-        cudaEventElapsedTime(&down, c->ev[5], c->ev[6]);
+        // uploads | width scans + packing | inner pipeline stages (ev 0..5) | unpack | download
+        float up = 0, down = 0, ms[5] = {0}, all = 0;
+        cudaEventElapsedTime(&up, c->user_ev[10], c->user_ev[12]);
+        for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&ms[i], c->ev[i], c->ev[i + 1]);
+        cudaEventElapsedTime(&all, c->user_ev[12], c->user_ev[13]);
+        cudaEventElapsedTime(&down, c->user_ev[13], c->user_ev[11]);
         (void)cudaGetLastError();
-        memset(times, 0, sizeof *times);
-        times->convert = up * 1e-3;
-        times->ntt_forward = mid * 1e-3;
-        times->recover = down * 1e-3;
+        float inner = 0;
+        for (int i = 0; i < 5; ++i) inner += ms[i];
+        const float packing = all > inner ? all - inner : 0.f;     // Kronecker pack + unpack kernels
+        fill_stage_times(c, packing, ms[0], ms[1], ms[2], ms[3], ms[4], up, down, times);
         times->total = now_s() - t_begin;
-        times->gpus = 1;
     }
     return flag_status(f, err_index);
 }
@@ -1306,6 +1348,89 @@ int multiply_host_impl(Ctx* c, const uint64_t* a, int64_t da, int32_t a_cw, int3
                        const uint64_t* b, int64_t db, int32_t b_cw, int32_t b_bits,
                        const tc_plan_t* plan, uint64_t* out, int64_t out_capacity_words,
                        tc_product_info_t* pinfo, tc_times_t* times, int64_t* err_index, double t_begin);
+
+// multiply_with_stats: the product as one sequential stream with events
+// between the kernel classes and the fused kernels' phase timers on, so every
+// StageTimings field carries the reference's meaning (tc/multiplier.py:131-166).
+int multiply_host_stats(Ctx* c, const uint64_t* a, int64_t da, int32_t a_cw, int32_t a_bits,
+                        const uint64_t* b, int64_t db, int32_t b_cw, int32_t b_bits,
+                        const tc_plan_t* plan, uint64_t* out, int64_t cap_words,
+                        tc_product_info_t* pinfo, tc_times_t* times, int64_t* err_index, double t_begin) {
+    int rc;
+    if ((rc = validate_plan(plan, da, db))) return rc;
+    const int64_t rows = da + db - 1;
+    CrtConst cc;
+    if ((rc = make_crt_const(plan, da < db ? da : db, &cc))) return rc;
+    if ((rc = c->in_a.ensure((size_t)da * a_cw * 8))) return rc;
+    if ((rc = c->in_b.ensure((size_t)db * b_cw * 8))) return rc;
+    if ((rc = c->dbg.ensure(64))) return rc;
+    if ((rc = c->profbuf.ensure(PROF_SLOTS * 8))) return rc;
+    c->a_dev = c->in_a.as<uint64_t>(); c->b_dev = c->in_b.as<uint64_t>();
+    c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true;
+    int* wf = c->dbg.as<int>();
+    Geometry G;
+    if ((rc = prepare(c, plan, G, true)) || (rc = c->grids.ensure((size_t)2 * G.P * G.S * 4))) return rc;
+    uint32_t* GA = c->grids.as<uint32_t>();
+    uint32_t* GB = GA + (size_t)G.P * G.S;
+    const ShardArgs one = single_gpu();
+    const int nh = (int)G.high.size();
+    cudaEvent_t* ev = c->ev;                    // 7 events: 0..6 (and user slot 0 for the end)
+    CK(cudaEventRecord(ev[0], c->st));
+    CK(cudaMemsetAsync(wf, 0, 16, c->st));
+    if ((rc = stage_upload(c, c->in_a.p, a, (size_t)da * a_cw * 8, c->st))) return rc;
+    if ((rc = stage_upload(c, c->in_b.p, b, (size_t)db * b_cw * 8, c->st))) return rc;
+    CK(cudaEventRecord(ev[1], c->st));
+    k_width<<<(unsigned)((da + 255) / 256), 256, 0, c->st>>>(c->a_dev, da, a_cw, wf);
+    k_width<<<(unsigned)((db + 255) / 256), 256, 0, c->st>>>(c->b_dev, db, b_cw, wf + 2);
+    c->launches += 2;
+    CKL();
+    CK(cudaMemcpyAsync(c->hinfo, wf, 16, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    int out_cw;
+    if ((rc = product_shape(c, da > db ? da : db, rows, cap_words, pinfo, out_cw))) return rc;
+    const int W32 = 2 * out_cw;
+    if ((rc = c->outbuf.ensure((size_t)rows * out_cw * 8))) return rc;
+    if ((rc = ensure_nbias(c, (int)plan->M, G.P, G.L, W32))) return rc;
+    if (plan->M >= 32 && plan->M <= 65 && (plan->M & 31) <= 1 && (rc = ensure_nbtab(c, (int)plan->M, G.P))) return rc;
+    if (!c->user_ev[15]) CK(cudaEventCreate(&c->user_ev[15]));
+    if (!c->user_ev[14]) CK(cudaEventCreate(&c->user_ev[14]));
+    if ((rc = prof_begin(c))) return rc;
+    CK(cudaEventRecord(c->user_ev[14], c->st));          // after the width scans
+    rc = launch_low(c, G, plan, c->a_dev, da, a_cw, a_bits > plan->N, GA, one);
+    if (!rc) rc = launch_low(c, G, plan, c->b_dev, db, b_cw, b_bits > plan->N, GB, one);
+    if (!rc) { CK(cudaEventRecord(ev[2], c->st)); }
+    for (int i = 0; !rc && i < nh; ++i) rc = launch_high(c, MODE_FWD, G, GA, nullptr, G.high[i].first, G.high[i].second, one);
+    for (int i = 0; !rc && i + 1 < nh; ++i) rc = launch_high(c, MODE_FWD, G, GB, nullptr, G.high[i].first, G.high[i].second, one);
+    if (!rc) { CK(cudaEventRecord(ev[3], c->st)); }
+    if (!rc) rc = nh > 0 ? launch_high(c, MODE_MID, G, GB, GA, G.high[nh - 1].first, G.high[nh - 1].second, one)
+                         : launch_high(c, MODE_MID, G, GB, GA, G.lgS, 0, one);
+    if (!rc) { CK(cudaEventRecord(ev[4], c->st)); }
+    for (int i = nh - 2; !rc && i >= 0; --i) rc = launch_high(c, MODE_INV, G, GB, nullptr, G.high[i].first, G.high[i].second, one);
+    if (!rc) { CK(cudaEventRecord(ev[5], c->st)); }
+    if (!rc) rc = launch_final(c, G, GB, rows, (int)plan->M, W32, c->outbuf.as<uint32_t>(), cc, false, one);
+    c->prof_on = false;
+    if (rc) return rc;
+    CK(cudaEventRecord(ev[6], c->st));
+    CK(cudaMemcpyAsync(out, c->outbuf.p, (size_t)rows * out_cw * 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaEventRecord(c->user_ev[15], c->st));
+    int f[4];
+    if ((rc = read_flags(c, f))) return rc;
+    float up = 0, scan = 0, low = 0, fwd = 0, mid = 0, inv = 0, fin = 0, down = 0;
+    cudaEventElapsedTime(&up, ev[0], ev[1]);
+    cudaEventElapsedTime(&scan, ev[1], c->user_ev[14]);
+    cudaEventElapsedTime(&low, c->user_ev[14], ev[2]);
+    cudaEventElapsedTime(&fwd, ev[2], ev[3]);
+    cudaEventElapsedTime(&mid, ev[3], ev[4]);
+    cudaEventElapsedTime(&inv, ev[4], ev[5]);
+    cudaEventElapsedTime(&fin, ev[5], ev[6]);
+    cudaEventElapsedTime(&down, ev[6], c->user_ev[15]);
+    (void)cudaGetLastError();
+    if (times) {
+        fill_stage_times(c, scan, low, fwd, mid, inv, fin, up, down, times);
+        times->total = now_s() - t_begin;
+    }
+    return flag_status(f, err_index);
+}
 
 }  // namespace
 
@@ -1322,8 +1447,12 @@ int tc_multiply_host(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int
     const int rc = plan->split_kind
         ? multiply_host_split(c, a, da, a_cw, a_bits, b, db, b_cw, b_bits, plan, out, out_capacity_words,
                               pinfo, times, err_index, t_begin)
+        : times
+        ? multiply_host_stats(c, a, da, a_cw, a_bits, b, db, b_cw, b_bits, plan, out, out_capacity_words,
+                              pinfo, times, err_index, t_begin)
         : multiply_host_impl(c, a, da, a_cw, a_bits, b, db, b_cw, b_bits, plan, out, out_capacity_words,
                              pinfo, times, err_index, t_begin);
+    if (rc) c->prof_on = false;
     if (rc) {
         // queued copies read the caller's inputs and write its output buffer:
         // none may outlive the call
@@ -1678,7 +1807,7 @@ int tc_host_free(void* hptr) {
 
 int tc_record_event(void* ctx, int32_t slot) {
     Ctx* c = static_cast<Ctx*>(ctx);
-    if (!c || slot < 0 || slot >= 16) return set_err(TC_ERR_BAD_ARG, "bad event slot");
+    if (!c || slot < 0 || slot >= 10) return set_err(TC_ERR_BAD_ARG, "bad event slot (0..9; 10..15 are internal)");
     if (!c->user_ev[slot]) CK(cudaEventCreate(&c->user_ev[slot]));
     CK(cudaEventRecord(c->user_ev[slot], c->st));
     return TC_OK;

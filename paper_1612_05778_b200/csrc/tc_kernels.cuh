@@ -120,6 +120,18 @@ static __global__ void k_twiddles(uint2* fwd, uint2* inv, int64_t n, uint32_t p,
     inv[idx] = make_uint2((uint32_t)wi, (uint32_t)((wi << 32) / p));
 }
 
+// Phase timers for multiply_with_stats (the reference's per-stage times,
+// tc/multiplier.py:131-166, attributed inside the fused kernels): thread 0 of
+// a CTA adds each phase's globaltimer duration to a device counter; `prof`
+// is null on every other launch.
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+enum { PROF_LOW_DIG = 0, PROF_LOW_REST, PROF_MID_FWD, PROF_MID_PW, PROF_MID_INV, PROF_FIN_X, PROF_FIN_CRT,
+       PROF_FIN_OUT, PROF_FIN_POST, PROF_SLOTS = 16 };
+
 __device__ __forceinline__ uint32_t bitrev(uint32_t x, int bits) {
     return bits ? __brev(x) >> (32 - bits) : 0u;
 }
@@ -1040,6 +1052,7 @@ struct LowArgs {
     const uint2* twx; const uint2* twy; int64_t twy_stride;
     const PrimeC* pcs; int P;
     int dual;              // two primes side by side in two tile buffers (host-checked shape)
+    unsigned long long* prof;   // phase timers (PROF_LOW_*), or null
 };
 
 template <int NT>
@@ -1090,6 +1103,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
     // D/2..D ways (measured unstaged: C2 k_low 166 -> 154 us, C3 8.98 -> 8.49
     // ms, C5 203 -> 189 us)
     const bool staged = !wide && (int64_t)Rc * A.src.cw * 8 <= (int64_t)padded_words(n) * 4;
+    uint64_t pt0 = 0;
+    if (A.prof && threadIdx.x == 0) pt0 = gtimer();
     if (!wide) {
         if (staged) compute_digits_staged<int64_t>(A.src, Rc, coeff, dig, ds, reinterpret_cast<uint64_t*>(tile));
         else compute_digits<int64_t>(A.src, Rc, coeff, dig, ds);
@@ -1097,6 +1112,14 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
         if (staged) compute_digits_staged<__int128>(A.src, Rc, coeff, dig2, ds, reinterpret_cast<uint64_t*>(tile));
         else compute_digits<__int128>(A.src, Rc, coeff, dig2, ds);
     }
+    uint64_t pt1 = 0;
+    if (A.prof && threadIdx.x == 0) { pt1 = gtimer(); atomicAdd(&A.prof[PROF_LOW_DIG], (unsigned long long)(pt1 - pt0)); }
+    struct LowTimerTail {      // the rest of the kernel (residues, transforms, stores) on every return path
+        const LowArgs& a; uint64_t t1;
+        __device__ ~LowTimerTail() {
+            if (a.prof && threadIdx.x == 0) atomicAdd(&a.prof[PROF_LOW_REST], (unsigned long long)(gtimer() - t1));
+        }
+    } low_tail{A, pt1};
     // residues of the K digit columns of prime q into tile tb; the top x level
     // (DIF on (x_j, 0) pairs, the theta-twist) is fused here: columns j and
     // j + K get x_j and x_j w_j
@@ -1204,6 +1227,7 @@ struct HighArgs {
     int lgL, lgS, u0, U, cb;
     const uint2* twf; const uint2* twi; int64_t tw_stride;
     const PrimeC* pcs;
+    unsigned long long* prof;   // MODE_MID phase timers (PROF_MID_*), or null
 };
 
 template <int MODE, int NT>
@@ -1239,8 +1263,11 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (NT <= 256 ? TC_HIGH_MINB :
     else tile_load_scalar(s, g, n, hidx);
     __syncthreads();
     const TwHigh tf{A.twf + (int64_t)q * A.tw_stride, A.lgL, A.u0, A.cb, mid << A.cb};
+    const bool prof = MODE == MODE_MID && A.prof && threadIdx.x == 0;
+    uint64_t pt = prof ? gtimer() : 0;
     if (MODE == MODE_FWD || MODE == MODE_MID)
         run_bits<false, (NT == 256 ? 2 : 1)>(s, tile_bits, A.cb, tile_bits, tf, pc.p, pc.two_p);
+    if (prof) { const uint64_t t = gtimer(); atomicAdd(&A.prof[PROF_MID_FWD], (unsigned long long)(t - pt)); pt = t; }
     if (MODE == MODE_MID) {
         const uint32_t* ga = A.other + (int64_t)q * qstride;
         auto pw = [&](uint32_t e, uint32_t y) {
@@ -1270,6 +1297,7 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (NT <= 256 ? TC_HIGH_MINB :
         }
         __syncthreads();
     }
+    if (prof) { const uint64_t t = gtimer(); atomicAdd(&A.prof[PROF_MID_PW], (unsigned long long)(t - pt)); pt = t; }
     if (MODE == MODE_INV || MODE == MODE_MID) {
         TwHigh ti = tf;
         ti.twy = A.twi + (int64_t)q * A.tw_stride;
@@ -1277,6 +1305,7 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (NT <= 256 ? TC_HIGH_MINB :
     }
     if (A.cb >= 2) tile_store(g, s, n, hidx);
     else tile_store_scalar(g, s, n, hidx);
+    if (prof) atomicAdd(&A.prof[PROF_MID_INV], (unsigned long long)(gtimer() - pt));
 }
 
 // ---------------------------------------------------------------------------
@@ -1453,8 +1482,11 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (CB == 3 ? 4 : (NT <= 256 ?
     tile_load<TC_HIGH_BATCH ? TC_HIGH_BATCH : (NT <= 256 ? 8 : 4)>(s, g, n, hidx);
 #endif
     __syncthreads();
+    const bool prof = MODE == MODE_MID && A.prof && threadIdx.x == 0;
+    uint64_t pt = prof ? gtimer() : 0;
     const CtTw tf{stw_f, A.twf + (int64_t)q * A.tw_stride, mid << CB, A.lgL, A.u0};
     if (MODE == MODE_FWD || MODE == MODE_MID) ct_pass<U, false, NT, CB, GTW>(s, tf, pc.p, pc.two_p);
+    if (prof) { const uint64_t t = gtimer(); atomicAdd(&A.prof[PROF_MID_FWD], (unsigned long long)(t - pt)); pt = t; }
     if (MODE == MODE_MID) {
         const uint32_t* ga = A.other + (int64_t)q * qstride;
         constexpr uint32_t nv = n >> 2;
@@ -1484,9 +1516,11 @@ __global__ void __launch_bounds__(NT, NT <= 64 ? 8 : (CB == 3 ? 4 : (NT <= 256 ?
         }
         __syncthreads();
     }
+    if (prof) { const uint64_t t = gtimer(); atomicAdd(&A.prof[PROF_MID_PW], (unsigned long long)(t - pt)); pt = t; }
     const CtTw ti{stw_i, A.twi + (int64_t)q * A.tw_stride, mid << CB, A.lgL, A.u0};
     if (MODE == MODE_INV || MODE == MODE_MID) ct_pass<U, true, NT, CB, GTW>(s, ti, pc.p, pc.two_p);
     tile_store(g, s, n, hidx);
+    if (prof) atomicAdd(&A.prof[PROF_MID_INV], (unsigned long long)(gtimer() - pt));
 }
 
 // ---------------------------------------------------------------------------
@@ -1637,7 +1671,10 @@ k_high_tma(HighArgs A, const __grid_constant__ TmaMap mg, const __grid_constant_
     }
     __syncthreads();
     mbar_wait(&bar[0], 0);
+    const bool prof = MODE == MODE_MID && A.prof && threadIdx.x == 0;
+    uint64_t pt = prof ? gtimer() : 0;
     if (MODE == MODE_FWD || MODE == MODE_MID) dense_pass<U, false, NT>(s, stw_f, pc.p, pc.two_p);
+    if (prof) { const uint64_t t = gtimer(); atomicAdd(&A.prof[PROF_MID_FWD], (unsigned long long)(t - pt)); pt = t; }
     if (MODE == MODE_MID && !AG) {
         mbar_wait(&bar[1], 0);
 #pragma unroll 4
@@ -1678,7 +1715,9 @@ k_high_tma(HighArgs A, const __grid_constant__ TmaMap mg, const __grid_constant_
         }
         __syncthreads();
     }
+    if (prof) { const uint64_t t = gtimer(); atomicAdd(&A.prof[PROF_MID_PW], (unsigned long long)(t - pt)); pt = t; }
     if (MODE == MODE_INV || MODE == MODE_MID) dense_pass<U, true, NT>(s, stw_i, pc.p, pc.two_p);
+    if (prof) atomicAdd(&A.prof[PROF_MID_INV], (unsigned long long)(gtimer() - pt));
     fence_proxy_async();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1812,6 +1851,7 @@ struct FinalArgs {
     int cw_aw, cw_b;               // > 0: warp-group CRT + ConvertOut (crt_convert_warp), M = 32 cw_aw + cw_b
     const uint32_t* nbtab;         // its bias tables: 2 x (32 cw_aw + cw_b) words (first group / later groups)
     int ld4;                       // tile loads: four cp.async per address computation
+    unsigned long long* prof;      // phase timers (PROF_FIN_*), or null
 };
 
 // ---------------------------------------------------------------------------
@@ -2164,7 +2204,12 @@ __device__ __forceinline__ void crt_convert_warp(const FinalArgs& A, const CrtCo
         if (ga > 0) {
             // warm-up: the group before the segment, for its tail pieces and last word
             const int g = ga - 1;
+            const uint64_t kw = A.prof ? clock64() : 0;
             warp_term_pieces<P, B>(A, cc, sm, stride, rowbase, 32 * g + lane, L, prow, false, prv);
+            if (A.prof && lane == 0) {
+                const unsigned long long dk = (unsigned long long)(clock64() - kw);
+                atomicAdd(&A.prof[PROF_FIN_CRT], dk);
+            }
             // last word of group g: lane 31's word AW*31 + AW - 1 (B = 0) or 32 AW (B = 1)
             uint64_t S = 0;
 #pragma unroll
@@ -2180,9 +2225,13 @@ __device__ __forceinline__ void crt_convert_warp(const FinalArgs& A, const CrtCo
             for (int k = 0; k < NPC; ++k) prv[k] = 0u;
         }
         uint32_t c0 = 0, c1 = 1;                          // running carry for segment carry-in 0 / 1
+        uint64_t cyc_crt = 0, cyc_all = 0;
+        const bool prof = A.prof != nullptr;
         for (int g = ga; g < gb; ++g) {
             uint32_t cur[NPC];
+            const uint64_t k0 = prof ? clock64() : 0;
             warp_term_pieces<P, B>(A, cc, sm, stride, rowbase, 32 * g + lane, L, prow, real_row, cur);
+            if (prof) cyc_crt += clock64() - k0;
             const uint32_t* nb = nbt[g == 0 ? 0 : 1];
             // word sums of the owned words: slot s < AW, and (lane 31, B = 1) the extra word
             uint64_t S[NOWN];
@@ -2250,6 +2299,11 @@ __device__ __forceinline__ void crt_convert_warp(const FinalArgs& A, const CrtCo
             }
 #pragma unroll
             for (int k = 0; k < NPC; ++k) prv[k] = cur[k];
+            if (prof) cyc_all += clock64() - k0;
+        }
+        if (prof && lane == 0) {
+            atomicAdd(&A.prof[PROF_FIN_CRT], (unsigned long long)cyc_crt);
+            atomicAdd(&A.prof[PROF_FIN_OUT], (unsigned long long)(cyc_all - cyc_crt));
         }
         segflags = c0 | (c1 << 1);
         seg_w0 = (int64_t)GW * ga;
@@ -2429,6 +2483,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
         if (bitrev(pos0 + r, A.lgS) < A.rows_out) s_any = 1;
     __syncthreads();
     if (!s_any) return;      // every row of this tile is zero padding
+    const uint64_t fin_t0 = (A.prof && threadIdx.x == 0) ? gtimer() : 0;
 
     // all P tiles stream in at once (one cp.async group per prime); prime q's
     // transform waits only for its own tile, later primes' loads overlap it
@@ -2485,6 +2540,20 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
     }
     // grouped ConvertOut staging: a dynamic region after the P tiles (host-sized)
     uint32_t* co_ost = A.co_stage ? sm + P * stride : nullptr;
+    struct FinTimer {          // transforms (ntt_inverse) vs CRT + ConvertOut, by thread 0
+        const FinalArgs& a; uint64_t t1, tc;
+        __device__ ~FinTimer() {
+            if (a.prof && threadIdx.x == 0 && t1) {
+                const uint64_t t = gtimer();
+                atomicAdd(&a.prof[PROF_FIN_POST], (unsigned long long)(t - t1));
+                if (tc) atomicAdd(&a.prof[PROF_FIN_OUT], (unsigned long long)(t - tc));
+            }
+        }
+    } fin_timer{A, 0, 0};
+    if (A.prof && threadIdx.x == 0) {
+        fin_timer.t1 = gtimer();
+        atomicAdd(&A.prof[PROF_FIN_X], (unsigned long long)(fin_timer.t1 - fin_t0));
+    }
 #ifndef TC_CO_FUSED_BUILD
 #define TC_CO_FUSED_BUILD 0     // fused CRT in the grouped path: spills at 64 registers (P >= 5)
 #endif
@@ -2548,6 +2617,10 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
     }
     if (DUMP) return;
     __syncthreads();
+    if (A.prof && threadIdx.x == 0) {         // the in-place CRT pass; the rest is ConvertOut
+        fin_timer.tc = gtimer();
+        atomicAdd(&A.prof[PROF_FIN_CRT], (unsigned long long)(fin_timer.tc - fin_timer.t1));
+    }
     if constexpr (P <= 8) {
         if constexpr (P >= 2)
             if (A.co_aw == 2) { crt_convert_grouped<P, 2, false, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }

@@ -47,13 +47,25 @@ class MulRequest:
 
 @dataclass(frozen=True)
 class StageTimings:
-    """Time per pipeline stage, in seconds (tc/multiplier.py:41-56).
+    """Time per pipeline stage, in seconds (tc/multiplier.py:41-56), with the
+    reference's meaning (tc/multiplier.py:131-166, tc/ntt2d.py:87-125):
 
-    Stages are CUDA-event times of the fused kernels: convert = H2D + ConvertIn
-    fused with the x-direction forward NTT; ntt_forward = forward y passes;
-    pointwise = fused last forward pass + pointwise product + first inverse
-    pass; ntt_inverse = remaining inverse passes; crt = 0 (fused into recover);
-    recover = fused CRT + ConvertOut + D2H.  total is wall clock."""
+      convert      ConvertIn: the balanced digits (k_low's digit phase) and the
+                   device width scans (the reference's min/max scans)
+      ntt_forward  residue embedding + theta twist + forward 2-D transforms
+      pointwise    the pointwise product (with the 1/S scale)
+      ntt_inverse  the inverse 2-D transforms
+      crt          the CRT lift of every slot
+      recover      ConvertOut (shift-add and carries) and the result wrapping
+      total        the whole call, wall clock
+      workers      worker_hint as given (GPUs used: gpus)
+
+    multiply_with_stats runs the product as one sequential CUDA stream with
+    events between the kernels; the kernels that fuse several stages
+    (ConvertIn + forward levels, the forward/pointwise/inverse pass, the
+    inverse levels + CRT + ConvertOut) are split by in-kernel phase timers.
+    The host <-> device copies have no reference counterpart: h2d and d2h,
+    outside stage_sum()."""
 
     convert: float
     ntt_forward: float
@@ -63,6 +75,9 @@ class StageTimings:
     recover: float
     total: float
     workers: int
+    h2d: float = 0.0
+    d2h: float = 0.0
+    gpus: int = 1
 
     def stage_sum(self) -> float:
         return (self.convert + self.ntt_forward + self.pointwise
@@ -106,7 +121,8 @@ def _as_words(p: IntPolynomial) -> np.ndarray:
     return w
 
 
-def _run_pipeline(req: MulRequest, plan_override: dict | None = None, device: int = -1):
+def _run_pipeline(req: MulRequest, plan_override: dict | None = None, device: int = -1,
+                  stats: bool = False):
     """tc_multiply_host: uploads, kernels and the product download overlapped.
 
     The plan is made from the declared bit widths (valid for every operand of
@@ -142,19 +158,21 @@ def _run_pipeline(req: MulRequest, plan_override: dict | None = None, device: in
         rc = lib.tc_multiply_host(ctx.handle, _lib.ptr(aw), da, aw.shape[1], a.bit_width,
                                   _lib.ptr(bw), db, bw.shape[1], b.bit_width,
                                   ctypes.byref(_lib.make_plan(plan, po.get("flags", 0))), _lib.ptr(buf), buf.size,
-                                  ctypes.byref(info), ctypes.byref(times), ctypes.byref(err))
+                                  ctypes.byref(info), ctypes.byref(times) if stats else None, ctypes.byref(err))
     if rc == _lib.TC_ERR_EMPTY:
         raise EmptyInputError("empty input: zero polynomial")
     if rc:
         _raise_status(rc, err.value, plan, a)
+    t_wrap = perf_counter()
     out = buf[: rows * info.out_cw].reshape(rows, info.out_cw)
     result = IntPolynomial._trusted(out, info.out_bits)
     total = perf_counter() - t_begin
-    stats = StageTimings(convert=times.convert, ntt_forward=times.ntt_forward,
-                         pointwise=times.pointwise, ntt_inverse=times.ntt_inverse,
-                         crt=times.crt, recover=times.recover, total=total,
-                         workers=req.worker_hint if req.worker_hint else 1)
-    return result, stats, plan
+    st = StageTimings(convert=times.convert, ntt_forward=times.ntt_forward,
+                      pointwise=times.pointwise, ntt_inverse=times.ntt_inverse,
+                      crt=times.crt, recover=times.recover + (perf_counter() - t_wrap), total=total,
+                      workers=req.worker_hint if req.worker_hint else 1,
+                      h2d=times.h2d, d2h=times.d2h, gpus=max(times.gpus, 1))
+    return result, st, plan
 
 
 def multiply(req: MulRequest) -> IntPolynomial:
@@ -168,8 +186,8 @@ def multiply(req: MulRequest) -> IntPolynomial:
 
 def multiply_with_stats(req: MulRequest) -> tuple:
     """Like multiply, plus time per pipeline stage (tc/multiplier.py:179-181)."""
-    result, stats, _ = _run_pipeline(req)
-    return result, stats
+    result, st, _ = _run_pipeline(req, stats=True)
+    return result, st
 
 
 def multiply_with_plan(req: MulRequest, K: int | None = None, M: int | None = None, split=None):

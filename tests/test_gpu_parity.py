@@ -250,6 +250,16 @@ def test_stats_accounting():
     assert stats.workers == 2
     assert poly == tc.multiply(tc.MulRequest(a, b))
     assert stats.total > 0 and stats.stage_sum() <= stats.total
+    # the reference's stage meaning (tc/multiplier.py:131-166): every stage of
+    # the fused kernels is attributed, transfers reported apart
+    for name in ("convert", "ntt_forward", "pointwise", "ntt_inverse", "crt", "recover", "h2d", "d2h"):
+        assert getattr(stats, name) > 0, (name, stats)
+    assert stats.stage_sum() + stats.h2d + stats.d2h <= stats.total
+    for name in ("C2", "C5"):            # the other k_final paths (warp-group ConvertOut), sizeable stages
+        (aw, ab), (bw, bb) = workloads.make_inputs(name)
+        p, st = tc.multiply_with_stats(tc.MulRequest(tc.IntPolynomial._trusted(aw, ab), tc.IntPolynomial._trusted(bw, bb)))
+        assert st.crt > 0 and st.recover > 0 and st.pointwise > 0 and st.convert > 0, st
+        assert p == tc.multiply(tc.MulRequest(tc.IntPolynomial._trusted(aw, ab), tc.IntPolynomial._trusted(bw, bb)))
 
 
 # ---------------------------------------------------------------- full BASELINE sizes
