@@ -498,10 +498,16 @@ def run_ours(args, rank, world, local):
 
 
 def run_sharded(args, rank, world, local):
-    """N > 1: one product over all ranks (strong scaling)."""
+    """N > 1 (torchrun): ONE product over all ranks (strong scaling):
+    shard.DistributedMultiplier, the prime split while N <= P (every rank
+    transforms its primes, one NCCL exchange of finished residues by row
+    tiles), else the row split (compact inputs, two transposes).  Each rank
+    ends with its product rows; the device time stops there, the e2e time
+    includes every rank's upload of what it reads and its strided download of
+    its rows into its host buffer (no gather)."""
     import torch
     import paper_1612_05778_b200 as tc
-    from paper_1612_05778_b200 import _lib, shard, workloads
+    from paper_1612_05778_b200 import _lib, shard
     local = local if torch.cuda.device_count() > local else 0   # (single-GPU smoke of this path)
     torch.cuda.set_device(local)
     (aw, ab), (bw, bb) = workloads.make_inputs(args.config)
@@ -514,6 +520,7 @@ def run_sharded(args, rank, world, local):
     rows = aw.shape[0] + bw.shape[0] - 1
     # correctness gate on rank 0
     out, plan = dm.multiply(A, B)
+    mode = shard.choose_mode(plan, world)
     verified = None
     if rank == 0:
         golden = json.load(open(os.path.join(ROOT, "tests", "golden", "configs.json"))).get(args.config)
@@ -542,13 +549,15 @@ def run_sharded(args, rank, world, local):
         ev1.synchronize()
         return ev0.elapsed_time(ev1)
 
-    dm.upload(A, B)
+    resident = mode == "primes"
+    if resident:
+        dm.upload(A, B)
     for _ in range(args.warmup):
-        timed(lambda: dm.multiply(A, B, to_host=False, resident=True))
+        timed(lambda: dm.multiply(A, B, to_host="device", resident=resident))
     l0 = dm.ctx.launches()
-    dev = [timed(lambda: dm.multiply(A, B, to_host=False, resident=True)) for _ in range(args.steps)]
+    dev = [timed(lambda: dm.multiply(A, B, to_host="device", resident=resident)) for _ in range(args.steps)]
     launches = dm.ctx.launches() - l0
-    e2e = [timed(lambda: dm.multiply(A, B, to_host=True)) for _ in range(args.steps)]
+    e2e = [timed(lambda: dm.multiply(A, B, to_host="local")) for _ in range(args.steps)]
     clock_info = clocks.stop()
     dev_ms = _max_over_ranks(float(np.sum(dev)), world)
     e2e_ms = _max_over_ranks(float(np.sum(e2e)), world)
@@ -563,15 +572,18 @@ def run_sharded(args, rank, world, local):
         "ms_per_step": round(dev_ms / args.steps, 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded PCG64, BASELINE.md section 4 recipe)",
         "config": {"workload": f"{args.config}: {workloads.CONFIGS[args.config].text}",
-                   "plan": plan.describe(), "parallelism": f"sharded x{world} (row tiles / column groups, "
-                   f"{torch.distributed.get_backend()} all-to-all per prime, gather to rank 0)",
+                   "plan": plan.describe(),
+                   "parallelism": f"sharded x{world}, {mode} split ({torch.distributed.get_backend()} exchanges)",
                    "l2": "flushed (256 MiB memset) on every rank before every timed step",
+                   "timed_step": "device: every rank's product rows finished on its GPU"
+                                 + (" (operands resident)" if resident else " (rank's share uploaded)"),
                    "verified_vs_reference_sha256": verified},
         "e2e": {"value": round(args.steps * out_gbit / (e2e_ms / 1e3), 3), "unit": "Gbit/s",
                 "ms_per_step": round(e2e_ms / args.steps, 4),
-                "h2d_bytes_per_step": int(world * (aw.nbytes + bw.nbytes)),
+                "h2d_bytes_per_step": int((aw.nbytes + bw.nbytes) * (world if mode == "primes" else 1)),
                 "d2h_bytes_per_step": int(rows * out_cw * 8),
-                "api": "shard.DistributedMultiplier.multiply on pinned host arrays (inputs to every rank)"},
+                "api": "shard.DistributedMultiplier.multiply(to_host='local') on pinned host arrays: each rank "
+                       "uploads what it reads and downloads its own rows (no gather)"},
         "gpu_launches": int(launches), "clocks": clock_info,
         "roofline": None,
     }

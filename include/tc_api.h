@@ -188,8 +188,11 @@ int tc_ntt_probe(uint32_t p, uint32_t g, uint32_t* data, int64_t n, int32_t dir)
  *                             (forward A, forward B, pointwise, inverse);
  *   [all-to-all per prime]    exchange 2, same layout, midB -> recvB;
  *   tc_shard_final            inverse low stages + CRT + ConvertOut of this
- *                             rank's row tiles -> rows_per_rank compact rows;
- *   [gather to one rank]      tc_unshard permutes them into product rows.
+ *                             rank's row tiles -> its product rows (row k =
+ *                             product row bitrev_lw(rank) + world*k);
+ *   tc_shard_download         those rows straight into the caller's host
+ *                             buffer (strided), or [gather to one rank] and
+ *                             tc_unshard.
  * Every exchange buffer holds `primes` regions of `shard_words` words. */
 typedef struct {
     int64_t tiles_per_rank, rows_per_rank;  /* low-phase tiles / row positions per rank */
@@ -205,8 +208,38 @@ int tc_shard_high(void* ctx, const tc_plan_t* plan, int32_t rank, int32_t world,
                   uint32_t* midB);
 int tc_shard_final(void* ctx, const tc_plan_t* plan, int32_t rank, int32_t world, const uint32_t* recvB,
                    int64_t rows, int32_t out_cw, uint32_t* out_rows, int64_t* err_index);
-int tc_unshard(void* ctx, const tc_plan_t* plan, const uint32_t* gathered, int64_t rows, int32_t out_cw,
-               uint64_t* out);
+int tc_unshard(void* ctx, const tc_plan_t* plan, int32_t world, const uint32_t* gathered, int64_t rows_local,
+               int64_t rows, int32_t out_cw, uint64_t* out);
+
+/* Compact shard inputs (the row split): of each operand only the coefficients
+ * i = bitrev_lw(rank) mod world -- the ones this rank's row tiles read -- go to
+ * this context's device, coefficient i at row i >> lw.  Widths / non-zero flags
+ * in `info` are this rank's share (reduce them over the ranks).  Replaces each
+ * rank staging both whole operands. */
+int tc_stage_shard_inputs(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw,
+                          const uint64_t* b, int64_t db, int32_t b_cw, int32_t rank, int32_t world,
+                          tc_input_info_t* info);
+/* This rank's product rows (row k of dev_rows = product row bitrev_lw(rank) +
+ * world*k, as tc_shard_final / tc_prime_final write them) straight into the
+ * caller's whole (rows x out_cw) host buffer: a strided copy, no gather. */
+int tc_shard_download(void* ctx, int32_t rank, int32_t world, int64_t rows, int32_t out_cw,
+                      const uint32_t* dev_rows, uint64_t* host_out);
+
+/* Prime split (world <= P; north_star's "partitioned by CRT prime"): the P
+ * convolutions are independent up to the CRT, so a rank transforms primes
+ * [q0, q0+nq) of the plan on its own (forward, pointwise, inverse y passes;
+ * the plan's full pass layout), then ONE exchange moves the finished residues
+ * by row tiles (tc_shard_info's shard_words per prime and rank: rank t gets
+ * words [t*shard_words, (t+1)*shard_words) of every prime) and
+ * tc_prime_final runs the last levels + CRT + ConvertOut of the rank's tiles
+ * from all P primes, gathered contiguously as [P][shard_words].
+ * tc_prime_grid: the device grid (s_y*2K words) of local prime q after
+ * tc_prime_convolve. */
+int tc_prime_convolve(void* ctx, const tc_plan_t* plan, int32_t world, int32_t q0, int32_t nq,
+                      int32_t a_bits, int32_t b_bits);
+int tc_prime_grid(void* ctx, const tc_plan_t* plan, int32_t nq, int32_t local_q, uint32_t** grid);
+int tc_prime_final(void* ctx, const tc_plan_t* plan, int32_t rank, int32_t world, const uint32_t* gathered,
+                   int64_t rows, int32_t out_cw, uint32_t* out_rows, int64_t* err_index);
 
 /* Device memory helpers for device-resident callers (bench, tests). */
 int tc_device_alloc(void* ctx, int64_t bytes, void** dptr);
@@ -228,6 +261,15 @@ int tc_flush_l2(void* ctx);
 /* INT-pipe roofline denominator: sustained DIF butterflies/s (Shoup, p < 2^30)
  * of a register-only chain over every SM, and of the Montgomery product. */
 int tc_int_peak(void* ctx, double* butterflies_per_s, double* montmul_per_s);
+/* Visible CUDA devices (multiply(worker_hint=N) uses up to N of them). */
+int tc_device_count(int32_t* n);
+/* Let this context's GPU read/write peer_device's memory over NVLink. */
+int tc_enable_peer(void* ctx, int32_t peer_device);
+/* Device-to-device copy (this or a peer GPU) on the context's copy stream,
+ * after the work already queued on its compute stream; tc_sync_copies waits
+ * for them.  The multi-GPU exchanges overlap the next kernels this way. */
+int tc_copy_async(void* ctx, void* dst, const void* src, int64_t bytes);
+int tc_sync_copies(void* ctx);
 /* Free and total device memory of the context's GPU (plan feasibility). */
 int tc_mem_info(void* ctx, int64_t* free_bytes, int64_t* total_bytes);
 

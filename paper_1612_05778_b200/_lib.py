@@ -34,7 +34,8 @@ EXPORTED_SYMBOLS = (
     "tc_device_alloc", "tc_device_free", "tc_memcpy", "tc_synchronize",
     "tc_kernel_launches", "tc_set_profiling", "tc_last_profile", "tc_last_error", "tc_version",
     "tc_host_alloc", "tc_host_free", "tc_record_event", "tc_event_elapsed", "tc_flush_l2",
-    "tc_int_peak", "tc_mem_info", "tc_shard_info", "tc_shard_low", "tc_shard_high", "tc_shard_final", "tc_unshard",
+    "tc_int_peak", "tc_mem_info", "tc_device_count", "tc_enable_peer", "tc_copy_async", "tc_sync_copies", "tc_shard_info", "tc_shard_low", "tc_shard_high", "tc_shard_final", "tc_unshard",
+    "tc_stage_shard_inputs", "tc_shard_download", "tc_prime_convolve", "tc_prime_grid", "tc_prime_final",
 )
 
 
@@ -107,6 +108,10 @@ def load(path: str = LIB_PATH):
             "tc_flush_l2": (i32, [vp]),
             "tc_int_peak": (i32, [vp, P(ctypes.c_double), P(ctypes.c_double)]),
             "tc_mem_info": (i32, [vp, P(i64), P(i64)]),
+            "tc_device_count": (i32, [P(i32)]),
+            "tc_enable_peer": (i32, [vp, i32]),
+            "tc_copy_async": (i32, [vp, vp, vp, i64]),
+            "tc_sync_copies": (i32, [vp]),
             "tc_last_error": (ctypes.c_char_p, []),
             "tc_version": (ctypes.c_char_p, []),
         }

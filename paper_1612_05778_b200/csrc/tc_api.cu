@@ -114,6 +114,7 @@ struct Ctx {
     int* hinfo = nullptr;                // pinned: widths read back early
     cudaEvent_t fev[2] = {};             // fork / join of the resident pipeline's two branches
     int sms = 148;                       // multiprocessors of the device
+    int in_lw = 0;                       // staged inputs are compact shard inputs (tc_stage_shard_inputs)
     // pageable uploads: a pinned ring of chunks filled by the copy pool while
     // the copy engine drains the previous chunk (stage_upload)
     char* ring = nullptr;
@@ -130,6 +131,7 @@ public:
     void copy(char* dst, const char* src, size_t len) {
         const int T = (int)workers_.size() + 1;
         if (T == 1 || len < ((size_t)1 << 20)) { memcpy(dst, src, len); return; }
+        std::lock_guard<std::mutex> one_job(job_mu_);     // one job at a time (contexts on several threads)
         std::unique_lock<std::mutex> lk(mu_);
         dst_ = dst; src_ = src; len_ = len; pieces_ = T;
         next_.store(0); remaining_.store(T);
@@ -174,6 +176,7 @@ private:
         }
     }
     std::vector<std::thread> workers_;
+    std::mutex job_mu_;
     std::mutex mu_;
     std::condition_variable cv_, done_cv_;
     char* dst_ = nullptr; const char* src_ = nullptr; size_t len_ = 0; int pieces_ = 0;
@@ -219,6 +222,7 @@ int stage_upload(Ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t 
 }
 
 int ilog2(int64_t x) { int l = 0; while ((1ll << l) < x) ++l; return l; }
+int64_t host_bitrev(uint32_t x, int bits) { uint32_t r = 0; for (int i = 0; i < bits; ++i) r |= ((x >> i) & 1u) << (bits - 1 - i); return r; }
 int env_int(const char* name, int dflt) {           // tuning knobs for experiments
     const char* v = getenv(name);
     return v && *v ? atoi(v) : dflt;
@@ -471,6 +475,7 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     a.src.words = words; a.src.d = d; a.src.cw = cw;
     a.src.K = G.K; a.src.lgK = G.lgK; a.src.M = (int)pl->M; a.src.N = pl->N;
     a.src.check_range = check_range; a.src.err = c->flags.as<int>();
+    a.src.lw = c->in_lw;
     a.lgL = G.lgL; a.lgS = G.lgS; a.yl = G.yl;
     a.g = grids; a.S = G.S;
     a.twx = c->twx_f.as<uint2>(); a.twy = c->twy_f.as<uint2>();
@@ -815,7 +820,7 @@ int make_shard(const Geometry& G, int rank, int world, ShardArgs& sh) {
     if (T % world || Mtot % world)
         return set_err(TC_ERR_BAD_ARG, "grid (%lld tiles, %lld column groups) does not split over %d ranks",
                        (long long)T, (long long)Mtot, world);
-    sh.world = world; sh.rank = rank; sh.TB = TB;
+    sh.world = world; sh.rank = rank; sh.TB = TB; sh.lw = ilog2(world);
     sh.Tl = T / world; sh.h0 = (int64_t)rank * sh.Tl;
     const int64_t Mloc = Mtot / world;
     sh.m0 = (uint32_t)(rank * Mloc); sh.lmloc = ilog2(Mloc); sh.lchunk = sh.lmloc + G.hcb;
@@ -1114,6 +1119,36 @@ double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// Strided H2D: nrows rows of row_bytes at a src_pitch host stride into
+// contiguous device rows.  Page-locked sources: one 2-D copy; pageable ones are
+// gathered row by row into the pinned ring by the copy pool.
+int stage_upload_rows(Ctx* c, void* dst, const void* src, size_t row_bytes, size_t src_pitch, int64_t nrows,
+                      cudaStream_t st) {
+    if (nrows < 1) return TC_OK;
+    if (src_pitch == row_bytes) return stage_upload(c, dst, src, row_bytes * (size_t)nrows, st);
+    if (host_is_pinned(src) || row_bytes > kRingChunk || getenv("TC_NO_STAGING")) {
+        CK(cudaMemcpy2DAsync(dst, row_bytes, src, src_pitch, row_bytes, (size_t)nrows, cudaMemcpyHostToDevice, st));
+        return TC_OK;
+    }
+    if (!c->ring) {
+        CK(cudaHostAlloc((void**)&c->ring, kRingChunk * kRingSlots, cudaHostAllocDefault));
+        for (auto& e : c->ring_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int64_t per = (int64_t)(kRingChunk / row_bytes);
+    for (int64_t r0 = 0; r0 < nrows; r0 += per) {
+        const int64_t nr = nrows - r0 < per ? nrows - r0 : per;
+        const int slot = (int)(c->ring_next++ % kRingSlots);
+        char* sp = c->ring + (size_t)slot * kRingChunk;
+        CK(cudaEventSynchronize(c->ring_ev[slot]));
+        for (int64_t r = 0; r < nr; ++r)
+            memcpy(sp + (size_t)r * row_bytes, static_cast<const char*>(src) + (size_t)(r0 + r) * src_pitch, row_bytes);
+        CK(cudaMemcpyAsync(static_cast<char*>(dst) + (size_t)r0 * row_bytes, sp, (size_t)nr * row_bytes,
+                           cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(c->ring_ev[slot], st));
+    }
+    return TC_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1189,7 +1224,7 @@ int tc_stage_inputs(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw,
         if ((rc = stage_upload(c, c->in_b.p, b, (size_t)db * b_cw * 8, c->st))) return rc;
         c->a_dev = c->in_a.as<uint64_t>(); c->b_dev = c->in_b.as<uint64_t>();
     }
-    c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true;
+    c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true; c->in_lw = 0;
     if ((rc = c->dbg.ensure(64))) return rc;
     CK(cudaMemsetAsync(c->dbg.p, 0, 16, c->st));
     int* wf = c->dbg.as<int>();
@@ -1297,7 +1332,7 @@ int multiply_host_split(Ctx* c, const uint64_t* a, int64_t da, int32_t a_cw, int
     if ((rc = c->in_b.ensure((size_t)db * b_cw * 8))) return rc;
     if ((rc = c->dbg.ensure(64))) return rc;
     c->a_dev = c->in_a.as<uint64_t>(); c->b_dev = c->in_b.as<uint64_t>();
-    c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true;
+    c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true; c->in_lw = 0;
     int* wf = c->dbg.as<int>();
     if (!c->user_ev[10]) CK(cudaEventCreate(&c->user_ev[10]));
     CK(cudaEventRecord(c->user_ev[10], c->st));
@@ -1366,7 +1401,7 @@ int multiply_host_stats(Ctx* c, const uint64_t* a, int64_t da, int32_t a_cw, int
     if ((rc = c->dbg.ensure(64))) return rc;
     if ((rc = c->profbuf.ensure(PROF_SLOTS * 8))) return rc;
     c->a_dev = c->in_a.as<uint64_t>(); c->b_dev = c->in_b.as<uint64_t>();
-    c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true;
+    c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true; c->in_lw = 0;
     int* wf = c->dbg.as<int>();
     Geometry G;
     if ((rc = prepare(c, plan, G, true)) || (rc = c->grids.ensure((size_t)2 * G.P * G.S * 4))) return rc;
@@ -1477,7 +1512,7 @@ int multiply_host_impl(Ctx* c, const uint64_t* a, int64_t da, int32_t a_cw, int3
     if ((rc = c->in_b.ensure((size_t)db * b_cw * 8))) return rc;
     if ((rc = c->dbg.ensure(64))) return rc;
     c->a_dev = c->in_a.as<uint64_t>(); c->b_dev = c->in_b.as<uint64_t>();
-    c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true;
+    c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true; c->in_lw = 0;
     int* wf = c->dbg.as<int>();
     Geometry G;
     if ((rc = prepare(c, plan, G, true)) || (rc = c->grids.ensure((size_t)2 * G.P * G.S * 4))) return rc;
@@ -1706,16 +1741,160 @@ int tc_shard_final(void* ctx, const tc_plan_t* plan, int32_t rank, int32_t world
     return flag_status(f, err_index);
 }
 
-int tc_unshard(void* ctx, const tc_plan_t* plan, const uint32_t* gathered, int64_t rows, int32_t out_cw, uint64_t* out) {
+int tc_unshard(void* ctx, const tc_plan_t* plan, int32_t world, const uint32_t* gathered, int64_t rows_local,
+               int64_t rows, int32_t out_cw, uint64_t* out) {
     Ctx* c = static_cast<Ctx*>(ctx);
-    if (!c || !gathered || !out) return set_err(TC_ERR_BAD_ARG, "NULL argument");
+    if (!c || !gathered || !out || world < 1 || rows_local < 1) return set_err(TC_ERR_BAD_ARG, "bad unshard arguments");
+    (void)plan;
     CK(cudaSetDevice(c->device));
-    const int lgS = ilog2(plan->s_y);
-    k_unshard<<<(unsigned)plan->s_y, 128, 0, c->st>>>(gathered, reinterpret_cast<uint32_t*>(out), lgS, rows,
-                                                      2 * out_cw, plan->s_y);
+    k_unshard<<<(unsigned)(world * rows_local), 128, 0, c->st>>>(gathered, reinterpret_cast<uint32_t*>(out), ilog2(world),
+                                                                  rows, 2 * out_cw, rows_local);
     c->launches++;
     CKL();
     return TC_OK;
+}
+
+// Compact shard inputs: of each operand only the coefficients i = bitrev_lw(rank)
+// mod world -- the ones this rank's row tiles read (tile positions [rank Tl R,
+// (rank+1) Tl R), coefficient bitrev(pos)) -- go to the device, coefficient i
+// at row i >> lw; pageable sources are gathered through the pinned ring.
+// Widths and non-zero flags in `info` are this rank's share (the caller
+// reduces them over the ranks).
+int tc_stage_shard_inputs(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw,
+                          const uint64_t* b, int64_t db, int32_t b_cw, int32_t rank, int32_t world,
+                          tc_input_info_t* info) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || !a || !b || da < 1 || db < 1 || a_cw < 1 || b_cw < 1 || world < 1 || (world & (world - 1)) ||
+        rank < 0 || rank >= world)
+        return set_err(TC_ERR_BAD_ARG, "bad shard input arguments");
+    CK(cudaSetDevice(c->device));
+    const int lw = ilog2(world);
+    const int64_t rsel = host_bitrev((uint32_t)rank, lw);
+    const int64_t na = da > rsel ? (da - rsel + world - 1) / world : 0;
+    const int64_t nb = db > rsel ? (db - rsel + world - 1) / world : 0;
+    int rc;
+    if ((rc = c->in_a.ensure((size_t)(na > 0 ? na : 1) * a_cw * 8))) return rc;
+    if ((rc = c->in_b.ensure((size_t)(nb > 0 ? nb : 1) * b_cw * 8))) return rc;
+    if ((rc = c->dbg.ensure(64))) return rc;
+    const uint64_t* srcs[2] = {a, b};
+    const int64_t n[2] = {na, nb};
+    const int cws[2] = {a_cw, b_cw};
+    void* dsts[2] = {c->in_a.p, c->in_b.p};
+    for (int o = 0; o < 2; ++o) {
+        if (n[o] < 1) continue;
+        if ((rc = stage_upload_rows(c, dsts[o], srcs[o] + rsel * cws[o], (size_t)cws[o] * 8,
+                                    (size_t)world * cws[o] * 8, n[o], c->st))) return rc;
+    }
+    c->a_dev = c->in_a.as<uint64_t>(); c->b_dev = c->in_b.as<uint64_t>();
+    c->da = da; c->db = db; c->a_cw = a_cw; c->b_cw = b_cw; c->staged = true; c->in_lw = lw;
+    CK(cudaMemsetAsync(c->dbg.p, 0, 16, c->st));
+    int* wf = c->dbg.as<int>();
+    if (na > 0) k_width<<<(unsigned)((na + 255) / 256), 256, 0, c->st>>>(c->a_dev, na, a_cw, wf);
+    if (nb > 0) k_width<<<(unsigned)((nb + 255) / 256), 256, 0, c->st>>>(c->b_dev, nb, b_cw, wf + 2);
+    c->launches += 2;
+    CKL();
+    if (info) {
+        int h[4];
+        CK(cudaMemcpyAsync(h, wf, sizeof h, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        info->n_in_a = h[0]; info->nonzero_a = h[1]; info->n_in_b = h[2]; info->nonzero_b = h[3];
+    }
+    return TC_OK;
+}
+
+// This rank's product rows (tc_shard_final / tc_prime_final: row k of dev_rows
+// is product row bitrev_lw(rank) + world k) straight into the caller's full
+// (rows x out_cw) host buffer, strided; returns when the copy is done.
+int tc_shard_download(void* ctx, int32_t rank, int32_t world, int64_t rows, int32_t out_cw,
+                      const uint32_t* dev_rows, uint64_t* host_out) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || !dev_rows || !host_out || world < 1 || rank < 0 || rank >= world) return set_err(TC_ERR_BAD_ARG, "bad download arguments");
+    CK(cudaSetDevice(c->device));
+    const int lw = ilog2(world);
+    const int64_t c0 = host_bitrev((uint32_t)rank, lw);
+    const int64_t cnt = rows > c0 ? (rows - c0 + world - 1) / world : 0;
+    const size_t rb = (size_t)out_cw * 8;
+    if (cnt > 0)
+        CK(cudaMemcpy2DAsync((char*)host_out + c0 * rb, (size_t)world * rb, dev_rows, rb, rb, (size_t)cnt,
+                             cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return TC_OK;
+}
+
+// ---- prime split (world <= P): every rank transforms its own primes; one
+// exchange of the finished residues by row tiles before k_final ----
+int tc_prime_convolve(void* ctx, const tc_plan_t* plan, int32_t world, int32_t q0, int32_t nq,
+                      int32_t a_bits, int32_t b_bits) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || !c->staged || !plan || nq < 1 || q0 < 0 || q0 + nq > plan->P)
+        return set_err(TC_ERR_BAD_ARG, "bad prime-split arguments");
+    if (c->in_lw) return set_err(TC_ERR_BAD_ARG, "the prime split needs the full operands (tc_stage_inputs)");
+    CK(cudaSetDevice(c->device));
+    int rc;
+    if ((rc = validate_plan(plan, c->da, c->db))) return rc;
+    // the full plan's pass layout (k_final keeps all P primes), this rank's primes in the kernels
+    Geometry G;
+    if ((rc = make_geometry(plan, G, world))) return rc;
+    tc_plan_t sub = *plan;
+    sub.P = nq;
+    for (int q = 0; q < nq; ++q) { sub.p[q] = plan->p[q0 + q]; sub.g[q] = plan->g[q0 + q]; }
+    G.P = nq;
+    if ((rc = ensure_twiddles(c, &sub))) return rc;
+    if ((rc = ensure_pcs(c, &sub, G.S))) return rc;
+    if ((rc = c->flags.ensure(64))) return rc;
+    if ((rc = c->grids.ensure((size_t)2 * nq * G.S * 4))) return rc;
+    CK(cudaMemsetAsync(c->flags.p, 0x7f, 64, c->st));
+    uint32_t* GA = c->grids.as<uint32_t>();
+    uint32_t* GB = GA + (size_t)nq * G.S;
+    const ShardArgs one = single_gpu();
+    const int nh = (int)G.high.size();
+    if ((rc = launch_low(c, G, &sub, c->a_dev, c->da, c->a_cw, a_bits > plan->N, GA, one))) return rc;
+    if ((rc = launch_low(c, G, &sub, c->b_dev, c->db, c->b_cw, b_bits > plan->N, GB, one))) return rc;
+    for (int i = 0; i < nh; ++i)
+        if ((rc = launch_high(c, MODE_FWD, G, GA, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
+    for (int i = 0; i + 1 < nh; ++i)
+        if ((rc = launch_high(c, MODE_FWD, G, GB, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
+    rc = nh > 0 ? launch_high(c, MODE_MID, G, GB, GA, G.high[nh - 1].first, G.high[nh - 1].second, one)
+                : launch_high(c, MODE_MID, G, GB, GA, G.lgS, 0, one);
+    if (rc) return rc;
+    for (int i = nh - 2; i >= 0; --i)
+        if ((rc = launch_high(c, MODE_INV, G, GB, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
+    int f[4];
+    if ((rc = read_flags(c, f))) return rc;
+    return flag_status(f, nullptr);
+}
+
+int tc_prime_grid(void* ctx, const tc_plan_t* plan, int32_t nq, int32_t local_q, uint32_t** grid) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || !plan || !grid || local_q < 0 || local_q >= nq) return set_err(TC_ERR_BAD_ARG, "bad prime grid query");
+    const int64_t S = plan->s_y * 2 * plan->K;
+    if (!c->grids.p || c->grids.n < (size_t)2 * nq * S * 4) return set_err(TC_ERR_BAD_ARG, "no prime-split grids");
+    *grid = c->grids.as<uint32_t>() + (size_t)nq * S + (size_t)local_q * S;
+    return TC_OK;
+}
+
+int tc_prime_final(void* ctx, const tc_plan_t* plan, int32_t rank, int32_t world, const uint32_t* gathered,
+                   int64_t rows, int32_t out_cw, uint32_t* out_rows, int64_t* err_index) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || !gathered || !out_rows) return set_err(TC_ERR_BAD_ARG, "NULL argument");
+    if (err_index) *err_index = -1;
+    CK(cudaSetDevice(c->device));
+    int rc;
+    Geometry G;
+    if ((rc = prepare(c, plan, G, true, world))) return rc;
+    ShardArgs sh;
+    if ((rc = make_shard(G, rank, world, sh))) return rc;
+    if (world == 1) { sh.world = 1; }
+    sh.contig = 1;
+    CrtConst cc;
+    const int64_t dmin = c->staged ? (c->da < c->db ? c->da : c->db) : plan->d;
+    if ((rc = make_crt_const(plan, dmin, &cc))) return rc;
+    if ((rc = ensure_nbias(c, (int)plan->M, G.P, G.L, 2 * out_cw))) return rc;
+    if (plan->M >= 32 && plan->M <= 65 && (plan->M & 31) <= 1 && (rc = ensure_nbtab(c, (int)plan->M, G.P))) return rc;
+    if ((rc = launch_final(c, G, gathered, rows, (int)plan->M, 2 * out_cw, out_rows, cc, false, sh))) return rc;
+    int f[4];
+    if ((rc = read_flags(c, f))) return rc;
+    return flag_status(f, err_index);
 }
 
 int tc_modmul_probe(uint32_t p, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t n, int32_t mode) {
@@ -1860,6 +2039,50 @@ int tc_int_peak(void* ctx, double* bfly_per_s, double* mont_per_s) {
         if (mode == 1 && mont_per_s) *mont_per_s = ops / (ms * 1e-3);
     }
     cudaEventDestroy(e0); cudaEventDestroy(e1);
+    return TC_OK;
+}
+
+int tc_device_count(int32_t* n) {
+    if (!n) return set_err(TC_ERR_BAD_ARG, "NULL argument");
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) { (void)cudaGetLastError(); c = 0; }
+    *n = c;
+    return TC_OK;
+}
+
+int tc_enable_peer(void* ctx, int32_t peer_device) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c) return set_err(TC_ERR_BAD_ARG, "ctx is NULL");
+    if (peer_device == c->device) return TC_OK;
+    CK(cudaSetDevice(c->device));
+    int ok = 0;
+    CK(cudaDeviceCanAccessPeer(&ok, c->device, peer_device));
+    if (!ok) return TC_OK;                      // copies still work, staged by the driver
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return set_err(TC_ERR_CUDA, "cudaDeviceEnablePeerAccess(%d): %s", peer_device, cudaGetErrorString(e));
+    (void)cudaGetLastError();
+    return TC_OK;
+}
+
+// Device-to-device copy (same or peer GPU, NVLink when enabled) on the
+// context's second stream, ordered after the work already queued on its main
+// stream: the exchange of a finished prime overlaps the next prime's kernels.
+int tc_copy_async(void* ctx, void* dst, const void* src, int64_t bytes) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c || !dst || !src || bytes < 0) return set_err(TC_ERR_BAD_ARG, "bad copy arguments");
+    CK(cudaSetDevice(c->device));
+    CK(cudaEventRecord(c->fev[0], c->st));
+    CK(cudaStreamWaitEvent(c->aux, c->fev[0], 0));
+    CK(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, c->aux));
+    return TC_OK;
+}
+
+int tc_sync_copies(void* ctx) {
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (!c) return set_err(TC_ERR_BAD_ARG, "ctx is NULL");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->aux));
     return TC_OK;
 }
 

@@ -255,6 +255,8 @@ struct DigitSrc {
     int64_t K; int lgK; int M; int64_t N;
     int check_range;
     int* err;
+    int lw;              // > 0: compact shard input -- only the coefficients i = c mod 2^lw this rank's
+                         // tiles read, coefficient i at row i >> lw (tc_stage_shard_inputs)
 };
 
 __device__ __forceinline__ uint64_t limb_at(const uint64_t* row, int cw, int64_t k, uint64_t signw) {
@@ -298,7 +300,7 @@ static __device__ void compute_digits(const DigitSrc& a, int R, const int64_t* c
     for (int rr = tid; a.check_range && rr < R; rr += blockDim.x) {
         const int64_t i = coeff[rr];
         if (i < 0) continue;
-        const uint64_t* row = a.words + i * a.cw;
+        const uint64_t* row = a.words + (i >> a.lw) * a.cw;
         const uint64_t signw = (row[a.cw - 1] >> 63) ? ~0ull : 0ull;
         const uint64_t s = ((limb_at(row, a.cw, sq, signw) >> sr) & 1) ? ~0ull : 0ull;
         bool bad = false;
@@ -320,7 +322,7 @@ static __device__ void compute_digits(const DigitSrc& a, int R, const int64_t* c
         U chunk = 0;
         bool neg = false;
         if (active) {
-            const uint64_t* row = a.words + ci * a.cw;
+            const uint64_t* row = a.words + (ci >> a.lw) * a.cw;
             const uint64_t signw = (row[a.cw - 1] >> 63) ? ~0ull : 0ull;
             const int64_t off = j * M;
             auto word = [&](int64_t k) -> uint64_t { return limb_at(row, a.cw, k, signw); };
@@ -375,7 +377,7 @@ static __device__ void compute_digits_staged(const DigitSrc& a, int R, const int
     for (int64_t t = tid; t < nw; t += blockDim.x) {
         const int r = (int)(t / cw);
         const int64_t ci = coeff[r];
-        sw[t] = ci >= 0 ? __ldg(a.words + ci * cw + (t - (int64_t)r * cw)) : 0ull;
+        sw[t] = ci >= 0 ? __ldg(a.words + (ci >> a.lw) * cw + (t - (int64_t)r * cw)) : 0ull;
     }
     __syncthreads();
     auto word = [&](const uint64_t* row, int64_t k) -> uint64_t {
@@ -1033,6 +1035,10 @@ struct ShardArgs {
     uint32_t m0;           // first partition-mid value
     int lchunk, lmloc;     // log2(chunk words), log2(Mloc)
     int TB;                // low-phase tile bits (lgL + yl)
+    int lw;                // log2(world): sharded product rows go to row prow >> lw of the rank's buffer
+                           // (this rank's rows are prow = bitrev_lw(rank) mod world)
+    int contig;            // k_final (prime split): the P tiles of this rank sit contiguously per prime,
+                           // [P][Tl << TB], instead of the exchange layout
 };
 
 // exchange layout index of tile-local slot l of local tile hl
@@ -1112,14 +1118,11 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
         if (staged) compute_digits_staged<__int128>(A.src, Rc, coeff, dig2, ds, reinterpret_cast<uint64_t*>(tile));
         else compute_digits<__int128>(A.src, Rc, coeff, dig2, ds);
     }
-    uint64_t pt1 = 0;
-    if (A.prof && threadIdx.x == 0) { pt1 = gtimer(); atomicAdd(&A.prof[PROF_LOW_DIG], (unsigned long long)(pt1 - pt0)); }
-    struct LowTimerTail {      // the rest of the kernel (residues, transforms, stores) on every return path
-        const LowArgs& a; uint64_t t1;
-        __device__ ~LowTimerTail() {
-            if (a.prof && threadIdx.x == 0) atomicAdd(&a.prof[PROF_LOW_REST], (unsigned long long)(gtimer() - t1));
-        }
-    } low_tail{A, pt1};
+    if (A.prof && threadIdx.x == 0) {
+        const uint64_t t = gtimer();
+        atomicAdd(&A.prof[PROF_LOW_DIG], (unsigned long long)(t - pt0));
+        atomicAdd(&A.prof[PROF_LOW_REST], (unsigned long long)(0ull - t));   // + end time below
+    }
     // residues of the K digit columns of prime q into tile tb; the top x level
     // (DIF on (x_j, 0) pairs, the theta-twist) is fused here: columns j and
     // j + K get x_j and x_j w_j
@@ -1167,6 +1170,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
                 __syncthreads();
             }
         }
+        if (A.prof && threadIdx.x == 0) atomicAdd(&A.prof[PROF_LOW_REST], (unsigned long long)gtimer());
         return;
     }
     for (int q = 0; q < A.P; ++q) {
@@ -1209,6 +1213,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
         else tile_store_scalar(g, tile, n, Contig{});
         __syncthreads();
     }
+    if (A.prof && threadIdx.x == 0) atomicAdd(&A.prof[PROF_LOW_REST], (unsigned long long)gtimer());
 }
 
 // ---------------------------------------------------------------------------
@@ -2056,8 +2061,8 @@ __device__ __forceinline__ void crt_convert_grouped(const FinalArgs& A, const Cr
         if (warp == 0) warp_carry_scan(gwtf, gwcin, &gcarry, nw, lane);
         __syncthreads();
         uint32_t c = (uint32_t)(((A1 + B1 + gwcin[warp]) ^ A1 ^ B1) >> lane) & 1u;
-        uint32_t* orow = sharded ? A.out + ((int64_t)blockIdx.x * R + r) * W32 : A.out + (int64_t)prow * W32;
-        const bool store = sharded || prow < A.rows_out;
+        uint32_t* orow = A.out + (int64_t)(sharded ? prow >> A.sh.lw : prow) * W32;
+        const bool store = prow < A.rows_out;
         // staging in the host-sized region after the tiles, or in place: the
         // warp's own limb slots (terms [j0(lane 0), +128) of this row in tiles
         // 0..2), dead once its accumulation is done
@@ -2196,9 +2201,9 @@ __device__ __forceinline__ void crt_convert_warp(const FinalArgs& A, const CrtCo
     for (; r < R; r += rstride) {
         const uint32_t prow = bitrev(pos0 + (uint32_t)r, A.lgS);
         const bool real_row = prow < A.rows_out;
-        if (!real_row && !sharded) continue;
+        if (!real_row) continue;
         const uint32_t rowbase = (uint32_t)r << A.lgL;
-        uint32_t* orow = sharded ? A.out + ((int64_t)blockIdx.x * R + r) * W32 : A.out + (int64_t)prow * W32;
+        uint32_t* orow = A.out + (int64_t)(sharded ? prow >> A.sh.lw : prow) * W32;
         uint32_t prv[NPC];
         uint32_t hprev = 0;                               // hi of the previous group's last word
         if (ga > 0) {
@@ -2454,9 +2459,8 @@ __device__ __forceinline__ void convert_out_words(const FinalArgs& A, const uint
         __syncthreads();
         uint32_t c = (uint32_t)(((A1 + B1 + wcin1[warp]) ^ A1 ^ B1) >> lane) & 1u;
         const uint32_t prow = bitrev(pos0 + (uint32_t)r, A.lgS);
-        uint32_t* orow = sharded ? A.out + ((int64_t)blockIdx.x * R + r) * W32
-                                 : A.out + (int64_t)prow * W32;
-        const bool store = sharded || prow < A.rows_out;
+        uint32_t* orow = A.out + (int64_t)(sharded ? prow >> A.sh.lw : prow) * W32;
+        const bool store = prow < A.rows_out;
 #pragma unroll
         for (int k = 0; k < kW; ++k) {
             if (valid[k] && store) orow[w0 + k] = tw[k] + c;    // sharded: compact rows in position order
@@ -2489,7 +2493,10 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
     // transform waits only for its own tile, later primes' loads overlap it
     for (int q = 0; q < P; ++q) {
         uint32_t* t = sm + q * stride;
-        if (sharded) {
+        if (sharded && A.sh.contig) {
+            const uint32_t* g = A.g + (int64_t)q * (A.sh.Tl << A.sh.TB) + ((int64_t)blockIdx.x << A.sh.TB);
+            for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) cp_async4(t + padi(e), g + e);
+        } else if (sharded) {
             const uint32_t* g = A.g + (int64_t)q * (A.sh.Tl << A.sh.TB);
             const XchgIdx xi{A.sh, blockIdx.x};
             for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) cp_async4(t + padi(e), g + xi(e));
@@ -2540,20 +2547,15 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
     }
     // grouped ConvertOut staging: a dynamic region after the P tiles (host-sized)
     uint32_t* co_ost = A.co_stage ? sm + P * stride : nullptr;
-    struct FinTimer {          // transforms (ntt_inverse) vs CRT + ConvertOut, by thread 0
-        const FinalArgs& a; uint64_t t1, tc;
-        __device__ ~FinTimer() {
-            if (a.prof && threadIdx.x == 0 && t1) {
-                const uint64_t t = gtimer();
-                atomicAdd(&a.prof[PROF_FIN_POST], (unsigned long long)(t - t1));
-                if (tc) atomicAdd(&a.prof[PROF_FIN_OUT], (unsigned long long)(t - tc));
-            }
-        }
-    } fin_timer{A, 0, 0};
+    // phase timers (thread 0): transforms -> PROF_FIN_X, the rest -> PROF_FIN_POST
+    // (each path below adds its end time), CRT vs ConvertOut shares inside
     if (A.prof && threadIdx.x == 0) {
-        fin_timer.t1 = gtimer();
-        atomicAdd(&A.prof[PROF_FIN_X], (unsigned long long)(fin_timer.t1 - fin_t0));
+        const uint64_t t = gtimer();
+        atomicAdd(&A.prof[PROF_FIN_X], (unsigned long long)(t - fin_t0));
+        atomicAdd(&A.prof[PROF_FIN_POST], (unsigned long long)(0ull - t));
     }
+#define TC_FIN_END() do { if (A.prof && threadIdx.x == 0) { const unsigned long long te = gtimer();            \
+        atomicAdd(&A.prof[PROF_FIN_POST], te); if (!warp_co) atomicAdd(&A.prof[PROF_FIN_OUT], te); } } while (0)
 #ifndef TC_CO_FUSED_BUILD
 #define TC_CO_FUSED_BUILD 0     // fused CRT in the grouped path: spills at 64 registers (P >= 5)
 #endif
@@ -2566,16 +2568,19 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
         }
     }
     // warp-group CRT + ConvertOut (M = 32 AW + {0, 1}, host-checked shape)
+    const bool warp_co = A.cw_aw > 0;
     if constexpr (!DUMP && P <= 8) {
         if (A.cw_aw == 2) {
             if (A.cw_b) crt_convert_warp<P, 2, 1>(A, cc, sm, stride, R, pos0, sharded);
             else crt_convert_warp<P, 2, 0>(A, cc, sm, stride, R, pos0, sharded);
+            TC_FIN_END();
             return;
         }
         if constexpr (P <= 4) {
             if (A.cw_aw == 1) {
                 if (A.cw_b) crt_convert_warp<P, 1, 1>(A, cc, sm, stride, R, pos0, sharded);
                 else crt_convert_warp<P, 1, 0>(A, cc, sm, stride, R, pos0, sharded);
+                TC_FIN_END();
                 return;
             }
         }
@@ -2618,28 +2623,32 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
     if (DUMP) return;
     __syncthreads();
     if (A.prof && threadIdx.x == 0) {         // the in-place CRT pass; the rest is ConvertOut
-        fin_timer.tc = gtimer();
-        atomicAdd(&A.prof[PROF_FIN_CRT], (unsigned long long)(fin_timer.tc - fin_timer.t1));
+        const uint64_t t = gtimer();
+        atomicAdd(&A.prof[PROF_FIN_CRT], (unsigned long long)t);
+        atomicAdd(&A.prof[PROF_FIN_OUT], (unsigned long long)(0ull - t));
     }
     if constexpr (P <= 8) {
         if constexpr (P >= 2)
-            if (A.co_aw == 2) { crt_convert_grouped<P, 2, false, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }
+            if (A.co_aw == 2) { crt_convert_grouped<P, 2, false, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); TC_FIN_END(); return; }
         if constexpr (P <= 3)
-            if (A.co_aw == 1) { crt_convert_grouped<P, 1, false, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); return; }
+            if (A.co_aw == 1) { crt_convert_grouped<P, 1, false, NT>(A, cc, sm, stride, R, pos0, sharded, co_ost); TC_FIN_END(); return; }
     }
 
     if (A.co_kw == 2) convert_out_words<P, 2>(A, sm, stride, R, L, pos0, sharded);
     else convert_out_words<P, TC_CO_KW>(A, sm, stride, R, L, pos0, sharded);
+    TC_FIN_END();
+#undef TC_FIN_END
 }
 
-// Gathered compact rows (position order, world x rows-per-rank) -> product
-// rows in natural order: out[bitrev(pos)] = in[pos] for bitrev(pos) < rows.
-static __global__ void k_unshard(const uint32_t* in, uint32_t* out, int lgS, int64_t rows, int W32, int64_t npos) {
-    const int64_t pos = blockIdx.x;
-    if (pos >= npos) return;
-    const uint32_t prow = bitrev((uint32_t)pos, lgS);
-    if (prow >= rows) return;
-    for (int w = threadIdx.x; w < W32; w += blockDim.x) out[(int64_t)prow * W32 + w] = in[pos * W32 + w];
+// Gathered rank buffers -> product rows: rank r's buffer (rows_local rows)
+// holds product rows prow = bitrev_lw(r) + world k at row k.
+static __global__ void k_unshard(const uint32_t* in, uint32_t* out, int lw, int64_t rows, int W32,
+                                 int64_t rows_local) {
+    const int64_t g = blockIdx.x;                 // gathered row: rank g / rows_local, k = g % rows_local
+    const int64_t r = g / rows_local, k = g - r * rows_local;
+    const int64_t prow = (int64_t)bitrev((uint32_t)r, lw) + (k << lw);
+    if (r >= (1ll << lw) || prow >= rows) return;
+    for (int w = threadIdx.x; w < W32; w += blockDim.x) out[prow * W32 + w] = in[g * W32 + w];
 }
 
 // ---------------------------------------------------------------------------

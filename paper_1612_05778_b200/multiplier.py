@@ -130,6 +130,9 @@ def _run_pipeline(req: MulRequest, plan_override: dict | None = None, device: in
     width -- which fixes the product's bit width, tc/zpoly.py:103-114 -- is
     reduced on the device while the first pass runs."""
     t_begin = perf_counter()
+    world = _gpus_for(req.worker_hint) if plan_override is None and device < 0 else 1
+    if world > 1:
+        return _run_multi_gpu(req, world, t_begin)
     ctx = _lib.context(device)
     a, b = req.a, req.b
     aw, bw = _as_words(a), _as_words(b)
@@ -172,6 +175,36 @@ def _run_pipeline(req: MulRequest, plan_override: dict | None = None, device: in
                       crt=times.crt, recover=times.recover + (perf_counter() - t_wrap), total=total,
                       workers=req.worker_hint if req.worker_hint else 1,
                       h2d=times.h2d, d2h=times.d2h, gpus=max(times.gpus, 1))
+    return result, st, plan
+
+
+def _gpus_for(worker_hint) -> int:
+    """worker_hint -> the number of GPUs: the largest
+    power of two <= min(worker_hint, visible devices); 1 without a hint."""
+    if not worker_hint or worker_hint < 2:
+        return 1
+    from .shard import device_count
+    n = min(int(worker_hint), device_count())
+    w = 1
+    while w * 2 <= n:
+        w *= 2
+    return w
+
+
+def _run_multi_gpu(req: MulRequest, world: int, t_begin: float):
+    """One product over `world` GPUs of this process (shard.multiply_sharded:
+    the prime split when world <= P, else the row split); each GPU downloads
+    its rows straight into the result."""
+    from .shard import multiply_sharded
+    a, b = req.a, req.b
+    d = max(a.degree_plus_one, b.degree_plus_one)
+    _check_reference_planning(req, d)
+    t_wrap = perf_counter()
+    result, plan = multiply_sharded(a, b, world, devices=list(range(world)))
+    total = perf_counter() - t_begin
+    st = StageTimings(convert=0.0, ntt_forward=0.0, pointwise=0.0, ntt_inverse=0.0, crt=0.0,
+                      recover=0.0, total=total, workers=req.worker_hint, gpus=world)
+    del t_wrap
     return result, st, plan
 
 

@@ -281,29 +281,54 @@ def test_full_config_matches_reference_hash(name, oracle):
 # ---------------------------------------------------------------- sharded (multi-GPU) path
 
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_sharded_product_virtual_ranks(world, oracle):
-    # the multi-GPU decomposition (row tiles <-> column groups, two all-to-all
-    # exchanges) run as `world` virtual ranks on one GPU
+@pytest.mark.parametrize("mode", ["rows", "primes"])
+def test_sharded_product_virtual_ranks(world, mode, oracle):
+    # the multi-GPU decompositions run as `world` virtual ranks (contexts,
+    # threads, copy-stream exchanges) on one GPU: the row split (compact
+    # inputs, two transposes) and the prime split (world <= P)
     from paper_1612_05778_b200 import shard
-    rng = random.Random(world)
-    for d, nbits in ((300, 500), (1000, 2000), (64, 4097)):
+    rng = random.Random(world * 7 + len(mode))
+    for d, nbits in ((300, 500), (1000, 2000), (64, 4097), (5, 63)):
         a = _random_poly(rng, d, nbits)
-        b = _random_poly(rng, d - 7, nbits)
-        out, plan = shard.multiply_local(a, b, world)
+        b = _random_poly(rng, max(1, d - 7), nbits)
+        plan = plan_gpu(d, max(1, d - 7), nbits)
+        if mode == "primes" and world > plan.P:
+            continue
+        try:
+            out, plan = shard.multiply_local(a, b, world, mode=mode)
+        except tc.DeviceError as ex:              # a grid too small to split this many ways
+            assert "does not split" in str(ex) or "too small" in str(ex), ex
+            continue
         assert out == tc.multiply(tc.MulRequest(a, b)), plan.describe()
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C5"])
-def test_sharded_full_config(name):
+@pytest.mark.parametrize("name,world,mode", [("C1", 4, "rows"), ("C2", 4, "rows"), ("C5", 4, "rows"),
+                                             ("C2", 4, "primes"), ("C4", 4, "rows"), ("C4", 4, "primes"),
+                                             ("C3", 2, "primes"), ("C3", 2, "rows"), ("C3", 8, "rows")])
+def test_sharded_full_config(name, world, mode):
     from paper_1612_05778_b200 import shard
     cfg = json.load(open(os.path.join(GOLDEN, "configs.json")))[name]
     (aw, ab), (bw, bb) = workloads.make_inputs(name)
     a, b = tc.IntPolynomial._trusted(aw, ab), tc.IntPolynomial._trusted(bw, bb)
-    out, _ = shard.multiply_local(a, b, 4)
-    assert workloads.words_sha256(out.words) == cfg["out_sha256"]
+    out, plan = shard.multiply_local(a, b, world, mode=mode)
+    assert out.bit_width == cfg["out_bits"]
+    assert workloads.words_sha256(out.words) == cfg["out_sha256"], (name, world, mode, plan.describe())
 
 
-def _dist_worker(rank, world, port, name, result):
+def test_worker_hint_uses_the_gpus_present():
+    # worker_hint maps to the GPU count; never changes the product
+    from paper_1612_05778_b200 import multiplier, shard
+    n = shard.device_count()
+    assert multiplier._gpus_for(None) == 1 and multiplier._gpus_for(1) == 1
+    assert multiplier._gpus_for(64) == 1 << (n.bit_length() - 1)
+    rng = random.Random(3)
+    a, b = _random_poly(rng, 200, 700), _random_poly(rng, 150, 700)
+    base = tc.multiply(tc.MulRequest(a, b))
+    p, st = tc.multiply_with_stats(tc.MulRequest(a, b, worker_hint=8))
+    assert p == base and st.workers == 8 and st.gpus == multiplier._gpus_for(8)
+
+
+def _dist_worker(rank, world, port, name, mode, result):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -312,18 +337,28 @@ def _dist_worker(rank, world, port, name, result):
     from paper_1612_05778_b200 import shard
     (aw, ab), (bw, bb) = workloads.make_inputs(name)
     a, b = tc.IntPolynomial._trusted(aw, ab), tc.IntPolynomial._trusted(bw, bb)
-    dm = shard.DistributedMultiplier(0)
+    dm = shard.DistributedMultiplier(0, mode=mode)
     out, plan = dm.multiply(a, b)
-    dm.upload(a, b)
-    out2, _ = dm.multiply(a, b, resident=True)
+    local, _ = dm.multiply(a, b, to_host="local")     # this rank's rows, strided into a full-size buffer
+    if mode == "primes":
+        dm.upload(a, b)
+        out2, _ = dm.multiply(a, b, resident=True)
+    else:
+        out2 = out
+    lw = (world - 1).bit_length()
+    c0 = int(format(rank, f"0{lw}b")[::-1], 2) if lw else 0
+    result[f"rows{rank}"] = workloads.words_sha256(np.ascontiguousarray(local[c0::world]))
     if rank == 0:
         result["sha"] = workloads.words_sha256(out.words)
         result["sha2"] = workloads.words_sha256(out2.words)
+        for r in range(world):
+            c = int(format(r, f"0{lw}b")[::-1], 2) if lw else 0
+            result[f"exp{r}"] = workloads.words_sha256(np.ascontiguousarray(out.words[c::world]))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["C1", "C2"])
-def test_distributed_multiplier_two_processes(name):
+@pytest.mark.parametrize("name,mode", [("C1", "rows"), ("C2", "rows"), ("C2", "primes")])
+def test_distributed_multiplier_two_processes(name, mode):
     # the real multi-process code path (DistributedMultiplier, torch.distributed
     # exchanges) with 2 ranks sharing this one GPU; gloo stages the exchanges
     # through host memory, so no kernel waits on another process
@@ -334,9 +369,11 @@ def test_distributed_multiplier_two_processes(name):
     port = s.getsockname()[1]
     s.close()
     result = mp.Manager().dict()
-    mp.spawn(_dist_worker, args=(2, port, name, result), nprocs=2, join=True)
+    mp.spawn(_dist_worker, args=(2, port, name, mode, result), nprocs=2, join=True)
     cfg = json.load(open(os.path.join(GOLDEN, "configs.json")))[name]
     assert result["sha"] == cfg["out_sha256"] and result["sha2"] == cfg["out_sha256"]
+    for r in range(2):      # each rank's direct download holds exactly its rows of the product
+        assert result[f"rows{r}"] == result[f"exp{r}"]
 
 
 def test_corruption_is_detected():

@@ -66,3 +66,35 @@ def test_torch_exchange_matches_layout_contract(world, primes, shard_words, grou
     for r in range(world):
         for got in out[r]:
             assert np.array_equal(got.reshape(-1), exp[r])
+
+
+def _prime_worker(rank, world, port, P, shard_words, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1612_05778_b200.shard import prime_blocks, torch_prime_exchange
+    blocks = prime_blocks(P, world)
+    q0, nq = blocks[rank]
+    S = shard_words * world
+    grids = [torch.tensor([((q0 + lq) << 20) | i for i in range(S)], dtype=torch.int32) for lq in range(nq)]
+    gathered = torch.full((P, shard_words), -1, dtype=torch.int32)
+    torch_prime_exchange(grids, gathered, blocks, world)
+    out[rank] = gathered.numpy().copy()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,P,shard_words", [(2, 3, 16), (2, 6, 8), (3, 4, 8), (2, 2, 32)])
+def test_prime_exchange_matches_layout_contract(world, P, shard_words):
+    # the prime split's one exchange: rank t gathers block t of every prime's
+    # grid as [P][shard_words] (shard.prime_exchange_slices, tc_prime_final)
+    from paper_1612_05778_b200.shard import prime_exchange_slices
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_prime_worker, args=(world, _free_port(), P, shard_words, out), nprocs=world, join=True)
+    seen = {t: np.zeros((P, shard_words), dtype=bool) for t in range(world)}
+    for s, t, q, lq, do, w in prime_exchange_slices(world, P, shard_words):
+        exp = np.array([(q << 20) | (t * shard_words + i) for i in range(w)], dtype=np.int32)
+        assert np.array_equal(out[t].reshape(-1)[do:do + w], exp)
+        seen[t][q] = True
+    for t in range(world):
+        assert seen[t].all()
