@@ -50,7 +50,6 @@ sys.path.insert(0, ROOT)
 
 from paper_1612_05778_b200 import workloads  # noqa: E402
 
-REF_SAMPLE_D = 16384        # reference-arm sample (see run_reference)
 METRIC = "product time (ms) & output Gbit/s, dxN-bit Z[x] multiply, at 1/2/4/8 B200"
 
 
@@ -645,14 +644,16 @@ def run_reference(args, rank, world):
     from paper_1612_05778_b200 import workloads
     (aw, ab), (bw, bb) = workloads.make_inputs(args.config)
     threads = os.cpu_count() or 1
-    # bounded sample: a full C3 product takes ~29 s on the box's 16 cores, so
-    # each step multiplies the first REF_SAMPLE_D coefficients of each operand
-    # (coefficient width unchanged; output Gbit/s of that product).  Per
-    # output bit the smaller product is slightly cheaper (log d in the NTT),
-    # so the sampled rate flatters the reference.
+    # each step is one FULL product of the workload (C3: ~24 s on the box's 16
+    # cores, so 20 steps take ~8 minutes).  A smaller sample is not
+    # representative: measured on the box, the first 16384 coefficients of C3
+    # run at 0.60 Gbit/s against 0.73 for the whole product (the port's fixed
+    # per-product costs), which would inflate the GPU/CPU ratio.
+    # TC_REF_SAMPLE_D=n (quick local runs only) multiplies the first n.
     full_d = aw.shape[0]
-    if aw.shape[0] > REF_SAMPLE_D:
-        aw, bw = aw[:REF_SAMPLE_D], bw[:REF_SAMPLE_D]
+    sample_d = int(os.environ.get("TC_REF_SAMPLE_D", "0"))
+    if 0 < sample_d < aw.shape[0]:
+        aw, bw = aw[:sample_d], bw[:sample_d]
     rows = aw.shape[0] + bw.shape[0] - 1
     out_bits = port.product_bit_width(aw, bw)
     out_gbit = rows * out_bits / 1e9
@@ -677,8 +678,9 @@ def run_reference(args, rank, world):
                    "parallelism": "CPU, all host threads"},
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 4), "unit": "Gbit/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} products of the first {aw.shape[0]} of the {full_d} coefficients "
-                                   f"of each {args.config} operand (width unchanged), oracle/ C restatement "
+                         "sample": (f"{args.steps} full {args.config} products" if aw.shape[0] == full_d else
+                                    f"{args.steps} products of the first {aw.shape[0]} of the {full_d} coefficients "
+                                    f"of each {args.config} operand (TC_REF_SAMPLE_D)") + ", oracle/ C restatement "
                                    f"of the reference kernels (the reference is pure Python/numba "
                                    f"and is not present on the GPU box); warm-up: one product of "
                                    f"the first 1024 coefficients",

@@ -19,7 +19,7 @@ def stage_of(kernel):
         return "convert"
     if "k_final" in kernel:
         return "recover"
-    m = re.search(r"k_high(?:_ct)?<(\d)", kernel)
+    m = re.search(r"k_high(?:_ct|_tma)?<(\d)", kernel)
     if m:
         return {"0": "ntt_forward", "1": "ntt_inverse", "2": "pointwise"}[m.group(1)]
     return None
@@ -70,8 +70,8 @@ def main():
         src = f"{rel} (ncu --set full --clock-control none, one capture)"
         traffic[cfg] = {"source": src, "stages": st}
         metrics[cfg] = {"source": rel, "kernels": kn}
-    json.dump(traffic, open(os.path.join(ROOT, "profiles", "r1_traffic.json"), "w"), indent=1)
-    json.dump(metrics, open(os.path.join(ROOT, "profiles", "r1_ncu_metrics.json"), "w"), indent=1)
+    json.dump(traffic, open(os.path.join(ROOT, "profiles", os.environ.get("TAG", "r2") + "_traffic.json"), "w"), indent=1)
+    json.dump(metrics, open(os.path.join(ROOT, "profiles", os.environ.get("TAG", "r2") + "_ncu_metrics.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":
