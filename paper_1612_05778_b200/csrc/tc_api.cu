@@ -22,6 +22,7 @@
 #include <mutex>
 #include <condition_variable>
 #include <atomic>
+#include <emmintrin.h>
 
 #include "../../include/tc_api.h"
 #include "tc_kernels.cuh"
@@ -151,8 +152,30 @@ private:
     CopyPool() {
         int n = (int)std::thread::hardware_concurrency();
         const char* e = getenv("TC_COPY_THREADS");
+        // 8 threads with streaming stores: C3 pageable e2e 92.8 -> 78.4 ms (page-locked inputs:
+        // 75.6); 12 / 16 threads on the box's 16 cores measured slower (87 / 103 ms)
         n = e && *e ? atoi(e) : (n > 8 ? 8 : n);
         for (int i = 1; i < n; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    // Streaming copy: the destination (a pinned ring slot, read next by the
+    // copy engine, never by this CPU) is written with non-temporal stores, so
+    // no destination line is read for ownership or left in the caches.
+    static void stream_copy(char* dst, const char* src, size_t len) {
+        static const bool nt = [] { const char* v = getenv("TC_COPY_NT"); return !(v && *v == '0'); }();
+        if (!nt || ((uintptr_t)dst & 15) || len < 4096) { memcpy(dst, src, len); return; }
+        size_t i = 0;
+        for (; i + 64 <= len; i += 64) {
+            const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+            const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+            const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+            const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+            _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d);
+        }
+        if (i < len) memcpy(dst + i, src + i, len - i);
+        _mm_sfence();
     }
     void work() {
         for (;;) {
@@ -160,7 +183,7 @@ private:
             if (k >= pieces_) break;
             const size_t per = (len_ / pieces_ + 63) & ~(size_t)63;
             const size_t a = (size_t)k * per;
-            if (a < len_) memcpy(dst_ + a, src_ + a, a + per < len_ ? per : len_ - a);
+            if (a < len_) stream_copy(dst_ + a, src_ + a, a + per < len_ ? per : len_ - a);
             if (remaining_.fetch_sub(1) == 1) { std::lock_guard<std::mutex> lk(mu_); done_cv_.notify_all(); }
         }
     }
@@ -774,6 +797,11 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
         // every stored word inside the groups' span (+ the flush group)
         static const int ld4 = env_int("TC_FINAL_LD4", 1);
         A.ld4 = ld4;
+        static const int fmulti = env_int("TC_FINAL_MULTI", 1);
+        A.multi = fmulti;
+        static const int ffuse0 = env_int("TC_FINAL_FUSE0", 1);
+        // pays when it saves a whole round (yl = 1, 5, 9: C3 k_final 11.0 -> 10.3 ms; C2's yl = 4: +3 %)
+        A.fuse0 = ffuse0 == 2 || (ffuse0 == 1 && G.yl % 4 == 1);
         static const int cwarp = env_int("TC_CO_WARP", 1);
         const int waw = M >> 5, wb = M & 31;
         if (cwarp && !dump && W32 > 0 && G.lgL >= 5 && wb <= 1 &&

@@ -643,24 +643,42 @@ __device__ __forceinline__ void run_bits(uint32_t* s, int tile_bits, int lo, int
 struct Span { uint32_t t0, nt; };
 __device__ __forceinline__ Span cta_span() { return Span{threadIdx.x, blockDim.x}; }
 
-template <int BL, int NB, bool DIF>
+// Several tiles (one per prime, `stride` words apart) worked as ONE list of
+// groups per round (k_final): item = tile * ngroups + group, so a round of
+// all the primes ends with one barrier and every thread gets nq * ngroups /
+// threads independent groups.  ps: the primes (shared memory); the twiddle
+// tables of consecutive primes are twstride entries apart.
+struct Multi { int nq; uint32_t stride; int64_t twstride; const uint32_t* ps; };
+
+template <int BL, int NB, bool DIF, bool MULTI = false>
 __device__ __forceinline__ void xct_round(uint32_t* s, int tile_bits, const uint2* twx, uint32_t p, uint32_t two_p,
-                                          Span sp) {
+                                          Span span, Multi mq = Multi{}) {
     constexpr int R = 1 << NB;
     constexpr uint32_t lowmask = (1u << BL) - 1;
     constexpr bool PERMC = BL >= 1 && BL <= 4 && BL >= NB;
     constexpr uint32_t pa = BL, pb = BL + 5 - NB;
     const uint32_t pm = (PERMC && tile_bits >= 10) ? (1u << (5 - BL)) - 1 : 0u;
     const uint32_t ngroups = 1u << (tile_bits - NB);
-    for (uint32_t g0 = sp.t0; g0 < ngroups; g0 += sp.nt) {
+    const uint32_t nitems = MULTI ? ngroups * (uint32_t)mq.nq : ngroups;
+    for (uint32_t g0 = span.t0; g0 < nitems; g0 += span.nt) {
         uint32_t g = g0;
+        uint32_t* sb = s;
+        const uint2* tb = twx;
+        if (MULTI) {
+            const uint32_t q = g0 >> (tile_bits - NB);
+            g = g0 & (ngroups - 1);
+            sb = s + q * mq.stride;
+            tb = twx + (int64_t)q * mq.twstride;
+            p = mq.ps[q];
+            two_p = 2 * p;
+        }
         if (PERMC) {
             const uint32_t t = ((g >> pa) ^ (g >> pb)) & pm;
             g ^= (t << pa) ^ (t << pb);
         }
         const uint32_t lo = g & lowmask;
-        uint32_t* sp = s + padi(((g & ~lowmask) << NB) | lo);
-        const uint2* tq = twx + lo;
+        uint32_t* sp = sb + padi(((g & ~lowmask) << NB) | lo);
+        const uint2* tq = tb + lo;
         uint32_t x[R];
 #pragma unroll
         for (int k = 0; k < R; ++k) x[k] = sp[(k << BL) + ((k << BL) >> 5)];
@@ -685,56 +703,57 @@ __device__ __forceinline__ void xct_round(uint32_t* s, int tile_bits, const uint
 }
 
 // bits [LO, HI) in rounds of <= 4 bits (run_segment's partition)
-template <int LO, int HI, bool DIF>
+template <int LO, int HI, bool DIF, bool MULTI = false>
 __device__ __forceinline__ void xct_seg(uint32_t* s, int tile_bits, const uint2* twx, uint32_t p, uint32_t two_p,
-                                        Span sp) {
+                                        Span sp, Multi mq = Multi{}) {
     constexpr int nbits = HI - LO;
     if constexpr (nbits > 0) {
         constexpr int nr = (nbits + 3) / 4;
         constexpr int nb = nbits / nr + (nbits % nr ? 1 : 0);
         if constexpr (!DIF) {
-            xct_round<LO, nb, false>(s, tile_bits, twx, p, two_p, sp);
-            xct_seg<LO + nb, HI, false>(s, tile_bits, twx, p, two_p, sp);
+            xct_round<LO, nb, false, MULTI>(s, tile_bits, twx, p, two_p, sp, mq);
+            xct_seg<LO + nb, HI, false, MULTI>(s, tile_bits, twx, p, two_p, sp, mq);
         } else {
-            xct_round<HI - nb, nb, true>(s, tile_bits, twx, p, two_p, sp);
-            xct_seg<LO, HI - nb, true>(s, tile_bits, twx, p, two_p, sp);
+            xct_round<HI - nb, nb, true, MULTI>(s, tile_bits, twx, p, two_p, sp, mq);
+            xct_seg<LO, HI - nb, true, MULTI>(s, tile_bits, twx, p, two_p, sp, mq);
         }
     }
 }
 
-template <int LGL, bool DIF>
-__device__ __forceinline__ void xct(uint32_t* s, int tile_bits, const uint2* twx, uint32_t p, uint32_t two_p, Span sp) {
+template <int LGL, bool DIF, bool MULTI = false>
+__device__ __forceinline__ void xct(uint32_t* s, int tile_bits, const uint2* twx, uint32_t p, uint32_t two_p, Span sp,
+                                    Multi mq = Multi{}) {
     constexpr int mid = LGL > 4 ? 4 : LGL;
     if (!DIF) {
-        xct_seg<0, mid, false>(s, tile_bits, twx, p, two_p, sp);
-        xct_seg<mid, LGL, false>(s, tile_bits, twx, p, two_p, sp);
+        xct_seg<0, mid, false, MULTI>(s, tile_bits, twx, p, two_p, sp, mq);
+        xct_seg<mid, LGL, false, MULTI>(s, tile_bits, twx, p, two_p, sp, mq);
     } else {
-        xct_seg<mid, LGL, true>(s, tile_bits, twx, p, two_p, sp);
-        xct_seg<0, mid, true>(s, tile_bits, twx, p, two_p, sp);
+        xct_seg<mid, LGL, true, MULTI>(s, tile_bits, twx, p, two_p, sp, mq);
+        xct_seg<0, mid, true, MULTI>(s, tile_bits, twx, p, two_p, sp, mq);
     }
 }
 
 // The x transform of a tile: one out-of-line copy per direction, dispatched on lgL.
-template <bool DIF>
+template <bool DIF, bool MULTI = false>
 __device__ __noinline__ void x_transform(uint32_t* s, int lgL, int tile_bits, const uint2* twx,
-                                         uint32_t p, uint32_t two_p, Span sp) {
+                                         uint32_t p, uint32_t two_p, Span sp, Multi mq = Multi{}) {
     switch (lgL) {
         case 0: break;
-        case 1: xct<1, DIF>(s, tile_bits, twx, p, two_p, sp); break;
-        case 2: xct<2, DIF>(s, tile_bits, twx, p, two_p, sp); break;
-        case 3: xct<3, DIF>(s, tile_bits, twx, p, two_p, sp); break;
-        case 4: xct<4, DIF>(s, tile_bits, twx, p, two_p, sp); break;
-        case 5: xct<5, DIF>(s, tile_bits, twx, p, two_p, sp); break;
-        case 6: xct<6, DIF>(s, tile_bits, twx, p, two_p, sp); break;
-        case 7: xct<7, DIF>(s, tile_bits, twx, p, two_p, sp); break;
-        case 8: xct<8, DIF>(s, tile_bits, twx, p, two_p, sp); break;
-        case 9: xct<9, DIF>(s, tile_bits, twx, p, two_p, sp); break;
-        case 10: xct<10, DIF>(s, tile_bits, twx, p, two_p, sp); break;
-        case 11: xct<11, DIF>(s, tile_bits, twx, p, two_p, sp); break;
-        case 12: xct<12, DIF>(s, tile_bits, twx, p, two_p, sp); break;
-        case 13: xct<13, DIF>(s, tile_bits, twx, p, two_p, sp); break;
-        case 14: xct<14, DIF>(s, tile_bits, twx, p, two_p, sp); break;
-        case 15: xct<15, DIF>(s, tile_bits, twx, p, two_p, sp); break;
+        case 1: xct<1, DIF, MULTI>(s, tile_bits, twx, p, two_p, sp, mq); break;
+        case 2: xct<2, DIF, MULTI>(s, tile_bits, twx, p, two_p, sp, mq); break;
+        case 3: xct<3, DIF, MULTI>(s, tile_bits, twx, p, two_p, sp, mq); break;
+        case 4: xct<4, DIF, MULTI>(s, tile_bits, twx, p, two_p, sp, mq); break;
+        case 5: xct<5, DIF, MULTI>(s, tile_bits, twx, p, two_p, sp, mq); break;
+        case 6: xct<6, DIF, MULTI>(s, tile_bits, twx, p, two_p, sp, mq); break;
+        case 7: xct<7, DIF, MULTI>(s, tile_bits, twx, p, two_p, sp, mq); break;
+        case 8: xct<8, DIF, MULTI>(s, tile_bits, twx, p, two_p, sp, mq); break;
+        case 9: xct<9, DIF, MULTI>(s, tile_bits, twx, p, two_p, sp, mq); break;
+        case 10: xct<10, DIF, MULTI>(s, tile_bits, twx, p, two_p, sp, mq); break;
+        case 11: xct<11, DIF, MULTI>(s, tile_bits, twx, p, two_p, sp, mq); break;
+        case 12: xct<12, DIF, MULTI>(s, tile_bits, twx, p, two_p, sp, mq); break;
+        case 13: xct<13, DIF, MULTI>(s, tile_bits, twx, p, two_p, sp, mq); break;
+        case 14: xct<14, DIF, MULTI>(s, tile_bits, twx, p, two_p, sp, mq); break;
+        case 15: xct<15, DIF, MULTI>(s, tile_bits, twx, p, two_p, sp, mq); break;
         default: __trap();
     }
 }
@@ -747,18 +766,30 @@ __device__ __noinline__ void x_transform(uint32_t* s, int lgL, int tile_bits, co
 // Requires lgL >= 5 (every round above bit 5: linear padded addressing, no
 // lane permutation).
 // ---------------------------------------------------------------------------
-template <int RB, int NB, bool DIF>
+template <int RB, int NB, bool DIF, bool MULTI = false>
 __device__ __forceinline__ void yct_round(uint32_t* s, int tile_bits, int lgL, const uint2* twy,
-                                          uint32_t p, uint32_t two_p, Span sp) {
+                                          uint32_t p, uint32_t two_p, Span sp, Multi mq = Multi{}) {
     constexpr int R = 1 << NB;
     const int bl = lgL + RB;
     const uint32_t lowmask = (1u << bl) - 1;
     const uint32_t astep = (1u << bl) + (1u << (bl - 5));
     const uint32_t ngroups = 1u << (tile_bits - NB);
-    for (uint32_t g = sp.t0; g < ngroups; g += sp.nt) {
+    const uint32_t nitems = MULTI ? ngroups * (uint32_t)mq.nq : ngroups;
+    for (uint32_t g0 = sp.t0; g0 < nitems; g0 += sp.nt) {
+        uint32_t g = g0;
+        uint32_t* sb = s;
+        const uint2* tb = twy;
+        if (MULTI) {
+            const uint32_t q = g0 >> (tile_bits - NB);
+            g = g0 & (ngroups - 1);
+            sb = s + q * mq.stride;
+            tb = twy + (int64_t)q * mq.twstride;
+            p = mq.ps[q];
+            two_p = 2 * p;
+        }
         const uint32_t lo = g & lowmask;
-        uint32_t* sq = s + padi(((g & ~lowmask) << NB) | lo);
-        const uint2* tq = twy + (lo >> lgL);
+        uint32_t* sq = sb + padi(((g & ~lowmask) << NB) | lo);
+        const uint2* tq = tb + (lo >> lgL);
         uint32_t x[R];
 #pragma unroll
         for (int k = 0; k < R; ++k) x[k] = sq[k * astep];
@@ -782,19 +813,19 @@ __device__ __forceinline__ void yct_round(uint32_t* s, int tile_bits, int lgL, c
     __syncthreads();
 }
 
-template <int LO, int HI, bool DIF>
+template <int LO, int HI, bool DIF, bool MULTI = false>
 __device__ __forceinline__ void yct_seg(uint32_t* s, int tile_bits, int lgL, const uint2* twy, uint32_t p,
-                                        uint32_t two_p, Span sp) {
+                                        uint32_t two_p, Span sp, Multi mq = Multi{}) {
     constexpr int nbits = HI - LO;
     if constexpr (nbits > 0) {
         constexpr int nr = (nbits + 3) / 4;
         constexpr int nb = nbits / nr + (nbits % nr ? 1 : 0);
         if constexpr (!DIF) {
-            yct_round<LO, nb, false>(s, tile_bits, lgL, twy, p, two_p, sp);
-            yct_seg<LO + nb, HI, false>(s, tile_bits, lgL, twy, p, two_p, sp);
+            yct_round<LO, nb, false, MULTI>(s, tile_bits, lgL, twy, p, two_p, sp, mq);
+            yct_seg<LO + nb, HI, false, MULTI>(s, tile_bits, lgL, twy, p, two_p, sp, mq);
         } else {
-            yct_round<HI - nb, nb, true>(s, tile_bits, lgL, twy, p, two_p, sp);
-            yct_seg<LO, HI - nb, true>(s, tile_bits, lgL, twy, p, two_p, sp);
+            yct_round<HI - nb, nb, true, MULTI>(s, tile_bits, lgL, twy, p, two_p, sp, mq);
+            yct_seg<LO, HI - nb, true, MULTI>(s, tile_bits, lgL, twy, p, two_p, sp, mq);
         }
     }
 }
@@ -894,10 +925,11 @@ __device__ __forceinline__ bool ysm_dispatch(uint32_t* s, int rb0, int tile_bits
 
 // y levels [lgL + rb0, tile_bits) of a tile; false if the shape has no
 // compile-time schedule (caller runs the generic rounds).
-template <bool DIF>
+template <bool DIF, bool MULTI = false>
 __device__ __noinline__ bool y_transform(uint32_t* s, int lgL, int rb0, int tile_bits, const uint2* twy,
-                                         uint32_t p, uint32_t two_p, Span sp) {
+                                         uint32_t p, uint32_t two_p, Span sp, Multi mq = Multi{}) {
     const int ny = tile_bits - lgL - rb0;
+    if (MULTI && lgL < 5) return false;                     // the multi-tile rounds cover wide rows only
     if (lgL >= 1 && lgL <= 4 && rb0 <= 1 && ny >= 1) {      // narrow rows
         switch (lgL) {
             case 1: return ysm_dispatch<1, DIF>(s, rb0, tile_bits, twy, p, two_p, sp);
@@ -907,7 +939,7 @@ __device__ __noinline__ bool y_transform(uint32_t* s, int lgL, int rb0, int tile
         }
     }
     if (lgL < 5 || ny < 0 || ny > 12 || rb0 > 1) return false;
-#define TC_YCASE(R0, N) case (R0) * 16 + (N): yct_seg<R0, R0 + N, DIF>(s, tile_bits, lgL, twy, p, two_p, sp); break;
+#define TC_YCASE(R0, N) case (R0) * 16 + (N): yct_seg<R0, R0 + N, DIF, MULTI>(s, tile_bits, lgL, twy, p, two_p, sp, mq); break;
     switch (rb0 * 16 + ny) {
         case 0: case 16: break;
         TC_YCASE(0, 1) TC_YCASE(0, 2) TC_YCASE(0, 3) TC_YCASE(0, 4) TC_YCASE(0, 5) TC_YCASE(0, 6)
@@ -1856,6 +1888,8 @@ struct FinalArgs {
     int cw_aw, cw_b;               // > 0: warp-group CRT + ConvertOut (crt_convert_warp), M = 32 cw_aw + cw_b
     const uint32_t* nbtab;         // its bias tables: 2 x (32 cw_aw + cw_b) words (first group / later groups)
     int ld4;                       // tile loads: four cp.async per address computation
+    int fuse0;                     // with multi + the warp CRT: y level 0 folded into the CRT's reads
+    int multi;                     // transforms: every round over all P tiles at once (one barrier per round)
     unsigned long long* prof;      // phase timers (PROF_FIN_*), or null
 };
 
@@ -2135,14 +2169,29 @@ struct WarpCoShape {
 template <int P, int B>
 __device__ __forceinline__ void warp_term_pieces(const FinalArgs& A, const CrtConst& cc, const uint32_t* sm,
                                                  uint32_t stride, uint32_t rowbase, int j, int L, uint32_t prow,
-                                                 bool real_row, uint32_t (&pc)[P + B]) {
+                                                 bool real_row, uint32_t (&pc)[P + B], bool fuse0 = false) {
     uint32_t x[P];
     if (j < L) {
         uint32_t rr[P];
         const uint32_t e = padi(rowbase + (uint32_t)j);
-        rr[0] = canon(sm[e], cc.p[0]);
+        if (fuse0) {
+            // the last inverse y level (row bit 0, twiddle 1) was left out of the
+            // transforms (it commutes with the x levels): rows (2m, 2m+1) hold
+            // (a, b), the finished values are a + b and a - b
+            const uint32_t ea = padi((rowbase & ~(uint32_t)L) + (uint32_t)j), eb = padi((rowbase | (uint32_t)L) + (uint32_t)j);
+            const bool odd = (rowbase & (uint32_t)L) != 0;
 #pragma unroll
-        for (int q = 1; q < P; ++q) rr[q] = reduce_2p(sm[q * stride + e], 2 * cc.p[q]);
+            for (int q = 0; q < P; ++q) {
+                const uint32_t tp = 2 * cc.p[q];
+                const uint32_t a = reduce_2p(sm[q * stride + ea], tp), b = reduce_2p(sm[q * stride + eb], tp);
+                rr[q] = reduce_2p(odd ? a - b + tp : a + b, tp);
+            }
+            rr[0] = min(rr[0], rr[0] - cc.p[0]);
+        } else {
+            rr[0] = canon(sm[e], cc.p[0]);
+#pragma unroll
+            for (int q = 1; q < P; ++q) rr[q] = reduce_2p(sm[q * stride + e], 2 * cc.p[q]);
+        }
         const int64_t flat = (int64_t)prow * L + j;
         if (A.inject >= 0 && flat == A.inject) rr[0] = rr[0] ? rr[0] - 1 : cc.p[0] - 1;   // fault injection (tests)
         if (A.inject_par >= 0 && flat == A.inject_par) {
@@ -2178,7 +2227,7 @@ __device__ __forceinline__ void warp_term_pieces(const FinalArgs& A, const CrtCo
 
 template <int P, int AW, int B>
 __device__ __forceinline__ void crt_convert_warp(const FinalArgs& A, const CrtConst& cc, const uint32_t* sm,
-                                                 uint32_t stride, int R, uint32_t pos0, bool sharded) {
+                                                 uint32_t stride, int R, uint32_t pos0, bool sharded, bool fuse0) {
     using Sh = WarpCoShape<P, AW, B>;
     constexpr int GW = Sh::GW, NPC = Sh::NPC, TMAX = Sh::TMAX;
     constexpr int NOWN = AW + B;                          // words a lane may own (lane 31: AW + B)
@@ -2210,7 +2259,7 @@ __device__ __forceinline__ void crt_convert_warp(const FinalArgs& A, const CrtCo
             // warm-up: the group before the segment, for its tail pieces and last word
             const int g = ga - 1;
             const uint64_t kw = A.prof ? clock64() : 0;
-            warp_term_pieces<P, B>(A, cc, sm, stride, rowbase, 32 * g + lane, L, prow, false, prv);
+            warp_term_pieces<P, B>(A, cc, sm, stride, rowbase, 32 * g + lane, L, prow, false, prv, fuse0);
             if (A.prof && lane == 0) {
                 const unsigned long long dk = (unsigned long long)(clock64() - kw);
                 atomicAdd(&A.prof[PROF_FIN_CRT], dk);
@@ -2235,7 +2284,7 @@ __device__ __forceinline__ void crt_convert_warp(const FinalArgs& A, const CrtCo
         for (int g = ga; g < gb; ++g) {
             uint32_t cur[NPC];
             const uint64_t k0 = prof ? clock64() : 0;
-            warp_term_pieces<P, B>(A, cc, sm, stride, rowbase, 32 * g + lane, L, prow, real_row, cur);
+            warp_term_pieces<P, B>(A, cc, sm, stride, rowbase, 32 * g + lane, L, prow, real_row, cur, fuse0);
             if (prof) cyc_crt += clock64() - k0;
             const uint32_t* nb = nbt[g == 0 ? 0 : 1];
             // word sums of the owned words: slot s < AW, and (lane 31, B = 1) the extra word
@@ -2518,7 +2567,20 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
     // tiles of 512-thread CTAs): two primes side by side, one per half.
     const uint32_t halfT = blockDim.x >> 1;
     const bool dual = A.dual_ok && P >= 2 && A.lgL >= 5 && A.yl <= 12 && (n >> 4) <= halfT;
-    if (dual) {
+    __shared__ uint32_t s_primes[kMaxPrimes];
+    // the lowest inverse y level (twiddle 1) folded into the CRT's reads (warp_term_pieces)
+    const bool fuse0 = !DUMP && P <= 8 && A.fuse0 && A.multi && P >= 2 && A.lgL >= 5 && A.yl >= 1 && A.yl <= 12 && A.cw_aw > 0;
+    if (A.multi && P >= 2 && A.lgL >= 5 && A.yl <= 12) {
+        // every round runs over the P tiles as one list of groups: one barrier
+        // per round (not per round and prime pair) and P n / (16 threads)
+        // independent groups per thread in between
+        if (threadIdx.x < P) s_primes[threadIdx.x] = cc.p[threadIdx.x];
+        cp_async_wait<0>();
+        __syncthreads();
+        const Multi my{P, stride, A.twy_stride, s_primes}, mx{P, stride, (int64_t)L, s_primes};
+        y_transform<true, true>(sm, A.lgL, fuse0 ? 1 : 0, tile_bits, A.twy, 0u, 0u, cta_span(), my);   // y low: DIF
+        x_transform<false, true>(sm, A.lgL, tile_bits, A.twx, 0u, 0u, cta_span(), mx);      // x: DIT
+    } else if (dual) {
         const int hsel = threadIdx.x >= halfT ? 1 : 0;
         for (int q0 = 0; q0 < P; q0 += 2) {
             const int q = q0 + hsel;
@@ -2571,15 +2633,15 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_fi
     const bool warp_co = A.cw_aw > 0;
     if constexpr (!DUMP && P <= 8) {
         if (A.cw_aw == 2) {
-            if (A.cw_b) crt_convert_warp<P, 2, 1>(A, cc, sm, stride, R, pos0, sharded);
-            else crt_convert_warp<P, 2, 0>(A, cc, sm, stride, R, pos0, sharded);
+            if (A.cw_b) crt_convert_warp<P, 2, 1>(A, cc, sm, stride, R, pos0, sharded, fuse0);
+            else crt_convert_warp<P, 2, 0>(A, cc, sm, stride, R, pos0, sharded, fuse0);
             TC_FIN_END();
             return;
         }
         if constexpr (P <= 4) {
             if (A.cw_aw == 1) {
-                if (A.cw_b) crt_convert_warp<P, 1, 1>(A, cc, sm, stride, R, pos0, sharded);
-                else crt_convert_warp<P, 1, 0>(A, cc, sm, stride, R, pos0, sharded);
+                if (A.cw_b) crt_convert_warp<P, 1, 1>(A, cc, sm, stride, R, pos0, sharded, fuse0);
+                else crt_convert_warp<P, 1, 0>(A, cc, sm, stride, R, pos0, sharded, fuse0);
                 TC_FIN_END();
                 return;
             }
