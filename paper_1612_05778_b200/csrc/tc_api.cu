@@ -351,6 +351,13 @@ PrimeC make_prime_const(uint32_t p, int64_t S) {
     pc.c64 = (uint32_t)(r32 * r32 % p);
     pc.c96 = (uint32_t)(r32 * r32 % p * r32 % p);
     pc.one_sh = (uint32_t)((1ull << 32) / p);
+    pc.c32 = (uint32_t)r32;
+    pc.c32_sh = (uint32_t)(((uint64_t)pc.c32 << 32) / p);
+    pc.c64_sh = (uint32_t)(((uint64_t)pc.c64 << 32) / p);
+    pc.c96_sh = (uint32_t)(((uint64_t)pc.c96 << 32) / p);
+    pc.n64 = p - pc.c64;
+    pc.n96 = p - pc.c96;
+    pc.n128 = p - (uint32_t)((uint64_t)pc.c96 * r32 % p);
     const uint64_t sinv = inv_mod((uint32_t)(S % p), p);
     pc.scale = (uint32_t)(sinv * r32 % p);
     pc.scale_sh = (uint32_t)(((uint64_t)pc.scale << 32) / p);

@@ -25,6 +25,11 @@ struct PrimeC {
     uint32_t scale;      // (s_y * L)^{-1} * 2^32 mod p, applied after the Montgomery pointwise product
     uint32_t scale_sh;   // Shoup companion of scale
     uint32_t c96;        // 2^96 mod p (residues of two-word digits, M > 63)
+    uint32_t c32;        // 2^32 mod p and the Shoup companions of c32, c64, c96
+    uint32_t c32_sh, c64_sh, c96_sh;
+    uint32_t n96, n128;  // p - (2^96 mod p), p - (2^128 mod p): the weight of a negative digit's sign
+    uint32_t n64;        // p - (2^64 mod p)
+    uint32_t pad;
 };
 
 // a * w mod p for a fixed w with companion wsh = floor(w * 2^32 / p).
@@ -68,30 +73,31 @@ __device__ __forceinline__ void bfly_dit(uint32_t& x, uint32_t& y, uint32_t w, u
     y = u - v + two_p;
 }
 
-// a mod p, canonical, for any 64-bit a.
-__device__ __forceinline__ uint32_t u64_mod(uint64_t a, const PrimeC& c) {
-    const uint32_t r = mont_mul((uint32_t)(a >> 32), c.c64, c.p, c.pinv_neg) + shoup_mul((uint32_t)a, 1u, c.one_sh, c.p);
-    return canon(r, c.p);
-}
-
-// |digit| mod p for a signed balanced digit (one word, M <= 63), canonical.
+// Residue in [0, 2p) of a signed balanced digit (one word, M <= 63) from the
+// two limbs of its two's complement: d0 + d1 2^32 - [negative] 2^64.
 __device__ __forceinline__ uint32_t digit_residue(int64_t dg, const PrimeC& c) {
-    const uint64_t a = dg < 0 ? (uint64_t)(-(dg + 1)) + 1 : (uint64_t)dg;
-    uint32_t r = u64_mod(a, c);
-    if (dg < 0 && r) r = c.p - r;
-    return r;
+    const uint32_t d0 = (uint32_t)dg, d1 = (uint32_t)((uint64_t)dg >> 32);
+    uint32_t t = d0 - __umulhi(d0, c.one_sh) * c.p;
+    t = reduce_2p(t + shoup_mul(d1, c.c32, c.c32_sh, c.p), c.two_p);
+    return reduce_2p(t + ((int32_t)d1 < 0 ? c.n64 : 0u), c.two_p);
 }
 
-// The same for a two-word digit (64 <= M <= 126): lo + hi * 2^64, the high
-// part through a Montgomery product with 2^96 mod p.
-__device__ __forceinline__ uint32_t digit_residue(__int128 dg, const PrimeC& c) {
-    const unsigned __int128 a = dg < 0 ? (unsigned __int128)(-(dg + 1)) + 1 : (unsigned __int128)dg;
-    const uint64_t h = (uint64_t)(a >> 64);
-    // M <= 96: the high word is below 2^32 and enters the Montgomery product as is
-    const uint32_t lo = u64_mod((uint64_t)a, c), hi = (h >> 32) ? u64_mod(h, c) : (uint32_t)h;
-    uint32_t r = canon(lo + mont_mul(hi, c.c96, c.p, c.pinv_neg), c.p);
-    if (dg < 0 && r) r = c.p - r;
-    return r;
+// Residue in [0, 2p) of a two-word balanced digit (64 <= M <= 126) from the
+// low nl = 3 (M <= 94) or 4 limbs d0..d3 of its two's complement: the value is
+// sum_k d_k 2^(32k) - [negative] 2^(32 nl), each limb times the fixed 2^(32k)
+// mod p (Shoup), no absolute value and no 128-bit arithmetic.
+__device__ __forceinline__ uint32_t digit_residue_limbs(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3, int nl,
+                                                        const PrimeC& c) {
+    uint32_t t = d0 - __umulhi(d0, c.one_sh) * c.p;
+    t = reduce_2p(t + shoup_mul(d1, c.c32, c.c32_sh, c.p), c.two_p);
+    t = reduce_2p(t + shoup_mul(d2, c.c64, c.c64_sh, c.p), c.two_p);
+    uint32_t top = d2, nw = c.n96;
+    if (nl == 4) {
+        t = reduce_2p(t + shoup_mul(d3, c.c96, c.c96_sh, c.p), c.two_p);
+        top = d3;
+        nw = c.n128;
+    }
+    return reduce_2p(t + ((int32_t)top < 0 ? nw : 0u), c.two_p);
 }
 
 }  // namespace tc

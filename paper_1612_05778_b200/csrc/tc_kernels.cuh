@@ -1107,6 +1107,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
     const int cbits = tile_bits - (prune ? 1 : 0);
     const uint32_t n = 1u << tile_bits, nc = 1u << cbits;
     const bool wide = A.src.M > 63;                         // two-word digits
+    const int wide_nl = A.src.M <= 94 ? 3 : 4;              // limbs of a digit's two's complement
     int64_t* dig = reinterpret_cast<int64_t*>(smem_raw);
     __int128* dig2 = reinterpret_cast<__int128*>(smem_raw);
     int64_t* coeff = dig + (int64_t)Rc * A.src.K * (wide ? 2 : 1);
@@ -1167,7 +1168,12 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
             const uint32_t e = (r << A.lgL) | j;
             uint32_t x = 0, y = 0;
             if (coeff[r] >= 0) {
-                x = wide ? digit_residue(dig2[t], pc) : digit_residue(dig[t], pc);
+                if (wide) {
+                    const uint4 dv = reinterpret_cast<const uint4*>(dig2)[t];
+                    x = digit_residue_limbs(dv.x, dv.y, dv.z, dv.w, wide_nl, pc);
+                } else {
+                    x = digit_residue(dig[t], pc);
+                }
                 const uint2 w = __ldg(wtop + j);
                 y = shoup_mul(x, w.x, w.y, pc.p);
             }
