@@ -1114,6 +1114,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
     uint32_t* tile = reinterpret_cast<uint32_t*>(coeff + Rc);
     __shared__ DigitScratch ds;
     __shared__ int s_nvalid;
+    __shared__ PrimeC s_pcs[kMaxPrimes];
     const uint32_t gtile = blockIdx.x + (uint32_t)A.sh.h0;     // global low-phase tile
     const uint32_t pos0 = gtile * (uint32_t)R;
     const bool sharded = A.sh.world > 1;
@@ -1122,6 +1123,9 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
         return sharded ? A.g + (int64_t)q * (A.sh.Tl << A.sh.TB) : A.g + (int64_t)q * A.S + (int64_t)blockIdx.x * n;
     };
     if (threadIdx.x == 0) s_nvalid = 0;
+    // the per-prime constants, once per CTA (each prime's pass starts from shared memory)
+    for (int i = threadIdx.x; i < A.P * (int)(sizeof(PrimeC) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t*>(s_pcs)[i] = __ldg(reinterpret_cast<const uint32_t*>(A.pcs) + i);
     __syncthreads();
     for (int r = threadIdx.x; r < Rc; r += blockDim.x) {
         const int64_t i = bitrev(pos0 + (prune ? 2 * r : r), A.lgS);
@@ -1160,25 +1164,37 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
     // (DIF on (x_j, 0) pairs, the theta-twist) is fused here: columns j and
     // j + K get x_j and x_j w_j
     auto residues = [&](int q, uint32_t* tb, Span sp) {
-        const PrimeC pc = A.pcs[q];
+        const PrimeC pc = s_pcs[q];
         const uint2* wtop = A.twx + (int64_t)q * L + (L >> 1);   // level lgL-1, entry 2^(lgL-1) + j
         const uint32_t kk = (uint32_t)A.src.K, nk = (uint32_t)Rc * kk;
-        for (uint32_t t = sp.t0; t < nk; t += sp.nt) {
-            const uint32_t r = t >> A.src.lgK, j = t & (kk - 1);
-            const uint32_t e = (r << A.lgL) | j;
-            uint32_t x = 0, y = 0;
-            if (coeff[r] >= 0) {
-                if (wide) {
-                    const uint4 dv = reinterpret_cast<const uint4*>(dig2)[t];
-                    x = digit_residue_limbs(dv.x, dv.y, dv.z, dv.w, wide_nl, pc);
-                } else {
-                    x = digit_residue(dig[t], pc);
-                }
-                const uint2 w = __ldg(wtop + j);
-                y = shoup_mul(x, w.x, w.y, pc.p);
+        constexpr int UB = 4;                                    // twist twiddles in flight per thread
+        for (uint32_t t0 = sp.t0; t0 < nk; t0 += UB * sp.nt) {
+            uint2 w[UB];
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const uint32_t t = t0 + u * sp.nt;
+                w[u] = t < nk ? __ldg(wtop + (t & (kk - 1))) : make_uint2(0u, 0u);
             }
-            tb[padi(e)] = x;
-            tb[padi(e + kk)] = y;
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const uint32_t t = t0 + u * sp.nt;
+                if (t < nk) {
+                    const uint32_t r = t >> A.src.lgK, j = t & (kk - 1);
+                    const uint32_t e = (r << A.lgL) | j;
+                    uint32_t x = 0, y = 0;
+                    if (coeff[r] >= 0) {
+                        if (wide) {
+                            const uint4 dv = reinterpret_cast<const uint4*>(dig2)[t];
+                            x = digit_residue_limbs(dv.x, dv.y, dv.z, dv.w, wide_nl, pc);
+                        } else {
+                            x = digit_residue(dig[t], pc);
+                        }
+                        y = shoup_mul(x, w[u].x, w[u].y, pc.p);
+                    }
+                    tb[padi(e)] = x;
+                    tb[padi(e + kk)] = y;
+                }
+            }
         }
     };
     if (A.dual) {
@@ -1193,7 +1209,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
             const bool act = q < A.P;
             const int qq = act ? q : q0;
             const Span sp{act ? threadIdx.x - hsel * halfT : 0x7fffffffu, halfT};
-            const PrimeC pc = A.pcs[qq];
+            const PrimeC pc = s_pcs[qq];
             residues(qq, tb, sp);
             __syncthreads();
             x_transform<true>(tb, A.lgL - 1, cbits, A.twx + (int64_t)qq * L, pc.p, pc.two_p, sp);
@@ -1212,7 +1228,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
         return;
     }
     for (int q = 0; q < A.P; ++q) {
-        const PrimeC pc = A.pcs[q];
+        const PrimeC pc = s_pcs[q];
         const TwRows tw{A.twx + (int64_t)q * L, A.twy + (int64_t)q * A.twy_stride, A.lgL};
         residues(q, tile, cta_span());
         __syncthreads();
