@@ -111,6 +111,8 @@ struct Ctx {
     cudaEvent_t user_ev[16] = {};
     DevBuf flush;
     cudaStream_t aux = nullptr;          // H2D of operand B and the chunked D2H of the product
+    cudaStream_t low2 = nullptr;         // tc_multiply_host: B's first-pass chunks beside A's forward passes
+    cudaEvent_t cev[20] = {};            // its upload-chunk events (A: 0..7, B: 8..15) and joins (16..)
     cudaEvent_t xev[24] = {};            // cross-stream events of tc_multiply_host: 0 A up, 1 widths back, 2.. chunks, 20 B up, 21 A width
     int* hinfo = nullptr;                // pinned: widths read back early
     cudaEvent_t fev[2] = {};             // fork / join of the resident pipeline's two branches
@@ -498,10 +500,12 @@ int make_geometry(const tc_plan_t* pl, Geometry& G, int world = 1) {
 }
 
 int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* words, int64_t d, int cw,
-               int check_range, uint32_t* grids, const ShardArgs& sh, cudaStream_t stream = nullptr) {
+               int check_range, uint32_t* grids, const ShardArgs& sh, cudaStream_t stream = nullptr,
+               int64_t x0 = 0, int64_t nx = -1) {
     cudaStream_t st = stream ? stream : c->st;
     LowArgs a{};
     a.sh = sh;
+    if (nx >= 0) { a.perm = 1; a.x0 = (uint32_t)x0; a.lgT = G.lgS - G.yl; }   // CTAs [x0, x0 + nx) of the permuted order
     a.src.words = words; a.src.d = d; a.src.cw = cw;
     a.src.K = G.K; a.src.lgK = G.lgK; a.src.M = (int)pl->M; a.src.N = pl->N;
     a.src.check_range = check_range; a.src.err = c->flags.as<int>();
@@ -515,7 +519,7 @@ int launch_low(Ctx* c, const Geometry& G, const tc_plan_t* pl, const uint64_t* w
     const int Rc = G.yl >= 1 ? 1 << (G.yl - 1) : 1;      // computed (even) rows, see k_low
     const uint32_t n = 1u << (G.lgL + G.yl);
     size_t smem = (size_t)Rc * G.K * (pl->M > 63 ? 16 : 8) + (size_t)Rc * 8 + (size_t)padded_words(n) * 4;
-    const int64_t ctas = sh.world > 1 ? sh.Tl : G.S / n;
+    const int64_t ctas = sh.world > 1 ? sh.Tl : (nx >= 0 ? nx : G.S / n);
     // a tile too large for two CTAs per SM gets 32 warps in one CTA
     const int lt = env_int("TC_LOW_THREADS", 0);
     // two primes side by side when a compact tile's radix-16 rounds fill at
@@ -1209,6 +1213,8 @@ int tc_ctx_create(int device, void** out) {
     for (auto& ev : c->xev) ok = ok && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
     for (auto& ev : c->fev) ok = ok && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) == cudaSuccess;
+    ok = ok && cudaStreamCreateWithFlags(&c->low2, cudaStreamNonBlocking) == cudaSuccess;
+    for (auto& ev : c->cev) ok = ok && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaHostAlloc((void**)&c->hinfo, 64, cudaHostAllocDefault) == cudaSuccess;
     if (!ok) {
         const cudaError_t e2 = cudaGetLastError();
@@ -1233,6 +1239,8 @@ int tc_ctx_destroy(void* ctx) {
     for (auto& ev : c->xev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : c->fev) if (ev) cudaEventDestroy(ev);
     if (c->aux) { cudaStreamSynchronize(c->aux); cudaStreamDestroy(c->aux); }
+    if (c->low2) { cudaStreamSynchronize(c->low2); cudaStreamDestroy(c->low2); }
+    for (auto& ev : c->cev) if (ev) cudaEventDestroy(ev);
     if (c->hinfo) cudaFreeHost(c->hinfo);
     for (auto& ev : c->ring_ev) if (ev) { cudaEventSynchronize(ev); cudaEventDestroy(ev); }
     if (c->ring) cudaFreeHost(c->ring);
@@ -1528,6 +1536,7 @@ int tc_multiply_host(void* ctx, const uint64_t* a, int64_t da, int32_t a_cw, int
         // none may outlive the call
         cudaStreamSynchronize(c->st);
         cudaStreamSynchronize(c->aux);
+        cudaStreamSynchronize(c->low2);
     }
     return rc;
 }
@@ -1554,34 +1563,62 @@ int multiply_host_impl(Ctx* c, const uint64_t* a, int64_t da, int32_t a_cw, int3
     uint32_t* GA = c->grids.as<uint32_t>();
     uint32_t* GB = GA + (size_t)G.P * G.S;
     const ShardArgs one = single_gpu();
-    // main: A's upload, width, first pass and forward high passes (A's whole
-    // forward transform: nothing of it waits for B); B's upload then goes out
-    // on the aux stream while A's kernels run (pageable sources are staged
-    // through the pinned ring by the host copy pool meanwhile)
+    // Both operands go up on the copy stream in chunks; the first pass (k_low)
+    // of the CTAs that read a chunk starts as soon as it has landed: A's on
+    // the main stream, followed by A's forward high passes (A's whole forward
+    // transform: nothing of it waits for B), B's on a third stream beside
+    // them.  Pageable sources are staged through the pinned ring by the host
+    // copy pool meanwhile.  Only B's high passes wait for the last byte.
     CK(cudaEventRecord(c->ev[0], c->st));
     CK(cudaMemsetAsync(wf, 0, 16, c->st));
-    if ((rc = stage_upload(c, c->in_a.p, a, (size_t)da * a_cw * 8, c->st))) return rc;
-    CK(cudaEventRecord(c->xev[0], c->st));            // A uploaded (and the width flags cleared)
+    CK(cudaEventRecord(c->cev[16], c->st));            // tables, flags and width words ready
+    CK(cudaStreamWaitEvent(c->low2, c->cev[16], 0));
+    CK(cudaStreamWaitEvent(c->aux, c->cev[16], 0));
     const int nh = (int)G.high.size();
+    const int64_t Tl = G.S >> (G.lgL + G.yl);          // low-phase tiles
+    const int64_t Rh = G.yl >= 1 ? (1ll << (G.yl - 1)) : 1;   // coefficient rows a tile reads
+    static const int up_chunks = env_int("TC_UPLOAD_CHUNKS", 8);
+    auto upload_convert = [&](const uint64_t* host, void* dev, int64_t d, int cw, int check_range, uint32_t* grid,
+                              cudaStream_t kst, cudaEvent_t* evs) -> int {
+        const size_t rb = (size_t)cw * 8;
+        int nch = 1;
+        while (nch < up_chunks && nch < 8 && Tl / (2 * nch) >= 1 && (size_t)d * rb / (2 * nch) >= ((size_t)4 << 20)) nch *= 2;
+        const int64_t nx = Tl / nch;
+        for (int ch = 0; ch < nch; ++ch) {
+            // CTA x of the permuted order takes tile bitrev(x): coefficients x + Tl k, k < Rh
+            const int64_t x0 = ch * nx;
+            for (int64_t k = 0; k < Rh; ++k) {
+                const int64_t r0 = k * Tl + x0, r1 = r0 + nx < d ? r0 + nx : d;
+                int urc;
+                if (r1 > r0 && (urc = stage_upload(c, static_cast<char*>(dev) + r0 * rb,
+                                                   reinterpret_cast<const char*>(host) + r0 * rb, (size_t)(r1 - r0) * rb, c->aux)))
+                    return urc;
+            }
+            CK(cudaEventRecord(evs[ch], c->aux));
+            CK(cudaStreamWaitEvent(kst, evs[ch], 0));
+            int lrc;
+            if ((lrc = launch_low(c, G, plan, static_cast<const uint64_t*>(dev), d, cw, check_range, grid, one, kst, x0, nx)))
+                return lrc;
+        }
+        return TC_OK;
+    };
+    if ((rc = upload_convert(a, c->in_a.p, da, a_cw, a_bits > plan->N, GA, c->st, c->cev))) return rc;
     k_width<<<(unsigned)((da + 255) / 256), 256, 0, c->st>>>(c->a_dev, da, a_cw, wf);
     c->launches++;
     CKL();
     CK(cudaEventRecord(c->xev[21], c->st));           // A's width reduced
-    if ((rc = launch_low(c, G, plan, c->a_dev, da, a_cw, a_bits > plan->N, GA, one))) return rc;
     for (int i = 0; i < nh; ++i)
         if ((rc = launch_high(c, MODE_FWD, G, GA, nullptr, G.high[i].first, G.high[i].second, one))) return rc;
-    CK(cudaStreamWaitEvent(c->aux, c->xev[0], 0));     // B's DMA behind A's on the copy engine
-    if ((rc = stage_upload(c, c->in_b.p, b, (size_t)db * b_cw * 8, c->aux))) return rc;
-    CK(cudaEventRecord(c->xev[20], c->aux));
-    // aux: B's width, both widths back to the host
+    if ((rc = upload_convert(b, c->in_b.p, db, b_cw, b_bits > plan->N, GB, c->low2, c->cev + 8))) return rc;
+    CK(cudaEventRecord(c->cev[17], c->low2));          // B's first pass done
+    // copy stream: B's width, both widths back to the host
     k_width<<<(unsigned)((db + 255) / 256), 256, 0, c->aux>>>(c->b_dev, db, b_cw, wf + 2);
     c->launches++;
     CKL();
     CK(cudaStreamWaitEvent(c->aux, c->xev[21], 0));
     CK(cudaMemcpyAsync(c->hinfo, wf, 16, cudaMemcpyDeviceToHost, c->aux));
     CK(cudaEventRecord(c->xev[1], c->aux));
-    CK(cudaStreamWaitEvent(c->st, c->xev[20], 0));      // B uploaded
-    if ((rc = launch_low(c, G, plan, c->b_dev, db, b_cw, b_bits > plan->N, GB, one))) return rc;
+    CK(cudaStreamWaitEvent(c->st, c->cev[17], 0));
     CK(cudaEventRecord(c->ev[1], c->st));
     for (int i = 0; i + 1 < nh; ++i)
         if ((rc = launch_high(c, MODE_FWD, G, GB, nullptr, G.high[i].first, G.high[i].second, one))) return rc;

@@ -1090,6 +1090,7 @@ struct LowArgs {
     const uint2* twx; const uint2* twy; int64_t twy_stride;
     const PrimeC* pcs; int P;
     int dual;              // two primes side by side in two tile buffers (host-checked shape)
+    int perm, lgT; uint32_t x0;   // world == 1: CTA -> tile bitrev(x0 + blockIdx.x) (chunked launches)
     unsigned long long* prof;   // phase timers (PROF_LOW_*), or null
 };
 
@@ -1115,12 +1116,17 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
     __shared__ DigitScratch ds;
     __shared__ int s_nvalid;
     __shared__ PrimeC s_pcs[kMaxPrimes];
-    const uint32_t gtile = blockIdx.x + (uint32_t)A.sh.h0;     // global low-phase tile
+    // perm (one GPU, chunked uploads): CTA x0 + blockIdx.x takes tile bitrev(x)
+    // over lgT bits, whose rows hold the coefficients x + (s_y / 2^yl) k -- a
+    // range of CTAs reads a range of coefficients, so it can run as soon as
+    // that part of the operand is on the device
+    const uint32_t bx = A.perm ? bitrev(A.x0 + blockIdx.x, A.lgT) : blockIdx.x;
+    const uint32_t gtile = bx + (uint32_t)A.sh.h0;             // global low-phase tile
     const uint32_t pos0 = gtile * (uint32_t)R;
     const bool sharded = A.sh.world > 1;
     // per-prime destination: the full grid, or the packed exchange buffer
     auto dst = [&](int q) -> uint32_t* {
-        return sharded ? A.g + (int64_t)q * (A.sh.Tl << A.sh.TB) : A.g + (int64_t)q * A.S + (int64_t)blockIdx.x * n;
+        return sharded ? A.g + (int64_t)q * (A.sh.Tl << A.sh.TB) : A.g + (int64_t)q * A.S + (int64_t)bx * n;
     };
     if (threadIdx.x == 0) s_nvalid = 0;
     // the per-prime constants, once per CTA (each prime's pass starts from shared memory)

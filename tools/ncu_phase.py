@@ -5,8 +5,29 @@ import csv, sys, collections
 rows = csv.reader(open(sys.argv[1]))
 fname = ""; hdr = None; seen = set(); inst = collections.Counter(); stall = collections.Counter()
 per_line = {}
-RANGES = [(225, 470, "digits"), (640, 745, "x-round"), (746, 925, "y-round"), (926, 1000, "y-expand"), (1064, 1128, "k_low-body"), (1129, 1146, "k_low-residues"), (1147, 1218, "k_low-body"),
-          (1757, 1812, "crt"), (2126, 2178, "co-pieces"), (2179, 2335, "co-warp"), (2472, 2650, "k_final-body")]
+def _ranges():
+    """Line ranges of the kernels' phases, from the current source."""
+    import os, re
+    src = open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1612_05778_b200", "csrc",
+                            "tc_kernels.cuh")).read().split("\n")
+    def at(pat, start=0):
+        for i in range(start, len(src)):
+            if re.search(pat, src[i]): return i + 1
+        return len(src)
+    marks = [("digits", r"struct DigitSrc"), ("other0", r"static __global__ void __launch_bounds__\(256\) k_digits"),
+             ("generic-round", r"struct LanePerm"), ("x-round", r"void xct_round"), ("y-round", r"void yct_round"),
+             ("y-expand", r"void yct_expand_columns"), ("other1", r"struct TwRows"), ("k_low-body", r"struct LowArgs"),
+             ("k_high", r"enum \{ MODE_FWD"), ("crt", r"struct CrtConst"), ("other2", r"int div_m\("),
+             ("co-grouped", r"struct WordAcc"), ("co-pieces", r"void warp_term_pieces"), ("co-warp", r"void crt_convert_warp"),
+             ("co-words", r"void convert_out_words"), ("k_final-body", r"FinalArgs A, const __grid_constant__ CrtConst"),
+             ("other3", r"void k_unshard")]
+    pos = [(at(pat), name) for name, pat in marks]
+    out = []
+    for i, (ln, name) in enumerate(pos):
+        end = pos[i + 1][0] - 1 if i + 1 < len(pos) else len(src)
+        out.append((ln, end, name))
+    return out
+RANGES = _ranges()
 stall_kinds = collections.defaultdict(collections.Counter)
 for r in rows:
     if not r: continue
@@ -26,8 +47,8 @@ for r in rows:
     per_line[key] = (ni, ns, r[1], d)
 def cat(f, l):
     if f == "tc_field.cuh":
-        if 60 <= l <= 75: return "bfly-alu"
-        if l in (33, 34): return "shoup_mul"
+        if 44 <= l <= 70: return "bfly-alu"
+        if l in (39, 40): return "shoup_mul"
         return "field-other"
     if f == "tc_kernels.cuh":
         for lo, hi, name in RANGES:
