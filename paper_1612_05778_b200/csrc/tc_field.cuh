@@ -86,18 +86,17 @@ __device__ __forceinline__ uint32_t digit_residue(int64_t dg, const PrimeC& c) {
 // low nl = 3 (M <= 94) or 4 limbs d0..d3 of its two's complement: the value is
 // sum_k d_k 2^(32k) - [negative] 2^(32 nl), each limb times the fixed 2^(32k)
 // mod p (Shoup), no absolute value and no 128-bit arithmetic.
-__device__ __forceinline__ uint32_t digit_residue_limbs(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3, int nl,
+template <int NL>
+__device__ __forceinline__ uint32_t digit_residue_limbs(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3,
                                                         const PrimeC& c) {
     uint32_t t = d0 - __umulhi(d0, c.one_sh) * c.p;
     t = reduce_2p(t + shoup_mul(d1, c.c32, c.c32_sh, c.p), c.two_p);
     t = reduce_2p(t + shoup_mul(d2, c.c64, c.c64_sh, c.p), c.two_p);
-    uint32_t top = d2, nw = c.n96;
-    if (nl == 4) {
+    if constexpr (NL == 4) {
         t = reduce_2p(t + shoup_mul(d3, c.c96, c.c96_sh, c.p), c.two_p);
-        top = d3;
-        nw = c.n128;
+        return reduce_2p(t + ((int32_t)d3 < 0 ? c.n128 : 0u), c.two_p);
     }
-    return reduce_2p(t + ((int32_t)top < 0 ? nw : 0u), c.two_p);
+    return reduce_2p(t + ((int32_t)d2 < 0 ? c.n96 : 0u), c.two_p);
 }
 
 }  // namespace tc

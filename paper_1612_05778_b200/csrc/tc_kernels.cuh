@@ -1191,7 +1191,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_lo
                     if (coeff[r] >= 0) {
                         if (wide) {
                             const uint4 dv = reinterpret_cast<const uint4*>(dig2)[t];
-                            x = digit_residue_limbs(dv.x, dv.y, dv.z, dv.w, wide_nl, pc);
+                            if (wide_nl == 3) x = digit_residue_limbs<3>(dv.x, dv.y, dv.z, dv.w, pc);
+                            else x = digit_residue_limbs<4>(dv.x, dv.y, dv.z, dv.w, pc);
                         } else {
                             x = digit_residue(dig[t], pc);
                         }
@@ -2220,15 +2221,17 @@ __device__ __forceinline__ void warp_term_pieces(const FinalArgs& A, const CrtCo
 #pragma unroll
             for (int q = 1; q < P; ++q) rr[q] = reduce_2p(sm[q * stride + e], 2 * cc.p[q]);
         }
-        const int64_t flat = (int64_t)prow * L + j;
-        if (A.inject >= 0 && flat == A.inject) rr[0] = rr[0] ? rr[0] - 1 : cc.p[0] - 1;   // fault injection (tests)
-        if (A.inject_par >= 0 && flat == A.inject_par) {
+        if ((A.inject & A.inject_par) != -1) {            // fault injection (tests): uniform, off in products
+            const int64_t flat = (int64_t)prow * L + j;
+            if (A.inject >= 0 && flat == A.inject) rr[0] = rr[0] ? rr[0] - 1 : cc.p[0] - 1;
+            if (A.inject_par >= 0 && flat == A.inject_par) {
 #pragma unroll
-            for (int q = 0; q < P; ++q) rr[q] = (rr[q] + 1) % cc.p[q];
+                for (int q = 0; q < P; ++q) rr[q] = (rr[q] + 1) % cc.p[q];
+            }
         }
         const bool bad = crt_term<P>(rr, cc, x);
         if (real_row) {
-            if (bad) atomicMin(&A.err[2], (int)min(flat, (int64_t)0x7fffffff));
+            if (bad) atomicMin(&A.err[2], (int)min((int64_t)prow * L + j, (int64_t)0x7fffffff));
             if (j == L - 1 && !bad) {      // the term 2K-1 must vanish (tc/_kernels.py:416-417)
                 uint32_t nz = 0;
 #pragma unroll
