@@ -2017,9 +2017,20 @@ __device__ __forceinline__ void crt_convert_grouped(const FinalArgs& A, const Cr
                     for (int q = 1; q < P; ++q) rr[q] = reduce_2p(sm[q * stride + e], 2 * cc.p[q]);
                     if (A.inject >= 0 && (int64_t)prow * L + j == A.inject)
                         rr[0] = rr[0] ? rr[0] - 1 : cc.p[0] - 1;     // fault injection (tests of the bound check)
+                    if (A.inject_par >= 0 && (int64_t)prow * L + j == A.inject_par) {
+#pragma unroll
+                        for (int q = 0; q < P; ++q) rr[q] = (rr[q] + 1) % cc.p[q];
+                    }
                     const bool bad = crt_term<P>(rr, cc, x);
-                    if (bad && prow < A.rows_out)
-                        atomicMin(&A.err[2], (int)min((int64_t)prow * L + j, (int64_t)0x7fffffff));
+                    if (prow < A.rows_out) {
+                        if (bad) atomicMin(&A.err[2], (int)min((int64_t)prow * L + j, (int64_t)0x7fffffff));
+                        if (j == L - 1 && !bad) {                 // the term 2K-1 must vanish (tc/_kernels.py:416-417)
+                            uint32_t nz = 0;
+#pragma unroll
+                            for (int l = 0; l < P; ++l) nz |= x[l];
+                            if (nz) atomicMin(&A.err[3], (int)prow);
+                        }
+                    }
                     x[P - 1] ^= 0x80000000u;                      // biased: c_ij + 2^(32P-1) >= 0
                 } else {                                          // biased limbs from the in-place CRT pass
 #pragma unroll
