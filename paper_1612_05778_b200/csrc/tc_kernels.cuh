@@ -69,6 +69,12 @@ constexpr int kMaxPrimes = 16;
 #ifndef TC_MID_BATCH
 #define TC_MID_BATCH 8      // k_high_ct MID: 16-byte loads of A in flight per thread (8: C2 MID 168 -> 157 us)
 #endif
+#ifndef TC_LOW_MINB256
+#define TC_LOW_MINB256 4    // 256-thread k_low CTAs per SM the register budget is sized for
+#endif
+#ifndef TC_FINAL_MINB256
+#define TC_FINAL_MINB256 4  // 256-thread k_final CTAs per SM the register budget is sized for
+#endif
 #ifndef TC_ROUND_G2
 #define TC_ROUND_G2 1       // interleave two register groups per round when each thread owns >= 2
 #endif
@@ -1095,7 +1101,7 @@ struct LowArgs {
 };
 
 template <int NT>
-__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_low(LowArgs A) {
+__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? TC_LOW_MINB256 : 2)) k_low(LowArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int R = 1 << A.yl;                 // row positions in the tile
     // Odd positions hold coefficients >= s_y/2 >= d: zero rows.  With yl >= 1
@@ -2561,7 +2567,7 @@ __device__ __forceinline__ void convert_out_words(const FinalArgs& A, const uint
 }
 
 template <int P, bool DUMP, int NT>
-__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2)) k_final(FinalArgs A, const __grid_constant__ CrtConst cc) {
+__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? TC_FINAL_MINB256 : 2)) k_final(FinalArgs A, const __grid_constant__ CrtConst cc) {
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int s_any;
     const int R = 1 << A.yl;
