@@ -1581,13 +1581,18 @@ int multiply_host_impl(Ctx* c, const uint64_t* a, int64_t da, int32_t a_cw, int3
     auto upload_convert = [&](const uint64_t* host, void* dev, int64_t d, int cw, int check_range, uint32_t* grid,
                               cudaStream_t kst, cudaEvent_t* evs) -> int {
         const size_t rb = (size_t)cw * 8;
+        // a chunk is Rh pieces of Tl / nch rows (one per coefficient row of the tiles): chunk only
+        // while a piece stays >= 2 MiB (C4's tiles read 1024 rows 8 bytes wide: one copy)
         int nch = 1;
-        while (nch < up_chunks && nch < 8 && Tl / (2 * nch) >= 1 && (size_t)d * rb / (2 * nch) >= ((size_t)4 << 20)) nch *= 2;
+        while (nch < up_chunks && nch < 8 && Tl / (2 * nch) >= 1 && (size_t)(Tl / (2 * nch)) * rb >= ((size_t)2 << 20) &&
+               (size_t)d * rb / (2 * nch) >= ((size_t)4 << 20)) nch *= 2;
         const int64_t nx = Tl / nch;
         for (int ch = 0; ch < nch; ++ch) {
             // CTA x of the permuted order takes tile bitrev(x): coefficients x + Tl k, k < Rh
             const int64_t x0 = ch * nx;
-            for (int64_t k = 0; k < Rh; ++k) {
+            int urc0;
+            if (nch == 1 && (urc0 = stage_upload(c, dev, host, (size_t)d * rb, c->aux))) return urc0;
+            for (int64_t k = 0; nch > 1 && k < Rh; ++k) {
                 const int64_t r0 = k * Tl + x0, r1 = r0 + nx < d ? r0 + nx : d;
                 int urc;
                 if (r1 > r0 && (urc = stage_upload(c, static_cast<char*>(dev) + r0 * rb,
