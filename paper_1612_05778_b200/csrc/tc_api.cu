@@ -822,6 +822,8 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
             if (rc) return rc;
             A.cw_aw = waw; A.cw_b = wb; A.nbtab = c->nbtab.as<uint32_t>();
             A.co_aw = 0;
+            static const int co64 = env_int("TC_CO_BLOCK64", 1);
+            A.co64 = co64 && waw == 2 && wb == 1 && G.P <= 6 && G.lgL >= 6;
         }
     }
     const uint32_t n = 1u << (G.lgL + G.yl);

@@ -1923,6 +1923,7 @@ struct FinalArgs {
     int cw_aw, cw_b;               // > 0: warp-group CRT + ConvertOut (crt_convert_warp), M = 32 cw_aw + cw_b
     const uint32_t* nbtab;         // its bias tables: 2 x (32 cw_aw + cw_b) words (first group / later groups)
     int ld4;                       // tile loads: four cp.async per address computation
+    int co64;                      // M = 65, P <= 6, L >= 64: crt_convert_block64 instead of crt_convert_warp
     int fuse0;                     // with multi + the warp CRT: y level 0 folded into the CRT's reads
     int multi;                     // transforms: every round over all P tiles at once (one barrier per round)
     unsigned long long* prof;      // phase timers (PROF_FIN_*), or null
@@ -2212,11 +2213,13 @@ struct WarpCoShape {
 
 // Pieces of lane's term j of the tile row at rowbase (virtual terms j >= L:
 // biased zeros).  Reports bound / parity errors of real product rows.
-template <int P, int B>
-__device__ __forceinline__ void warp_term_pieces(const FinalArgs& A, const CrtConst& cc, const uint32_t* sm,
-                                                 uint32_t stride, uint32_t rowbase, int j, int L, uint32_t prow,
-                                                 bool real_row, uint32_t (&pc)[P + B], bool fuse0 = false) {
-    uint32_t x[P];
+// The biased P-limb term j of the tile row at rowbase: c_ij + 2^(32P-1) >= 0
+// (virtual terms j >= L: biased zeros).  Reports bound / parity errors of real
+// product rows.
+template <int P>
+__device__ __forceinline__ void warp_term_limbs(const FinalArgs& A, const CrtConst& cc, const uint32_t* sm,
+                                                uint32_t stride, uint32_t rowbase, int j, int L, uint32_t prow,
+                                                bool real_row, uint32_t (&x)[P], bool fuse0) {
     if (j < L) {
         uint32_t rr[P];
         const uint32_t e = padi(rowbase + (uint32_t)j);
@@ -2261,6 +2264,15 @@ __device__ __forceinline__ void warp_term_pieces(const FinalArgs& A, const CrtCo
         for (int l = 0; l < P; ++l) x[l] = 0u;
     }
     x[P - 1] ^= 0x80000000u;                              // biased: c_ij + 2^(32P-1) >= 0
+}
+
+// Pieces of lane's term j (crt_convert_warp): the biased term shifted by B (j mod 32) bits.
+template <int P, int B>
+__device__ __forceinline__ void warp_term_pieces(const FinalArgs& A, const CrtConst& cc, const uint32_t* sm,
+                                                 uint32_t stride, uint32_t rowbase, int j, int L, uint32_t prow,
+                                                 bool real_row, uint32_t (&pc)[P + B], bool fuse0 = false) {
+    uint32_t x[P];
+    warp_term_limbs<P>(A, cc, sm, stride, rowbase, j, L, prow, real_row, x, fuse0);
     const int r = B ? (j & 31) : 0;
 #pragma unroll
     for (int k = 0; k < P + B; ++k) {
@@ -2426,6 +2438,189 @@ __device__ __forceinline__ void crt_convert_warp(const FinalArgs& A, const CrtCo
                     if (v != 0u) break;
                 }
             }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Block CRT + ConvertOut for M = 65 (P <= 6, L >= 64): the form of
+// crt_convert_warp with 64-bit digits and two consecutive terms per lane.
+// A warp takes 64 consecutive terms of a row ("block" b: lane i lifts terms
+// 64 b + 2 i and + 1).  Term j sits at bit 65 j, so the pair is
+// W = (T0 + T1 2^65) 2^(2i) at the 64-bit digit 65 b + 2 i of the row: five
+// digits d0..d4 (T < 2^192: W < 2^319), of which lane i owns the first two and
+// hands d2, d3 to lane i + 1 and d4 to lane i + 2 (6 shuffles per pair of terms
+// against 24 in crt_convert_warp); a block is exactly 65 digits, the last one
+// (lane 31's third) collecting d2 of lane 31 and d4 of lane 30, and lane 31's
+// d3, d4 open the next block.  The digit sums (with carry counts) resolve as
+// in crt_convert_warp: t_w = lo(S_w) + count(S_(w-1)), generate / propagate,
+// one ballot add per block, a running carry across the warp's blocks.  A warp
+// works a contiguous segment of a row's blocks with no warm-up: what flows
+// into a segment's first two digits from the block before it (lane 31's d3,
+// d4, the last digit's carry count and the binary carry) is published by the
+// previous segment's warp and added after a barrier -- the held-back digits go
+// out as atomic adds onto zeroed words, so a carry rippling out of one fix-up
+// into another's words commutes with it.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void acc64_add(uint32_t& lo, uint32_t& hi, uint32_t& cnt, uint64_t v) {
+    asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, 0;"
+        : "+r"(lo), "+r"(hi), "+r"(cnt) : "r"((uint32_t)v), "r"((uint32_t)(v >> 32)));
+}
+__device__ __forceinline__ uint64_t shfl_up64(uint64_t v, int d) {
+    const uint32_t lo = __shfl_up_sync(0xffffffffu, (uint32_t)v, d), hi = __shfl_up_sync(0xffffffffu, (uint32_t)(v >> 32), d);
+    return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t shfl_idx64(uint64_t v, int l) {
+    const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, l), hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), l);
+    return ((uint64_t)hi << 32) | lo;
+}
+// row[w..] += v (32-bit words, w < W32), carries rippling on; every step an atomic add
+__device__ __forceinline__ void atomic_ripple_add(uint32_t* row, int64_t w, int64_t W32, uint32_t v) {
+    while (v && w < W32) {
+        const uint32_t old = atomicAdd(row + w, v);
+        v = (uint32_t)(old + v) < v ? 1u : 0u;
+        ++w;
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void crt_convert_block64(const FinalArgs& A, const CrtConst& cc, const uint32_t* sm,
+                                                    uint32_t stride, int R, uint32_t pos0, bool sharded, bool fuse0) {
+    static_assert(P <= 6, "five digits per pair of terms");
+    constexpr int GW = 65, BW = 2 * GW;                  // words per group of 32 / block of 64 terms
+    __shared__ uint32_t nbw[2][BW];                      // bias words of a row's first block / the later blocks
+    __shared__ uint64_t seg_pub[32][3];                  // per warp: lane 31's d3, d4 of its last block; count + carry
+    __shared__ uint64_t seg_hold[32][2];                 // per warp: the held-back first two digits of its segment
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int L = 1 << A.lgL, nblk = (L >> 6) + 1;       // + the virtual block that flushes the tail
+    const int64_t W32 = A.W32;
+    for (int i = threadIdx.x; i < 2 * BW; i += blockDim.x) {
+        const int f = i / BW, w = i % BW;                // nbtab: GW words of the first group, GW of the later ones
+        nbw[f][w] = __ldg(A.nbtab + (w < GW ? (f == 0 ? w : GW + w) : GW + (w - GW)));
+    }
+    __syncthreads();
+    const int wpr = nw > R ? nw / R : 1;                 // warps per row
+    const int nseg = wpr < nblk ? wpr : nblk;            // segments per row: every one holds >= 1 block
+    const int rstride = nw > R ? R : nw;
+    int r = nw > R ? warp / wpr : warp;
+    const int seg = nw > R ? warp % wpr : 0;
+    const bool idle = seg >= nseg || (nw > R && warp >= wpr * R);   // warps beyond a row's segments / the last row
+    const int ba = idle ? 0 : (int)(((int64_t)nblk * seg) / nseg), bb = idle ? 0 : (int)(((int64_t)nblk * (seg + 1)) / nseg);
+    uint32_t* seg_row = nullptr;
+    for (; !idle && r < R; r += rstride) {
+        const uint32_t prow = bitrev(pos0 + (uint32_t)r, A.lgS);
+        if (prow >= A.rows_out) continue;                // zero padding row
+        const uint32_t rowbase = (uint32_t)r << A.lgL;
+        uint32_t* orow = A.out + (int64_t)(sharded ? prow >> A.sh.lw : prow) * W32;
+        seg_row = orow;
+        uint64_t co0 = 0, co1 = 0;                       // lane 31's d3, d4 of the previous block
+        uint32_t hprev = 0, cyin = 0;                    // its last digit's carry count; the binary carry
+        for (int b = ba; b < bb; ++b) {
+            const int j0 = 64 * b + 2 * lane;
+            uint32_t w[10];
+            {
+                uint32_t x0[P], x1[P];
+                warp_term_limbs<P>(A, cc, sm, stride, rowbase, j0, L, prow, true, x0, fuse0);
+                warp_term_limbs<P>(A, cc, sm, stride, rowbase, j0 + 1, L, prow, true, x1, fuse0);
+                // U0 = T0 << 2i (words 0..7), U1 = T1 << (2i + 1) two words up (the 64 of 65)
+                const int s0 = 2 * lane, s1 = s0 + 1;
+                uint32_t v0[8], v1[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t lo0 = (k >= 1 && k - 1 < P) ? x0[(k >= 1 && k - 1 < P) ? k - 1 : 0] : 0u;
+                    const uint32_t hi0 = k < P ? x0[k < P ? k : 0] : 0u;
+                    v0[k] = __funnelshift_l(lo0, hi0, s0 & 31);
+                    const uint32_t lo1 = (k >= 1 && k - 1 < P) ? x1[(k >= 1 && k - 1 < P) ? k - 1 : 0] : 0u;
+                    const uint32_t hi1 = k < P ? x1[k < P ? k : 0] : 0u;
+                    v1[k] = __funnelshift_l(lo1, hi1, s1 & 31);
+                }
+                uint32_t a0[8], a1[8];
+                const bool up0 = s0 >= 32, up1 = s1 >= 32;      // a whole word more
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    a0[k] = up0 ? (k >= 1 ? v0[k >= 1 ? k - 1 : 0] : 0u) : v0[k];
+                    a1[k] = up1 ? (k >= 1 ? v1[k >= 1 ? k - 1 : 0] : 0u) : v1[k];
+                }
+                // W = U0 + (U1 << 64): ten words
+                w[0] = a0[0]; w[1] = a0[1];
+                asm("add.cc.u32 %0, %8, %14;\n\t"
+                    "addc.cc.u32 %1, %9, %15;\n\t"
+                    "addc.cc.u32 %2, %10, %16;\n\t"
+                    "addc.cc.u32 %3, %11, %17;\n\t"
+                    "addc.cc.u32 %4, %12, %18;\n\t"
+                    "addc.cc.u32 %5, %13, %19;\n\t"
+                    "addc.cc.u32 %6, %20, 0;\n\t"
+                    "addc.u32 %7, %21, 0;"
+                    : "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]), "=r"(w[8]), "=r"(w[9])
+                    : "r"(a0[2]), "r"(a0[3]), "r"(a0[4]), "r"(a0[5]), "r"(a0[6]), "r"(a0[7]),
+                      "r"(a1[0]), "r"(a1[1]), "r"(a1[2]), "r"(a1[3]), "r"(a1[4]), "r"(a1[5]), "r"(a1[6]), "r"(a1[7]));
+            }
+            const uint64_t d2 = ((uint64_t)w[5] << 32) | w[4], d3 = ((uint64_t)w[7] << 32) | w[6],
+                           d4 = ((uint64_t)w[9] << 32) | w[8];
+            const uint64_t r1a = shfl_up64(d2, 1), r1b = shfl_up64(d3, 1), r2 = shfl_up64(d4, 2), rE = shfl_up64(d4, 1);
+            const uint32_t* nb = nbw[b == 0 ? 0 : 1];
+            // digit sums with carry counts: S0 (digit 2i), S1 (2i + 1), SE (lane 31: digit 64)
+            uint32_t s0l = w[0], s0h = w[1], k0 = 0, s1l = w[2], s1h = w[3], k1 = 0;
+            acc64_add(s0l, s0h, k0, ((uint64_t)nb[4 * lane + 1] << 32) | nb[4 * lane]);
+            acc64_add(s0l, s0h, k0, lane >= 1 ? r1a : co0);
+            acc64_add(s0l, s0h, k0, lane >= 2 ? r2 : 0ull);
+            acc64_add(s1l, s1h, k1, ((uint64_t)nb[4 * lane + 3] << 32) | nb[4 * lane + 2]);
+            acc64_add(s1l, s1h, k1, lane >= 1 ? r1b : co1);
+            uint32_t sel = (uint32_t)d2, seh = (uint32_t)(d2 >> 32), kE = 0;
+            acc64_add(sel, seh, kE, ((uint64_t)nb[129] << 32) | nb[128]);
+            acc64_add(sel, seh, kE, rE);
+            // carry terms t = lo(S) + count of the digit below
+            uint32_t hin = __shfl_up_sync(0xffffffffu, k1, 1);
+            if (lane == 0) hin = hprev;
+            uint32_t g0 = 0, g1 = 0, gE = 0;
+            acc64_add(s0l, s0h, g0, (uint64_t)hin);
+            acc64_add(s1l, s1h, g1, (uint64_t)k0);
+            acc64_add(sel, seh, gE, (uint64_t)k1);
+            const uint32_t p0 = (s0l & s0h) == 0xffffffffu, p1 = (s1l & s1h) == 0xffffffffu, pE = (sel & seh) == 0xffffffffu;
+            uint32_t gl = g1 | (p1 & g0), pl = p0 & p1;
+            if (lane == 31) { gl = gE | (pE & gl); pl &= pE; }
+            const unsigned G1 = __ballot_sync(0xffffffffu, gl);
+            const unsigned P1 = __ballot_sync(0xffffffffu, pl & !gl);
+            const uint64_t Am = (uint64_t)(G1 | P1), Bm = (uint64_t)G1, sum = Am + Bm + cyin;
+            const uint32_t c = (uint32_t)((sum ^ Am ^ Bm) >> lane) & 1u;
+            cyin = (uint32_t)(sum >> 32) & 1u;
+            const uint32_t c1 = g0 | (p0 & c), c2 = g1 | (p1 & c1);
+            const uint64_t f0 = (((uint64_t)s0h << 32) | s0l) + c, f1 = (((uint64_t)s1h << 32) | s1l) + c1,
+                           fE = (((uint64_t)seh << 32) | sel) + c2;
+            const int64_t wb = (int64_t)BW * b + 4 * lane;
+            const bool hold = b == ba && ba > 0 && lane == 0;      // fixed up after the barrier
+            if (hold) { seg_hold[warp][0] = f0; seg_hold[warp][1] = f1; }
+            if (wb < W32) orow[wb] = hold ? 0u : (uint32_t)f0;
+            if (wb + 1 < W32) orow[wb + 1] = hold ? 0u : (uint32_t)(f0 >> 32);
+            if (wb + 2 < W32) orow[wb + 2] = hold ? 0u : (uint32_t)f1;
+            if (wb + 3 < W32) orow[wb + 3] = hold ? 0u : (uint32_t)(f1 >> 32);
+            if (lane == 31) {
+                const int64_t we = (int64_t)BW * b + 128;
+                if (we < W32) orow[we] = (uint32_t)fE;
+                if (we + 1 < W32) orow[we + 1] = (uint32_t)(fE >> 32);
+            }
+            co0 = shfl_idx64(d3, 31);
+            co1 = shfl_idx64(d4, 31);
+            hprev = __shfl_sync(0xffffffffu, kE, 31);
+        }
+        if (lane == 0) { seg_pub[warp][0] = co0; seg_pub[warp][1] = co1; seg_pub[warp][2] = (uint64_t)hprev + cyin; }
+    }
+    if (nseg > 1) {
+        __syncthreads();
+        if (lane == 0 && !idle && seg > 0 && seg_row != nullptr) {
+            // X0 = held digit 0 + d3 + count + carry of the segment before; X1 = held digit 1 + d4 + carries
+            uint32_t x0l = (uint32_t)seg_hold[warp][0], x0h = (uint32_t)(seg_hold[warp][0] >> 32), q0 = 0;
+            acc64_add(x0l, x0h, q0, seg_pub[warp - 1][0]);
+            acc64_add(x0l, x0h, q0, seg_pub[warp - 1][2]);
+            uint32_t x1l = (uint32_t)seg_hold[warp][1], x1h = (uint32_t)(seg_hold[warp][1] >> 32), q1 = 0;
+            acc64_add(x1l, x1h, q1, seg_pub[warp - 1][1]);
+            acc64_add(x1l, x1h, q1, (uint64_t)q0);
+            const int64_t w0 = (int64_t)BW * ba;
+            atomic_ripple_add(seg_row, w0, W32, x0l);
+            atomic_ripple_add(seg_row, w0 + 1, W32, x0h);
+            atomic_ripple_add(seg_row, w0 + 2, W32, x1l);
+            atomic_ripple_add(seg_row, w0 + 3, W32, x1h);
+            atomic_ripple_add(seg_row, w0 + 4, W32, q1);
         }
     }
 }
@@ -2679,6 +2874,12 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? TC_FINAL_MIN
     }
     // warp-group CRT + ConvertOut (M = 32 AW + {0, 1}, host-checked shape)
     const bool warp_co = A.cw_aw > 0;
+    if constexpr (!DUMP && P <= 6) {
+        if (A.co64 && A.cw_aw == 2 && A.cw_b == 1 && A.prof == nullptr) {
+            crt_convert_block64<P>(A, cc, sm, stride, R, pos0, sharded, fuse0);
+            return;
+        }
+    }
     if constexpr (!DUMP && P <= 8) {
         if (A.cw_aw == 2) {
             if (A.cw_b) crt_convert_warp<P, 2, 1>(A, cc, sm, stride, R, pos0, sharded, fuse0);

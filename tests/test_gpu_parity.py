@@ -449,6 +449,40 @@ def test_two_word_digits(oracle):
         tc.multiply_with_plan(tc.MulRequest(a, a), K=2, M=100)
 
 
+def test_block_convert_out_carry_chains(oracle):
+    # M = 65 with rows of >= 64 terms (crt_convert_block64: 64-term blocks, 64-bit digits, segments
+    # fixed up after a barrier): operands whose products carry across every block and segment boundary
+    # (all-ones and sign-alternating coefficients), few rows (many segments per row) and many, P = 3..6
+    rng = random.Random(6564)
+    def const_poly(d, nbits, pattern):
+        limbs = -(-nbits // 64)
+        w = np.zeros((d, limbs), dtype=np.uint64)
+        for i in range(d):
+            v = pattern(i)
+            v &= (1 << (64 * limbs)) - 1
+            for k in range(limbs):
+                w[i, k] = (v >> (64 * k)) & 0xFFFFFFFFFFFFFFFF
+        return _poly(w, nbits)
+    cases = [(1, 1, 2070, 32), (2, 1, 4150, 64), (3, 3, 4100, 64), (1, 2, 66000, 1024), (5, 4, 33000, 512),
+             (40, 33, 8300, 128), (300, 7, 2070, 32), (1, 1, 16600, 256)]
+    for da, db, nbits, K in cases:
+        top = (1 << (nbits - 1)) - 1
+        pats = [(lambda i: top, lambda i: top), (lambda i: -top, lambda i: top),
+                (lambda i: top if i % 2 else -top, lambda i: -top - 1 + (i % 3)),
+                (lambda i: (1 << (nbits - 2)) + i, lambda i: -1 - i)]
+        for pa, pb in pats:
+            a, b = const_poly(da, nbits, pa), const_poly(db, nbits, pb)
+            out, _, plan = tc.multiply_with_plan(tc.MulRequest(a, b), K=K, M=65)
+            assert plan.M == 65 and plan.K == K, plan.describe()
+            exp, bits = oracle.multiply_words(a.words, a.bit_width, b.words, b.bit_width)
+            assert out.bit_width == bits and np.array_equal(out.words, exp), (da, db, nbits, plan.describe())
+        a = _random_poly(rng, da, nbits, extremes=True)
+        b = _random_poly(rng, db, nbits, extremes=True)
+        out, _, plan = tc.multiply_with_plan(tc.MulRequest(a, b), K=K, M=65)
+        exp, bits = oracle.multiply_words(a.words, a.bit_width, b.words, b.bit_width)
+        assert out.bit_width == bits and np.array_equal(out.words, exp), (da, db, nbits, plan.describe())
+
+
 def test_plan_sweep(oracle):
     # every transform length 2K = 2 .. 2^14 (the compile-time x schedules, the
     # fused twist / duplication rounds, k_high_ct / generic passes), degrees
