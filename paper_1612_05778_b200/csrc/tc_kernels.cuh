@@ -2488,7 +2488,7 @@ __device__ __forceinline__ void crt_convert_block64(const FinalArgs& A, const Cr
                                                     uint32_t stride, int R, uint32_t pos0, bool sharded, bool fuse0) {
     static_assert(P <= 6, "five digits per pair of terms");
     constexpr int GW = 65, BW = 2 * GW;                  // words per group of 32 / block of 64 terms
-    __shared__ uint32_t nbw[2][BW];                      // bias words of a row's first block / the later blocks
+    __shared__ __align__(8) uint32_t nbw[2][BW];         // bias words of a row's first block / the later blocks
     __shared__ uint64_t seg_pub[32][3];                  // per warp: lane 31's d3, d4 of its last block; count + carry
     __shared__ uint64_t seg_hold[32][2];                 // per warp: the held-back first two digits of its segment
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -2558,16 +2558,16 @@ __device__ __forceinline__ void crt_convert_block64(const FinalArgs& A, const Cr
             const uint64_t d2 = ((uint64_t)w[5] << 32) | w[4], d3 = ((uint64_t)w[7] << 32) | w[6],
                            d4 = ((uint64_t)w[9] << 32) | w[8];
             const uint64_t r1a = shfl_up64(d2, 1), r1b = shfl_up64(d3, 1), r2 = shfl_up64(d4, 2), rE = shfl_up64(d4, 1);
-            const uint32_t* nb = nbw[b == 0 ? 0 : 1];
+            const uint64_t* nb = reinterpret_cast<const uint64_t*>(nbw[b == 0 ? 0 : 1]);   // bias per digit
             // digit sums with carry counts: S0 (digit 2i), S1 (2i + 1), SE (lane 31: digit 64)
             uint32_t s0l = w[0], s0h = w[1], k0 = 0, s1l = w[2], s1h = w[3], k1 = 0;
-            acc64_add(s0l, s0h, k0, ((uint64_t)nb[4 * lane + 1] << 32) | nb[4 * lane]);
+            acc64_add(s0l, s0h, k0, nb[2 * lane]);
             acc64_add(s0l, s0h, k0, lane >= 1 ? r1a : co0);
             acc64_add(s0l, s0h, k0, lane >= 2 ? r2 : 0ull);
-            acc64_add(s1l, s1h, k1, ((uint64_t)nb[4 * lane + 3] << 32) | nb[4 * lane + 2]);
+            acc64_add(s1l, s1h, k1, nb[2 * lane + 1]);
             acc64_add(s1l, s1h, k1, lane >= 1 ? r1b : co1);
             uint32_t sel = (uint32_t)d2, seh = (uint32_t)(d2 >> 32), kE = 0;
-            acc64_add(sel, seh, kE, ((uint64_t)nb[129] << 32) | nb[128]);
+            acc64_add(sel, seh, kE, nb[64]);
             acc64_add(sel, seh, kE, rE);
             // carry terms t = lo(S) + count of the digit below
             uint32_t hin = __shfl_up_sync(0xffffffffu, k1, 1);
@@ -2590,14 +2590,22 @@ __device__ __forceinline__ void crt_convert_block64(const FinalArgs& A, const Cr
             const int64_t wb = (int64_t)BW * b + 4 * lane;
             const bool hold = b == ba && ba > 0 && lane == 0;      // fixed up after the barrier
             if (hold) { seg_hold[warp][0] = f0; seg_hold[warp][1] = f1; }
-            if (wb < W32) orow[wb] = hold ? 0u : (uint32_t)f0;
-            if (wb + 1 < W32) orow[wb + 1] = hold ? 0u : (uint32_t)(f0 >> 32);
-            if (wb + 2 < W32) orow[wb + 2] = hold ? 0u : (uint32_t)f1;
-            if (wb + 3 < W32) orow[wb + 3] = hold ? 0u : (uint32_t)(f1 >> 32);
-            if (lane == 31) {
-                const int64_t we = (int64_t)BW * b + 128;
-                if (we < W32) orow[we] = (uint32_t)fE;
-                if (we + 1 < W32) orow[we + 1] = (uint32_t)(fE >> 32);
+            const uint64_t o0 = hold ? 0ull : f0, o1 = hold ? 0ull : f1;
+            if ((int64_t)BW * (b + 1) <= W32 && !(W32 & 1)) {     // the whole block lies inside the row (rows are
+                uint64_t* o64 = reinterpret_cast<uint64_t*>(orow + wb);   // 8-byte aligned: W32 is even)
+                o64[0] = o0;
+                o64[1] = o1;
+                if (lane == 31) o64[2] = fE;
+            } else {
+                if (wb < W32) orow[wb] = (uint32_t)o0;
+                if (wb + 1 < W32) orow[wb + 1] = (uint32_t)(o0 >> 32);
+                if (wb + 2 < W32) orow[wb + 2] = (uint32_t)o1;
+                if (wb + 3 < W32) orow[wb + 3] = (uint32_t)(o1 >> 32);
+                if (lane == 31) {
+                    const int64_t we = (int64_t)BW * b + 128;
+                    if (we < W32) orow[we] = (uint32_t)fE;
+                    if (we + 1 < W32) orow[we + 1] = (uint32_t)(fE >> 32);
+                }
             }
             co0 = shfl_idx64(d3, 31);
             co1 = shfl_idx64(d4, 31);
@@ -2615,12 +2623,16 @@ __device__ __forceinline__ void crt_convert_block64(const FinalArgs& A, const Cr
             uint32_t x1l = (uint32_t)seg_hold[warp][1], x1h = (uint32_t)(seg_hold[warp][1] >> 32), q1 = 0;
             acc64_add(x1l, x1h, q1, seg_pub[warp - 1][1]);
             acc64_add(x1l, x1h, q1, (uint64_t)q0);
+            // five independent atomic adds in flight (the held words were zeroed: a carry out of one
+            // of them needs a ripple from another fix-up to have landed first), then the rare ripples
             const int64_t w0 = (int64_t)BW * ba;
-            atomic_ripple_add(seg_row, w0, W32, x0l);
-            atomic_ripple_add(seg_row, w0 + 1, W32, x0h);
-            atomic_ripple_add(seg_row, w0 + 2, W32, x1l);
-            atomic_ripple_add(seg_row, w0 + 3, W32, x1h);
-            atomic_ripple_add(seg_row, w0 + 4, W32, q1);
+            const uint32_t v[5] = {x0l, x0h, x1l, x1h, q1};
+            uint32_t old[5];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) old[k] = (v[k] && w0 + k < W32) ? atomicAdd(seg_row + w0 + k, v[k]) : 0u;
+#pragma unroll
+            for (int k = 0; k < 5; ++k)
+                if ((uint32_t)(old[k] + v[k]) < v[k]) atomic_ripple_add(seg_row, w0 + k + 1, W32, 1u);
         }
     }
 }
