@@ -654,7 +654,7 @@ __device__ __forceinline__ Span cta_span() { return Span{threadIdx.x, blockDim.x
 // all the primes ends with one barrier and every thread gets nq * ngroups /
 // threads independent groups.  ps: the primes (shared memory); the twiddle
 // tables of consecutive primes are twstride entries apart.
-struct Multi { int nq; uint32_t stride; int64_t twstride; const uint32_t* ps; };
+struct Multi { int nq; uint32_t stride; int64_t twstride; const uint32_t* ps; int rp2; };   // rp2: x rounds take two rows per thread
 
 template <int BL, int NB, bool DIF, bool MULTI = false>
 __device__ __forceinline__ void xct_round(uint32_t* s, int tile_bits, const uint2* twx, uint32_t p, uint32_t two_p,
@@ -665,6 +665,56 @@ __device__ __forceinline__ void xct_round(uint32_t* s, int tile_bits, const uint
     constexpr uint32_t pa = BL, pb = BL + 5 - NB;
     const uint32_t pm = (PERMC && tile_bits >= 10) ? (1u << (5 - BL)) - 1 : 0u;
     const uint32_t ngroups = 1u << (tile_bits - NB);
+    if constexpr (MULTI && NB <= 4) {
+        if (mq.rp2) {
+            // two rows per thread: the groups of rows r and r + R/2 (the top bit of the group index)
+            // share their twiddles, so one set of loads serves both butterfly chains
+            const uint32_t ng2 = ngroups >> 1, hs = (1u << (tile_bits - 1)) + (1u << (tile_bits - 6));
+            for (uint32_t g0 = span.t0; g0 < ng2 * (uint32_t)mq.nq; g0 += span.nt) {
+                const uint32_t q = g0 >> (tile_bits - NB - 1);
+                uint32_t g = g0 & (ng2 - 1);
+                p = mq.ps[q];
+                two_p = 2 * p;
+                if (PERMC) {
+                    const uint32_t t = ((g >> pa) ^ (g >> pb)) & pm;
+                    g ^= (t << pa) ^ (t << pb);
+                }
+                const uint32_t lo = g & lowmask;
+                uint32_t* sp = s + q * mq.stride + padi(((g & ~lowmask) << NB) | lo);
+                const uint2* tq = twx + (int64_t)q * mq.twstride + lo;
+                uint32_t x[2][R];
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    x[0][k] = sp[(k << BL) + ((k << BL) >> 5)];
+                    x[1][k] = sp[hs + (k << BL) + ((k << BL) >> 5)];
+                }
+#pragma unroll
+                for (int it = 0; it < NB; ++it) {
+                    const int lv = DIF ? NB - 1 - it : it;
+#pragma unroll
+                    for (int m = 0; m < (1 << lv); ++m) {
+                        const uint2 w = __ldg(tq + (1 << (BL + lv)) + (m << BL));
+#pragma unroll
+                        for (int jj = 0; jj < R / (2 << lv); ++jj) {
+                            const int k = m + jj * (2 << lv);
+#pragma unroll
+                            for (int u = 0; u < 2; ++u) {
+                                if (DIF) bfly_dif(x[u][k], x[u][k + (1 << lv)], w.x, w.y, p, two_p);
+                                else bfly_dit(x[u][k], x[u][k + (1 << lv)], w.x, w.y, p, two_p);
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    sp[(k << BL) + ((k << BL) >> 5)] = x[0][k];
+                    sp[hs + (k << BL) + ((k << BL) >> 5)] = x[1][k];
+                }
+            }
+            __syncthreads();
+            return;
+        }
+    }
     const uint32_t nitems = MULTI ? ngroups * (uint32_t)mq.nq : ngroups;
     for (uint32_t g0 = span.t0; g0 < nitems; g0 += span.nt) {
         uint32_t g = g0;
@@ -1923,6 +1973,7 @@ struct FinalArgs {
     int cw_aw, cw_b;               // > 0: warp-group CRT + ConvertOut (crt_convert_warp), M = 32 cw_aw + cw_b
     const uint32_t* nbtab;         // its bias tables: 2 x (32 cw_aw + cw_b) words (first group / later groups)
     int ld4;                       // tile loads: four cp.async per address computation
+    int rp2;                       // multi x rounds: two rows per thread (shared twiddles) where balanced
     int co64;                      // M = 65, P <= 6, L >= 64: crt_convert_block64 instead of crt_convert_warp
     int fuse0;                     // with multi + the warp CRT: y level 0 folded into the CRT's reads
     int multi;                     // transforms: every round over all P tiles at once (one barrier per round)
@@ -2832,7 +2883,10 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? TC_FINAL_MIN
         if (threadIdx.x < P) s_primes[threadIdx.x] = cc.p[threadIdx.x];
         cp_async_wait<0>();
         __syncthreads();
-        const Multi my{P, stride, A.twy_stride, s_primes}, mx{P, stride, (int64_t)L, s_primes};
+        // x rounds with two rows per thread where the tile has >= 2 rows and the (prime, column group)
+        // items of a radix-16 round divide evenly over the threads
+        const int rp2 = A.rp2 && A.yl >= 1 && tile_bits >= 11 && (((uint32_t)P << (tile_bits - 5)) % blockDim.x) == 0;
+        const Multi my{P, stride, A.twy_stride, s_primes, 0}, mx{P, stride, (int64_t)L, s_primes, rp2};
         y_transform<true, true>(sm, A.lgL, fuse0 ? 1 : 0, tile_bits, A.twy, 0u, 0u, cta_span(), my);   // y low: DIF
         x_transform<false, true>(sm, A.lgL, tile_bits, A.twx, 0u, 0u, cta_span(), mx);      // x: DIT
     } else if (dual) {
