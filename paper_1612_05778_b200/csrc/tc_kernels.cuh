@@ -1230,6 +1230,43 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? TC_LOW_MINB2
         const uint2* wtop = A.twx + (int64_t)q * L + (L >> 1);   // level lgL-1, entry 2^(lgL-1) + j
         const uint32_t kk = (uint32_t)A.src.K, nk = (uint32_t)Rc * kk;
         constexpr int UB = 4;                                    // twist twiddles in flight per thread
+        if (kk >= UB * sp.nt && !(sp.nt & 31u)) {              // (C2's K = nt keeps the flat loop: 144 vs 170 us)
+            // rows of >= nt digits: a thread walks columns j = t0 + u nt of one row at a time, so the
+            // row test, the digit / twiddle pointers and the padded tile addresses advance by constants
+            const uint32_t pstep = sp.nt + (sp.nt >> 5), koff = kk + (kk >> 5);
+            for (int r = 0; sp.t0 < sp.nt && r < Rc; ++r) {
+                const bool live = coeff[r] >= 0;
+                uint32_t* px = tb + padi(((uint32_t)r << A.lgL) + sp.t0);
+                const uint2* wt = wtop + sp.t0;
+                const uint4* dw = reinterpret_cast<const uint4*>(dig2) + (size_t)r * kk + sp.t0;
+                const int64_t* dn = dig + (size_t)r * kk + sp.t0;
+                for (uint32_t j = sp.t0; j < kk; j += UB * sp.nt, px += UB * pstep, wt += UB * sp.nt, dw += UB * sp.nt,
+                              dn += UB * sp.nt) {
+                    uint2 w[UB];
+#pragma unroll
+                    for (int u = 0; u < UB; ++u) w[u] = j + u * sp.nt < kk ? __ldg(wt + u * sp.nt) : make_uint2(0u, 0u);
+#pragma unroll
+                    for (int u = 0; u < UB; ++u) {
+                        if (j + u * sp.nt < kk) {
+                            uint32_t x = 0, y = 0;
+                            if (live) {
+                                if (wide) {
+                                    const uint4 dv = dw[u * sp.nt];
+                                    if (wide_nl == 3) x = digit_residue_limbs<3>(dv.x, dv.y, dv.z, dv.w, pc);
+                                    else x = digit_residue_limbs<4>(dv.x, dv.y, dv.z, dv.w, pc);
+                                } else {
+                                    x = digit_residue(dn[u * sp.nt], pc);
+                                }
+                                y = shoup_mul(x, w[u].x, w[u].y, pc.p);
+                            }
+                            px[u * pstep] = x;
+                            px[u * pstep + koff] = y;
+                        }
+                    }
+                }
+            }
+            return;
+        }
         for (uint32_t t0 = sp.t0; t0 < nk; t0 += UB * sp.nt) {
             uint2 w[UB];
 #pragma unroll
