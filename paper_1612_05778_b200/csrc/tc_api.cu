@@ -812,6 +812,8 @@ int launch_final(Ctx* c, const Geometry& G, const uint32_t* grids, int64_t rows,
         A.multi = fmulti;
         static const int frp2 = env_int("TC_FINAL_RP2", 1);
         A.rp2 = frp2;
+        static const int ffold = env_int("TC_FINAL_FOLDY0", 1);
+        A.fold_y0 = ffold;
         static const int ffuse0 = env_int("TC_FINAL_FUSE0", 1);
         // pays when it saves a whole round (yl = 1, 5, 9: C3 k_final 11.0 -> 10.3 ms; C2's yl = 4: +3 %)
         A.fuse0 = ffuse0 == 2 || (ffuse0 == 1 && G.yl % 4 == 1);

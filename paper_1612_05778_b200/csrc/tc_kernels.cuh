@@ -654,7 +654,8 @@ __device__ __forceinline__ Span cta_span() { return Span{threadIdx.x, blockDim.x
 // all the primes ends with one barrier and every thread gets nq * ngroups /
 // threads independent groups.  ps: the primes (shared memory); the twiddle
 // tables of consecutive primes are twstride entries apart.
-struct Multi { int nq; uint32_t stride; int64_t twstride; const uint32_t* ps; int rp2; };   // rp2: x rounds take two rows per thread
+struct Multi { int nq; uint32_t stride; int64_t twstride; const uint32_t* ps; int rp2; int fold_y0; };
+// rp2: x rounds take two rows per thread; fold_y0 = lgL: the round ending at bit lgL also does y level 0
 
 template <int BL, int NB, bool DIF, bool MULTI = false>
 __device__ __forceinline__ void xct_round(uint32_t* s, int tile_bits, const uint2* twx, uint32_t p, uint32_t two_p,
@@ -703,6 +704,16 @@ __device__ __forceinline__ void xct_round(uint32_t* s, int tile_bits, const uint
                                 else bfly_dit(x[u][k], x[u][k + (1 << lv)], w.x, w.y, p, two_p);
                             }
                         }
+                    }
+                }
+                if (mq.fold_y0 == BL + NB) {
+                    // two-row tiles: the last x round also runs the lowest inverse y level (rows 0 / 1,
+                    // twiddle 1) on the register pairs: (a, b) -> (a + b, a - b), lazily in [0, 4p)
+#pragma unroll
+                    for (int k = 0; k < R; ++k) {
+                        const uint32_t a = reduce_2p(x[0][k], two_p), b = reduce_2p(x[1][k], two_p);
+                        x[0][k] = a + b;
+                        x[1][k] = a - b + two_p;
                     }
                 }
 #pragma unroll
@@ -2010,6 +2021,7 @@ struct FinalArgs {
     int cw_aw, cw_b;               // > 0: warp-group CRT + ConvertOut (crt_convert_warp), M = 32 cw_aw + cw_b
     const uint32_t* nbtab;         // its bias tables: 2 x (32 cw_aw + cw_b) words (first group / later groups)
     int ld4;                       // tile loads: four cp.async per address computation
+    int fold_y0;                   // with rp2 on two-row tiles: y level 0 in the last x round
     int rp2;                       // multi x rounds: two rows per thread (shared twiddles) where balanced
     int co64;                      // M = 65, P <= 6, L >= 64: crt_convert_block64 instead of crt_convert_warp
     int fuse0;                     // with multi + the warp CRT: y level 0 folded into the CRT's reads
@@ -2912,7 +2924,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? TC_FINAL_MIN
     const bool dual = A.dual_ok && P >= 2 && A.lgL >= 5 && A.yl <= 12 && (n >> 4) <= halfT;
     __shared__ uint32_t s_primes[kMaxPrimes];
     // the lowest inverse y level (twiddle 1) folded into the CRT's reads (warp_term_pieces)
-    const bool fuse0 = !DUMP && P <= 8 && A.fuse0 && A.multi && P >= 2 && A.lgL >= 5 && A.yl >= 1 && A.yl <= 12 && A.cw_aw > 0;
+    bool fuse0 = !DUMP && P <= 8 && A.fuse0 && A.multi && P >= 2 && A.lgL >= 5 && A.yl >= 1 && A.yl <= 12 && A.cw_aw > 0;
     if (A.multi && P >= 2 && A.lgL >= 5 && A.yl <= 12) {
         // every round runs over the P tiles as one list of groups: one barrier
         // per round (not per round and prime pair) and P n / (16 threads)
@@ -2923,8 +2935,10 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? TC_FINAL_MIN
         // x rounds with two rows per thread where the tile has >= 2 rows and the (prime, column group)
         // items of a radix-16 round divide evenly over the threads
         const int rp2 = A.rp2 && A.yl >= 1 && tile_bits >= 11 && (((uint32_t)P << (tile_bits - 5)) % blockDim.x) == 0;
-        const Multi my{P, stride, A.twy_stride, s_primes, 0}, mx{P, stride, (int64_t)L, s_primes, rp2};
-        y_transform<true, true>(sm, A.lgL, fuse0 ? 1 : 0, tile_bits, A.twy, 0u, 0u, cta_span(), my);   // y low: DIF
+        const bool fold_x = rp2 && A.yl == 1 && A.fold_y0;      // level 0 in the last x round instead of the CRT reads
+        fuse0 = fuse0 && !fold_x;
+        const Multi my{P, stride, A.twy_stride, s_primes, 0, 0}, mx{P, stride, (int64_t)L, s_primes, rp2, fold_x ? A.lgL : 0};
+        y_transform<true, true>(sm, A.lgL, (fuse0 || fold_x) ? 1 : 0, tile_bits, A.twy, 0u, 0u, cta_span(), my);   // y low: DIF
         x_transform<false, true>(sm, A.lgL, tile_bits, A.twx, 0u, 0u, cta_span(), mx);      // x: DIT
     } else if (dual) {
         const int hsel = threadIdx.x >= halfT ? 1 : 0;
