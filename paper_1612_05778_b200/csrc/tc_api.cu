@@ -661,7 +661,9 @@ int launch_high(Ctx* c, int mode, const Geometry& G, uint32_t* grids, const uint
         if ((rc = high_tile_map(G, grids, G.lgL + u0, U, &mg))) return rc;
         if (mode == MODE_MID && (rc = high_tile_map(G, other, G.lgL + u0, U, &mo))) return rc;
         if (mode != MODE_MID) mo = mg;
-        static const int mid_ag = env_int("TC_MID_GLOBAL_A", 0);   // A via TMA: C3 MID 6.32 -> 6.10 ms
+        // A's tile read from global memory in the pointwise step: one tile buffer per CTA, 64 registers,
+        // 4 CTAs per SM instead of 3 with a second TMA buffer (C3 MID 6.26 -> 5.48 ms)
+        static const int mid_ag = env_int("TC_MID_GLOBAL_A", 1);
         cudaError_t e = mode == MODE_FWD ? launch_high_tma_mode<MODE_FWD, 8>(A, mg, mo, grid, c->st)
                       : mode == MODE_INV ? launch_high_tma_mode<MODE_INV, 8>(A, mg, mo, grid, c->st)
                       : mid_ag           ? launch_high_tma_mode<MODE_MID, 8, true>(A, mg, mo, grid, c->st)

@@ -69,6 +69,12 @@ constexpr int kMaxPrimes = 16;
 #ifndef TC_MID_BATCH
 #define TC_MID_BATCH 8      // k_high_ct MID: 16-byte loads of A in flight per thread (8: C2 MID 168 -> 157 us)
 #endif
+#ifndef TC_TMA_MINB
+#define TC_TMA_MINB 3       // FWD / INV TMA passes: CTAs per SM the register budget is sized for (they use 64: 4 resident)
+#endif
+#ifndef TC_MID_AG_MINB4
+#define TC_MID_AG_MINB4 1   // MID with A read from global memory: register budget for 4 CTAs per SM (C3 MID 6.26 -> 5.48 ms)
+#endif
 #ifndef TC_LOW_MINB256
 #define TC_LOW_MINB256 4    // 256-thread k_low CTAs per SM the register budget is sized for
 #endif
@@ -1791,7 +1797,7 @@ __device__ __forceinline__ void dense_pass(uint32_t* s, const uint2* stw, uint32
 }
 
 template <int MODE, int U, int NT, bool AG = false>
-__global__ void __launch_bounds__(NT, NT <= 256 ? 3 : 1)
+__global__ void __launch_bounds__(NT, NT <= 256 ? (MODE != MODE_MID ? TC_TMA_MINB : ((AG && TC_MID_AG_MINB4) ? 4 : 3)) : 1)
 k_high_tma(HighArgs A, const __grid_constant__ TmaMap mg, const __grid_constant__ TmaMap mo) {
     // AG (MODE_MID): A's tile read from global memory in the pointwise step
     // (16-byte loads, 8 in flight per thread) instead of a second TMA buffer
