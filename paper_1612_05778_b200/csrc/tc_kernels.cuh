@@ -2910,6 +2910,16 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? TC_FINAL_MIN
             const uint32_t* g = A.g + (int64_t)q * (A.sh.Tl << A.sh.TB);
             const XchgIdx xi{A.sh, blockIdx.x};
             for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) cp_async4(t + padi(e), g + xi(e));
+        } else if (A.ld4 && n >= 128 && !(blockDim.x & 31)) {
+            // four copies per address computation, conflict-free: a warp takes four consecutive
+            // 32-slot runs, lane l slot l of each (source +32 k words, padded destination +33 k)
+            const uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)tile * n;
+            const uint32_t lane = threadIdx.x & 31, nwp = blockDim.x >> 5;
+            for (uint32_t W = threadIdx.x >> 5; W < (n >> 7); W += nwp) {
+                uint32_t* d = t + 132u * W + lane;
+                const uint32_t* src = g + 128u * W + lane;
+                cp_async4(d, src); cp_async4(d + 33, src + 32); cp_async4(d + 66, src + 64); cp_async4(d + 99, src + 96);
+            }
         } else if (A.ld4 && n >= 4) {
             // four consecutive slots per address computation (one padded 32-slot run)
             const uint32_t* g = A.g + (int64_t)q * A.S + (int64_t)tile * n;
