@@ -69,6 +69,9 @@ constexpr int kMaxPrimes = 16;
 #ifndef TC_MID_BATCH
 #define TC_MID_BATCH 8      // k_high_ct MID: 16-byte loads of A in flight per thread (8: C2 MID 168 -> 157 us)
 #endif
+#ifndef TC_LOW_UB
+#define TC_LOW_UB 4         // k_low residues: digits / twist twiddles in flight per thread
+#endif
 #ifndef TC_TMA_MINB
 #define TC_TMA_MINB 3       // FWD / INV TMA passes: CTAs per SM the register budget is sized for (they use 64: 4 resident)
 #endif
@@ -1246,7 +1249,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? TC_LOW_MINB2
         const PrimeC pc = s_pcs[q];
         const uint2* wtop = A.twx + (int64_t)q * L + (L >> 1);   // level lgL-1, entry 2^(lgL-1) + j
         const uint32_t kk = (uint32_t)A.src.K, nk = (uint32_t)Rc * kk;
-        constexpr int UB = 4;                                    // twist twiddles in flight per thread
+        constexpr int UB = TC_LOW_UB;                            // twist twiddles in flight per thread
         if (kk >= UB * sp.nt && !(sp.nt & 31u)) {              // (C2's K = nt keeps the flat loop: 144 vs 170 us)
             // rows of >= nt digits: a thread walks columns j = t0 + u nt of one row at a time, so the
             // row test, the digit / twiddle pointers and the padded tile addresses advance by constants
