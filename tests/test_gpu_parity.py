@@ -483,6 +483,32 @@ def test_block_convert_out_carry_chains(oracle):
         assert out.bit_width == bits and np.array_equal(out.words, exp), (da, db, nbits, plan.describe())
 
 
+def test_chunked_upload_unbalanced(oracle):
+    # multiply() uploads large operands in chunks and starts the first pass of the CTAs that read a
+    # chunk as it lands (k_low in bit-reversed CTA order): unbalanced lengths, so chunks clip at d
+    # and whole chunks of the shorter operand are empty; pageable and page-locked sources
+    from paper_1612_05778_b200 import _lib
+    rng = np.random.default_rng(20000)
+    def rand_words(d, nbits):
+        limbs = -(-nbits // 64)
+        w = rng.integers(0, 2**64 - 1, endpoint=True, size=(d, limbs), dtype=np.uint64)
+        top = nbits - 64 * (limbs - 1)                      # sign-extend bit nbits-1 through the top limb
+        if top < 64:
+            sign = (w[:, -1] >> np.uint64(top - 1)) & np.uint64(1)
+            keep = (np.uint64(1) << np.uint64(top)) - np.uint64(1)
+            w[:, -1] = (w[:, -1] & keep) | np.where(sign == 1, ~keep, np.uint64(0))
+        return w
+    for da, db, nbits in [(20000, 3000, 16384), (2500, 18000, 20001)]:
+        aw, bw = rand_words(da, nbits), rand_words(db, nbits)
+        exp, bits = oracle.multiply_words(aw, nbits, bw, nbits)
+        out = tc.multiply(tc.MulRequest(_poly(aw, nbits), _poly(bw, nbits)))
+        assert out.bit_width == bits and np.array_equal(out.words, exp), (da, db, nbits)
+        pa = _lib.pinned.empty(aw.shape, np.uint64); pa[...] = aw
+        pb = _lib.pinned.empty(bw.shape, np.uint64); pb[...] = bw
+        out = tc.multiply(tc.MulRequest(tc.IntPolynomial._trusted(pa, nbits), tc.IntPolynomial._trusted(pb, nbits)))
+        assert out.bit_width == bits and np.array_equal(out.words, exp), (da, db, nbits, "pinned")
+
+
 def test_plan_sweep(oracle):
     # every transform length 2K = 2 .. 2^14 (the compile-time x schedules, the
     # fused twist / duplication rounds, k_high_ct / generic passes), degrees
