@@ -2592,22 +2592,27 @@ __device__ __forceinline__ void atomic_ripple_add(uint32_t* row, int64_t w, int6
     }
 }
 
+// bias words of a row's first block / the later blocks from nbtab (GW words of a row's first group of 32
+// terms, GW of the later groups): loaded at the top of k_final, long before the blocks need them
+__device__ __forceinline__ void block64_bias_load(const FinalArgs& A, uint32_t (*nbw)[130]) {
+    constexpr int GW = 65, BW = 2 * GW;
+    for (int i = threadIdx.x; i < 2 * BW; i += blockDim.x) {
+        const int f = i / BW, w = i % BW;
+        nbw[f][w] = __ldg(A.nbtab + (w < GW ? (f == 0 ? w : GW + w) : GW + (w - GW)));
+    }
+}
+
 template <int P>
 __device__ __forceinline__ void crt_convert_block64(const FinalArgs& A, const CrtConst& cc, const uint32_t* sm,
-                                                    uint32_t stride, int R, uint32_t pos0, bool sharded, bool fuse0) {
+                                                    uint32_t stride, int R, uint32_t pos0, bool sharded, bool fuse0,
+                                                    const uint32_t (*nbw)[130]) {
     static_assert(P <= 6, "five digits per pair of terms");
     constexpr int GW = 65, BW = 2 * GW;                  // words per group of 32 / block of 64 terms
-    __shared__ __align__(8) uint32_t nbw[2][BW];         // bias words of a row's first block / the later blocks
     __shared__ uint64_t seg_pub[32][3];                  // per warp: lane 31's d3, d4 of its last block; count + carry
     __shared__ uint64_t seg_hold[32][2];                 // per warp: the held-back first two digits of its segment
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int L = 1 << A.lgL, nblk = (L >> 6) + 1;       // + the virtual block that flushes the tail
     const int64_t W32 = A.W32;
-    for (int i = threadIdx.x; i < 2 * BW; i += blockDim.x) {
-        const int f = i / BW, w = i % BW;                // nbtab: GW words of the first group, GW of the later ones
-        nbw[f][w] = __ldg(A.nbtab + (w < GW ? (f == 0 ? w : GW + w) : GW + (w - GW)));
-    }
-    __syncthreads();
     const int wpr = nw > R ? nw / R : 1;                 // warps per row
     const int nseg = wpr < nblk ? wpr : nblk;            // segments per row: every one holds >= 1 block
     const int rstride = nw > R ? R : nw;
@@ -2901,6 +2906,9 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? TC_FINAL_MIN
     __syncthreads();
     if (!s_any) return;      // every row of this tile is zero padding
     const uint64_t fin_t0 = (A.prof && threadIdx.x == 0) ? gtimer() : 0;
+    __shared__ __align__(8) uint32_t s_nbw[2][130];      // crt_convert_block64's bias words
+    const bool use_co64 = !DUMP && P <= 6 && A.co64 && A.cw_aw == 2 && A.cw_b == 1 && A.prof == nullptr;
+    if (use_co64) block64_bias_load(A, s_nbw);           // visible after the transforms' barriers
 
     // all P tiles stream in at once (one cp.async group per prime); prime q's
     // transform waits only for its own tile, later primes' loads overlap it
@@ -3011,8 +3019,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT <= 256 ? TC_FINAL_MIN
     // warp-group CRT + ConvertOut (M = 32 AW + {0, 1}, host-checked shape)
     const bool warp_co = A.cw_aw > 0;
     if constexpr (!DUMP && P <= 6) {
-        if (A.co64 && A.cw_aw == 2 && A.cw_b == 1 && A.prof == nullptr) {
-            crt_convert_block64<P>(A, cc, sm, stride, R, pos0, sharded, fuse0);
+        if (use_co64) {
+            crt_convert_block64<P>(A, cc, sm, stride, R, pos0, sharded, fuse0, s_nbw);
             return;
         }
     }
