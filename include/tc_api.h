@@ -137,9 +137,12 @@ int tc_multiply(void* ctx,
                 uint64_t* out, int64_t rows, int32_t out_cw,
                 tc_times_t* times, int64_t* err_index);
 
-/* The end-to-end product from host buffers with transfers overlapped: B's
- * upload runs beside operand A's first pass, and the last pass runs in chunks
- * whose product rows are copied to the host while later chunks compute.  The
+/* The end-to-end product from host buffers with transfers overlapped: both
+ * operands go up in chunks (pageable sources through a pinned ring filled by a
+ * host copy pool), the first pass of the CTAs that read a chunk starts as it
+ * lands, operand A's forward passes run beside B's upload, and the last pass
+ * runs in chunks whose product rows are copied to the host while later chunks
+ * compute (tc/multiplier.py:131-181 end to end).  The
  * plan may be made from the declared bit widths (any plan whose capacity
  * covers the operands is exact); the real widths are reduced on the device
  * and returned in *info with the product's out_bits / out_cw.  `out` is a
