@@ -210,8 +210,19 @@ private:
     bool stop_ = false;
 };
 
-constexpr size_t kRingChunk = (size_t)16 << 20;   // bytes per ring slot
+constexpr size_t kRingChunk = (size_t)16 << 20;   // bytes per ring slot (allocation)
 constexpr int kRingSlots = 4;
+// bytes staged per copy (<= kRingChunk): TC_RING_CHUNK_MB for experiments
+size_t ring_piece() {
+    static const size_t v = [] {
+        const char* e = getenv("TC_RING_CHUNK_MB");
+        size_t mb = e && *e ? (size_t)atoi(e) : 16;
+        if (mb < 1) mb = 1;
+        if (mb > 16) mb = 16;
+        return mb << 20;
+    }();
+    return v;
+}
 
 bool host_is_pinned(const void* p) {
     cudaPointerAttributes at;
@@ -234,10 +245,11 @@ int stage_upload(Ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t 
         CK(cudaHostAlloc((void**)&c->ring, kRingChunk * kRingSlots, cudaHostAllocDefault));
         for (auto& e : c->ring_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    for (size_t off = 0; off < bytes; off += kRingChunk) {
+    const size_t piece = ring_piece();
+    for (size_t off = 0; off < bytes; off += piece) {
         const int slot = (int)(c->ring_next++ % kRingSlots);
-        char* sp = c->ring + (size_t)slot * kRingChunk;
-        const size_t len = bytes - off < kRingChunk ? bytes - off : kRingChunk;
+        char* sp = c->ring + (size_t)slot * piece;
+        const size_t len = bytes - off < piece ? bytes - off : piece;
         CK(cudaEventSynchronize(c->ring_ev[slot]));          // the copy that last read this slot is done
         CopyPool::get().copy(sp, static_cast<const char*>(src) + off, len);
         CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, sp, len, cudaMemcpyHostToDevice, st));
